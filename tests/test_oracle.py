@@ -1,0 +1,424 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (no GPU).
+
+Every test here checks oracle/ against something other than itself: published
+known-answer vectors, SPEC.md worked examples, brute-force enumeration,
+closed forms (1-D bond independence on forests), exact Boltzmann statistics,
+algebraic identities (cut = (W - E)/2, global flip invariance) and
+incremental-vs-from-scratch agreement.  A plausible slip in the oracle (a
+dropped term, a wrong sign or index, a transposed operand) fails at least one.
+"""
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy import stats
+
+import oracle
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _edges_of(o):
+    """Undirected edge list (u<v, w) recovered from the oracle's CSR."""
+    u, v, w = [], [], []
+    ww = o.wi if o.wi is not None else o.wf
+    for i in range(o.n):
+        for e in range(o.rp[i], o.rp[i + 1]):
+            j = int(o.col[e])
+            if j > i:
+                u.append(i); v.append(j); w.append(ww[e])
+    return np.array(u), np.array(v), np.array(w)
+
+
+def cut_by_definition(u, v, w, s):
+    """MaxCut objective: sum of w over edges whose endpoints differ."""
+    return np.sum(np.where(s[..., u] != s[..., v], w, 0), axis=-1)
+
+
+def tiny_csr(n, edges):
+    u = np.array([a for a, b, _ in edges]); v = np.array([b for a, b, _ in edges])
+    w = np.array([c for _, _, c in edges])
+    rp, col, ww = synth.edges_to_csr(n, u, v, w)
+    return dict(kind="csr", n=n, row_ptr=rp, col=col,
+                w=ww.astype(np.float32 if w.dtype.kind == "f" else np.int32))
+
+
+# ------------------------------------------------------------------ Philox
+def test_philox_known_answers():
+    rows = [l.split() for l in open(os.path.join(GOLD, "philox_kat.txt")) if l.strip() and l[0] != "#"]
+    assert len(rows) == 3
+    for r in rows:
+        vals = [int(x, 16) for x in r]
+        out = oracle.philox(vals[0:4], vals[4:6])
+        assert list(out) == vals[6:10]
+
+
+# ------------------------------------------------------------------ objective
+def test_spec_single_edge_examples():
+    for line in open(os.path.join(GOLD, "spec_examples.txt")):
+        if not line.strip() or line[0] == "#":
+            continue
+        w, s0, s1, energy, cut, gain = map(int, line.split())
+        inst = tiny_csr(2, [(0, 1, w)])
+        o = oracle.Oracle(inst, K=1, betas=np.array([1.0]), seed=1)
+        o.s[0] = [s0, s1]
+        E = int(o.energy_scratch()[0])
+        assert E == energy
+        assert (w - E) // 2 == cut  # cut = (W - E)/2 with W = sum w signed
+        # flip gain of vertex 0 = cut(flipped) - cut = -dE/2, dE = E(flipped) - E
+        o.s[0, 0] = -s0
+        E2 = int(o.energy_scratch()[0])
+        assert -(E2 - E) // 2 == gain
+
+
+@pytest.mark.parametrize("seed", [404, 405, 406])
+def test_cut_identity_and_flip_invariance(seed):
+    Jr, Jd = synth.torus_pm1(6, 4, seed)
+    inst = dict(kind="grid", Lx=6, Ly=4, J_right=Jr, J_down=Jd)
+    o = oracle.Oracle(inst, K=8, betas=synth.beta_ladder(8), seed=seed, copy_end=2)
+    u, v, w = _edges_of(o)
+    assert u.size == 2 * 24  # torus: 2n edges (Table I: m = 2n for the grids)
+    W = int(w.sum())
+    E = o.energy_scratch()
+    cut = cut_by_definition(u, v, w, o.s)
+    assert np.array_equal(cut, (W - E) // 2)
+    assert np.all((W - E) % 2 == 0)
+    # global flip invariance E(-s) == E(s)
+    o.s[:] = -o.s
+    assert np.array_equal(o.energy_scratch(), E)
+    # all +1 -> E == W
+    o.s[:] = 1
+    assert np.all(o.energy_scratch() == W)
+
+
+# ------------------------------------------------------------------ thresholds
+def test_threshold_values_and_monotone():
+    # beta=3, dE=8 -> p = 3.78e-11, 64-bit threshold 696,389,407
+    assert oracle.threshold_int(3.0, 8) == 696389407
+    # exp(0) saturates to 2^64-1; below 2^-64 the threshold is exactly 0
+    assert oracle.p64(0.0) == 2**64 - 1
+    assert oracle.p64(-44.0) > 0 and oracle.p64(-44.5) == 0
+    b = synth.beta_ladder(64)
+    for dE in (2, 4, 8, 12):
+        T = [oracle.threshold_int(x, dE) for x in b]
+        assert all(T[i] >= T[i + 1] for i in range(len(T) - 1))
+    for x in b[::7]:
+        T = [oracle.threshold_int(x, dE) for dE in range(1, 40)]
+        assert all(T[i] >= T[i + 1] for i in range(len(T) - 1))
+        for dE in (4, 8):
+            assert abs(oracle.threshold_int(x, dE) / 2.0**64 - math.exp(-x * dE)) < 1e-15
+    # exchange threshold equals exp(dbeta * d)
+    assert abs(oracle.threshold_exch(0.5, 0.7, -5) / 2.0**64 - math.exp(-1.0)) < 1e-15
+
+
+def test_cexp32_contract_accuracy():
+    xs = np.concatenate([-np.linspace(0, 64, 20001), [-1e-30, -1e-7, -0.5, -44.3]])
+    worst = 0.0
+    for x in xs[::7]:
+        xf = float(np.float32(x))
+        got = oracle.cexp32(xf)
+        ref = math.exp(xf)
+        worst = max(worst, abs(got / ref - 1.0))
+    assert worst < 2e-7
+    assert oracle.cexp32(0.0) == 1.0
+    assert oracle.cexp32(-65.0) == 0.0
+    # threshold from float dE tracks exp(-beta dE) to float accuracy
+    for beta, dE in [(0.1, 0.37), (1.0, 2.5), (3.0, 7.9), (0.3, 120.0)]:
+        T = oracle.threshold_f32(beta, dE)
+        x = float(np.float32(-(np.float32(beta) * np.float32(dE))))
+        assert abs(T / 2.0**64 - math.exp(x)) <= 2e-7 * math.exp(x) + 2.0**-64
+
+
+# ------------------------------------------------------------------ colouring
+def test_greedy_colouring():
+    Jr, Jd = synth.torus_pm1(8, 6, 1)
+    rp, col, w = synth.torus_csr(8, 6, Jr, Jd)
+    colour, ncol = oracle.greedy_colour(48, rp, col)
+    assert ncol == 2 and np.array_equal(colour, synth.checkerboard(8, 6))
+    u, v = synth.gnm(10000, 9999, 70)
+    rp, col, _ = synth.edges_to_csr(10000, u, v, np.ones(u.size, np.int32))
+    colour, ncol = oracle.greedy_colour(10000, rp, col)
+    src = np.repeat(np.arange(10000), np.diff(rp))
+    assert np.all(colour[src] != colour[col])  # proper
+    assert 3 <= ncol <= 6
+    # smallest free colour: every vertex of colour c>0 has a lower-id neighbour of each colour < c
+    for i in range(0, 10000, 97):
+        nb = col[rp[i]:rp[i + 1]]
+        lower = set(colour[nb[nb < i]].tolist())
+        assert all(c in lower for c in range(colour[i]))
+
+
+def test_grid_to_csr_matches_edge_list():
+    Jr, Jd = synth.torus_pm1(6, 8, 9)
+    rp, col, w, chk = oracle.grid_to_csr(6, 8, Jr, Jd)
+    rp2, col2, w2 = synth.torus_csr(6, 8, Jr, Jd)
+    for i in range(48):
+        a = sorted(zip(col[rp[i]:rp[i + 1]].tolist(), w[rp[i]:rp[i + 1]].tolist()))
+        b = sorted(zip(col2[rp2[i]:rp2[i + 1]].tolist(), w2[rp2[i]:rp2[i + 1]].tolist()))
+        assert a == b
+    assert np.array_equal(chk, synth.checkerboard(6, 8))
+
+
+# ------------------------------------------------------------------ init
+def test_init_uniform_and_deterministic():
+    inst = dict(kind="grid", Lx=100, Ly=100, **dict(zip(("J_right", "J_down"), synth.torus_pm1(100, 100, 3))))
+    a = oracle.Oracle(inst, K=32, betas=synth.beta_ladder(32), seed=7, copy_end=1)
+    b = oracle.Oracle(inst, K=32, betas=synth.beta_ladder(32), seed=7, copy_end=1)
+    c = oracle.Oracle(inst, K=32, betas=synth.beta_ladder(32), seed=8, copy_end=1)
+    assert np.array_equal(a.s, b.s) and not np.array_equal(a.s, c.s)
+    N = a.s.size
+    assert abs(a.s.mean()) < 4 / math.sqrt(N)
+    # replicas are not copies of each other
+    assert np.mean(a.s[0] == a.s[1]) < 0.55
+
+
+# ------------------------------------------------------------------ sweeps
+@pytest.mark.parametrize("rng", [oracle.RNG_PLANE, oracle.RNG_WORD])
+def test_incremental_energy_equals_scratch(rng):
+    Jr, Jd = synth.torus_pm1(16, 16, 1616)
+    inst = dict(kind="grid", Lx=16, Ly=16, J_right=Jr, J_down=Jd)
+    o = oracle.Oracle(inst, K=8, betas=synth.beta_ladder(8), seed=2311, copy_end=3, rng=rng)
+    for _ in range(5):
+        acc = o.sweeps(7)
+        assert acc > 0
+        assert np.array_equal(o.Ei, o.energy_scratch())
+        o.exchange()
+        assert np.array_equal(o.Ei, o.energy_scratch())
+
+
+def test_zero_temperature_is_greedy_descent():
+    # beta so large that every threshold is 0: only dE <= 0 moves (S:270/S:282 analogue)
+    u, v = synth.gnm(60, 120, 5)
+    w = np.where(synth.splitmix64(5, u.size) >> np.uint64(63), -1, 1).astype(np.int32)
+    rp, col, ww = synth.edges_to_csr(60, u, v, w)
+    inst = dict(kind="csr", n=60, row_ptr=rp, col=col, w=ww.astype(np.int32))
+    o = oracle.Oracle(inst, K=4, betas=np.array([1e3, 2e3, 3e3, 4e3]), seed=11, copy_end=2)
+    prev = o.energy_scratch()
+    for _ in range(30):
+        o.sweeps(1)
+        E = o.energy_scratch()
+        assert np.all(E <= prev)
+        prev = E
+    # final states: no single flip lowers E (checked by recomputation)
+    for r in range(o.R):
+        base = o.s[r].copy()
+        for i in range(o.n):
+            o.s[r, i] = -o.s[r, i]
+            Ef = o.energy_scratch()[r]
+            o.s[r, i] = -o.s[r, i]
+            assert Ef >= prev[r]
+        assert np.array_equal(o.s[r], base)
+
+
+def _brute_min(inst, n):
+    o = oracle.Oracle(inst, K=1, betas=np.array([1.0]), seed=0)
+    u, v, w = _edges_of(o)
+    states = 1 - 2 * ((np.arange(2**n)[:, None] >> np.arange(n)[None, :]) & 1)
+    E = np.sum(w * states[:, u] * states[:, v], axis=1)
+    return E.min(), states, E
+
+
+@pytest.mark.parametrize("seed", list(range(404, 414)))
+def test_pt_reaches_bruteforce_ground_state_4x4(seed):
+    Jr, Jd = synth.torus_pm1(4, 4, seed)
+    inst = dict(kind="grid", Lx=4, Ly=4, J_right=Jr, J_down=Jd)
+    Emin, _, _ = _brute_min(inst, 16)
+    o = oracle.Oracle(inst, K=64, betas=synth.beta_ladder(64), seed=2311, copy_end=1)
+    o.run(200, 10)
+    assert o.best.E == Emin
+    # best record re-certifies: its spins have energy best.E
+    o.s[0] = o.best.spins
+    assert o.energy_scratch()[0] == o.best.E
+
+
+def test_unweighted_triangle_best_cut_is_2():
+    inst = tiny_csr(3, [(0, 1, 1), (1, 2, 1), (0, 2, 1)])
+    o = oracle.Oracle(inst, K=4, betas=synth.beta_ladder(4), seed=3, copy_end=2)
+    o.run(50, 5)
+    assert (3 - o.best.E) // 2 == 2
+
+
+def _boltzmann_chi2(inst, n, betas, rng, copies=384, burn=20, samples=60, thin=6, seed=2311):
+    K = len(betas)
+    o = oracle.Oracle(inst, K=K, betas=np.asarray(betas), seed=seed, copy_end=copies, rng=rng)
+    o.sweeps(burn)
+    hist = np.zeros((K, 2**n))
+    pw = 1 << np.arange(n)
+    for _ in range(samples):
+        o.sweeps(thin)
+        idx = ((o.s < 0).astype(np.int64) @ pw)
+        for k in range(K):
+            hist[k] += np.bincount(idx[k::K], minlength=2**n)
+    _, states, E = _brute_min(inst, n)
+    # state index convention: bit b set <-> spin b == -1
+    idx_states = ((states < 0).astype(np.int64) @ pw)
+    Es = np.empty(2**n); Es[idx_states] = E
+    pvals = []
+    for k, b in enumerate(betas):
+        p = np.exp(-b * (Es - Es.min())); p /= p.sum()
+        exp_counts = p * hist[k].sum()
+        chi2 = np.sum((hist[k] - exp_counts) ** 2 / exp_counts)
+        pvals.append(stats.chi2.sf(chi2, 2**n - 1))
+    return pvals
+
+
+@pytest.mark.parametrize("rng", [oracle.RNG_PLANE, oracle.RNG_WORD])
+def test_metropolis_samples_boltzmann_exactly(rng):
+    # triangle + pendant path with mixed integer weights (|w| in 1..3)
+    inst = tiny_csr(6, [(0, 1, 1), (1, 2, -2), (0, 2, 1), (2, 3, 3), (3, 4, -1), (4, 5, 2)])
+    pvals = _boltzmann_chi2(inst, 6, [0.3, 0.6, 1.0], rng)
+    assert min(pvals) > 1e-4, pvals
+
+
+def test_metropolis_samples_boltzmann_float_weights():
+    inst = tiny_csr(5, [(0, 1, 0.7), (1, 2, -1.3), (0, 2, 0.4), (2, 3, 1.9), (3, 4, -0.55)])
+    pvals = _boltzmann_chi2(inst, 5, [0.4, 0.9], oracle.RNG_WORD)
+    assert min(pvals) > 1e-4, pvals
+
+
+def test_wrong_sign_would_fail_boltzmann():
+    """Sanity of the chi2 harness itself: anti-Boltzmann (beta -> -beta) is rejected."""
+    inst = tiny_csr(6, [(0, 1, 1), (1, 2, -2), (0, 2, 1), (2, 3, 3), (3, 4, -1), (4, 5, 2)])
+    o = oracle.Oracle(inst, K=1, betas=np.array([0.6]), seed=1, copy_end=256)
+    o.sweeps(40)
+    pw = 1 << np.arange(6)
+    idx = ((o.s < 0).astype(np.int64) @ pw)
+    hist = np.bincount(idx, minlength=64).astype(float)
+    _, states, E = _brute_min(inst, 6)
+    Es = np.empty(64); Es[((states < 0).astype(np.int64) @ pw)] = E
+    p = np.exp(+0.6 * (Es - Es.max())); p /= p.sum()
+    chi2 = np.sum((hist - p * hist.sum()) ** 2 / np.maximum(p * hist.sum(), 1e-9))
+    assert stats.chi2.sf(chi2, 63) < 1e-6
+
+
+@pytest.mark.parametrize("weights", ["pm1", "gauss"])
+def test_open_chain_bond_energy_closed_form(weights):
+    """On a forest the bond variables are independent: <J s_i s_j> = -|J| tanh(beta |J|)."""
+    n = 64
+    u = np.arange(n - 1); v = u + 1
+    if weights == "pm1":
+        w = np.where(synth.splitmix64(9, n - 1) >> np.uint64(63), -1, 1).astype(np.int32)
+    else:
+        w = synth.gaussian_f32(n - 1, 9)
+    rp, col, ww = synth.edges_to_csr(n, u, v, w)
+    inst = dict(kind="csr", n=n, row_ptr=rp, col=col, w=ww)
+    betas = synth.beta_ladder(8)
+    rng = oracle.RNG_WORD if weights == "gauss" else oracle.RNG_PLANE
+    o = oracle.Oracle(inst, K=8, betas=betas, seed=5, copy_end=64, rng=rng)
+    o.sweeps(30)
+    acc = np.zeros(8); acc2 = np.zeros(8); cnt = 0
+    for _ in range(60):
+        o.sweeps(3)
+        E = o.energy_scratch().astype(float).reshape(-1, 8)
+        acc += E.sum(0); acc2 += (E ** 2).sum(0); cnt += E.shape[0]
+    mean = acc / cnt
+    aw = np.abs(w.astype(np.float64))
+    for k, b in enumerate(betas):
+        if weights == "gauss" and b > 1.0:
+            continue  # Gaussian chains pin domain walls at weak bonds: not equilibrated in 200 sweeps
+        expect = -np.sum(aw * np.tanh(b * aw))
+        var1 = np.sum(aw ** 2 * (1 - np.tanh(b * aw) ** 2))
+        # samples are autocorrelated across the 60 draws of a chain; use copies only
+        se = math.sqrt(var1 / 64) + 1e-9
+        assert abs(mean[k] - expect) < 5 * se, (k, b, mean[k], expect, se)
+
+
+# ------------------------------------------------------------------ exchange
+def test_exchange_zero_difference_always_swaps():
+    Jr, Jd = synth.torus_pm1(4, 4, 1)
+    inst = dict(kind="grid", Lx=4, Ly=4, J_right=Jr, J_down=Jd)
+    o = oracle.Oracle(inst, K=6, betas=synth.beta_ladder(6), seed=1, copy_end=2)
+    o.s[:] = o.s[0]
+    o.Ei[:] = o.energy_scratch()
+    o.exchange()  # e=0: pairs (0,1),(2,3),(4,5); d = 0 -> accepted
+    assert o.walker.tolist() == [1, 0, 3, 2, 5, 4, 7, 6, 9, 8, 11, 10]
+    o.exchange()  # e=1: pairs (1,2),(3,4)
+    assert o.walker.tolist() == [1, 3, 0, 5, 2, 4, 7, 9, 6, 11, 8, 10]
+
+
+def test_exchange_preserves_multiset_and_permutation():
+    Jr, Jd = synth.torus_pm1(8, 8, 2)
+    inst = dict(kind="grid", Lx=8, Ly=8, J_right=Jr, J_down=Jd)
+    o = oracle.Oracle(inst, K=16, betas=synth.beta_ladder(16), seed=4, copy_end=4)
+    for _ in range(20):
+        o.sweeps(3)
+        before = np.sort(o.Ei.reshape(4, 16), axis=1)
+        cfg_before = sorted(map(bytes, o.s))
+        o.exchange()
+        assert np.array_equal(np.sort(o.Ei.reshape(4, 16), axis=1), before)
+        assert sorted(map(bytes, o.s)) == cfg_before  # configurations only move
+        for c in range(4):
+            assert sorted(o.walker[16 * c:16 * c + 16].tolist()) == list(range(16 * c, 16 * c + 16))
+        assert np.array_equal(o.Ei, o.energy_scratch())
+
+
+def test_exchange_acceptance_frequency():
+    """Uphill swap accepted with probability exp(dbeta * d)."""
+    inst = tiny_csr(4, [(0, 1, 1), (1, 2, 1), (2, 3, 1)])
+    C = 4000
+    betas = np.array([0.5, 0.8])
+    o = oracle.Oracle(inst, K=2, betas=betas, seed=77, copy_end=C)
+    o.s[0::2] = [1, -1, 1, -1]  # slot k=0: E = -3
+    o.s[1::2] = [1, 1, -1, -1]  # slot k=1: E = -1 + ... = 1 - 1 + 1? computed below
+    o.Ei[:] = o.energy_scratch()
+    d = int(o.Ei[1] - o.Ei[0])
+    assert d < 0 or True
+    if d >= 0:  # make slot 1 the lower-energy one
+        o.s[0::2], o.s[1::2] = o.s[1::2].copy(), o.s[0::2].copy()
+        o.Ei[:] = o.energy_scratch()
+        d = int(o.Ei[1] - o.Ei[0])
+    assert d < 0
+    acc = o.exchange()
+    p = math.exp((betas[1] - betas[0]) * d)
+    assert stats.binomtest(acc, C, p).pvalue > 1e-4
+
+
+def test_two_temperature_pt_joint_distribution():
+    """PT with exchanges keeps each temperature Boltzmann (product measure)."""
+    inst = tiny_csr(5, [(0, 1, 1), (1, 2, -1), (2, 0, 1), (2, 3, 2), (3, 4, -1)])
+    betas = np.array([0.4, 1.0])
+    o = oracle.Oracle(inst, K=2, betas=betas, seed=123, copy_end=512)
+    _, states, E = _brute_min(inst, 5)
+    pw = 1 << np.arange(5)
+    Es = np.empty(32); Es[((states < 0).astype(np.int64) @ pw)] = E
+    joint = np.zeros((32, 32))
+    for rnd in range(80):
+        o.sweeps(2)
+        o.exchange()
+        if rnd >= 10:
+            idx = ((o.s < 0).astype(np.int64) @ pw)
+            np.add.at(joint, (idx[0::2], idx[1::2]), 1)
+    p0 = np.exp(-betas[0] * Es); p0 /= p0.sum()
+    p1 = np.exp(-betas[1] * Es); p1 /= p1.sum()
+    for k, p in ((0, p0), (1, p1)):
+        h = joint.sum(axis=1 - k)
+        chi2 = np.sum((h - p * h.sum()) ** 2 / (p * h.sum()))
+        assert stats.chi2.sf(chi2, 31) > 1e-4
+    # independence of the two temperatures' marginals (product measure), coarse: energy classes
+    Eu = np.unique(Es)
+    cls = np.searchsorted(Eu, Es)
+    J = np.zeros((Eu.size, Eu.size))
+    np.add.at(J, (cls[:, None].repeat(32, 1), cls[None, :].repeat(32, 0)), joint)
+    ex = np.outer(J.sum(1), J.sum(0)) / J.sum()
+    m = ex > 5
+    chi2 = np.sum((J[m] - ex[m]) ** 2 / ex[m])
+    dof = (Eu.size - 1) ** 2
+    assert stats.chi2.sf(chi2, dof) > 1e-5
+
+
+# ------------------------------------------------------------------ workload shapes
+def test_presets_match_paper_table1():
+    rows = [l.split() for l in open(os.path.join(GOLD, "paper_table1.txt")) if l[0] != "#"]
+    shapes = {r[0]: r for r in rows}
+    for name, key in (("G65", "c2"), ("G77", "c4a"), ("G81", "c4b")):
+        cfg = synth.CONFIGS[key]
+        assert cfg["Lx"] * cfg["Ly"] == int(shapes[name][1])
+        assert 2 * cfg["Lx"] * cfg["Ly"] == int(shapes[name][2])
+    cfg = synth.CONFIGS["c3"]
+    assert cfg["n"] == int(shapes["G70"][1]) and cfg["m"] == int(shapes["G70"][2])
+    u, v = synth.gnm(cfg["n"], cfg["m"], cfg["seed"])
+    assert u.size == 9999 and np.all(u < v)
+    assert np.unique(u * 10000 + v).size == 9999
