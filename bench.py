@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: replica-parallel Metropolis sweeps + parallel tempering.
+
+Metric (BASELINE.json): spin-flip attempts/s (attempts = n x replicas x sweeps, every
+site of every replica counted once per sweep) at N GPUs, plus the
+fraction of the roofline of the dominant kernel.
+
+Workload at N=1 (BASELINE.json configs[1], the metric's config): 80x100 +-1 torus
+(G65 shape, Table I), 64 temperatures x 64 copies = 4096 replicas, beta
+0.1-3.0 geometric, 10,000 sweeps with a replica exchange every 10 sweeps, bit-packed
+spins.  One step = that whole schedule (1,000 rounds of 10 sweeps + best check +
+exchange) on inputs already resident on the GPU.  N>1: weak scaling -- every rank
+runs its own 64-copy shard (distinct global copy ids), local exchanges, and one NCCL
+all-gather of the per-rank best records per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4a|c4b|c1|c5]
+    python bench.py --impl reference ...   # the CPU oracle on the host cores
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+PROFILE_FILE = os.path.join(ROOT, "profiles", "inst_per_attempt.json")
+
+WORKLOADS = {
+    "c1": "16x16 +-1 torus, 64 temps x 1 copy, 1000 sweeps, exchange every 10, int8 spins",
+    "c2": "80x100 +-1 torus (G65 shape), 64 temps x 64 copies = 4096 replicas, beta 0.1-3.0 "
+          "geometric, 10000 sweeps, exchange every 10, bit-packed spins",
+    "c3": "G(10000, 9999) unweighted MaxCut (J=+1, G70 shape), greedy colouring, 64 temps x 64 "
+          "copies, 10000 sweeps, exchange every 10, bit-packed spins",
+    "c4a": "100x140 +-1 torus (G77 shape), 128 temps x 128 copies, exchange every 10, bit-packed",
+    "c4b": "100x200 +-1 torus (G81 shape), 128 temps x 128 copies, exchange every 10, bit-packed",
+    "c5": "random 3-regular, 4e6 vertices, N(0,1) float32 couplings, 256 replicas/GPU, 1000 "
+          "sweeps, int8 spins",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sweeps", type=int, default=0, help="override sweeps per step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--threads", type=int, default=0, help="CTA size override")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload_params(name, sweeps_override):
+    cfg = dict(synth.CONFIGS[name])
+    if sweeps_override:
+        cfg["sweeps"] = sweeps_override
+    return cfg
+
+
+def json_line(d):
+    print(json.dumps(d), flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], [], set()
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                "sw_power_cap"), f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------ reference (oracle) arm
+def cpu_oracle_sample(cfg, target_s=12.0):
+    """The CPU oracle as it stands, one thread per copy on the host cores, on a bounded
+    sample of the workload: `threads` copies x S sweeps (S sized for ~target_s)."""
+    import oracle
+    inst = synth.make_instance(cfg)
+    K = cfg["K"]
+    betas = synth.beta_ladder(K)
+    cores = os.cpu_count() or 1
+    threads = max(1, min(cores, cfg["C"], 16))
+    n = inst["n"]
+    kex = cfg["k_ex"] if cfg["k_ex"] > 0 else 0
+    rng = oracle.RNG_PLANE if cfg["layout"] == "bits" else oracle.RNG_WORD
+    # calibrate on one copy x 2 sweeps
+    t0 = time.perf_counter()
+    if cfg["C"] == 1 and cfg["K"] > 64:
+        o = oracle.Oracle(inst, K, betas, synth.PHILOX_KEY, 0, 1, rng=rng, slots=(0, 4))
+        o.sweeps(1)
+        per = (time.perf_counter() - t0) / (4 * n)
+    else:
+        o = oracle.Oracle(inst, K, betas, synth.PHILOX_KEY, 0, 1, rng=rng)
+        o.sweeps(2)
+        per = (time.perf_counter() - t0) / (2 * K * n)
+    if cfg["C"] == 1 and cfg["K"] > 64:
+        # replica sample (no exchange): `threads` slots per thread-run
+        import threading
+        reps = threads * 2
+        sweeps = max(1, int(target_s * threads / (per * n * reps)))
+        res = []
+
+        def work(q):
+            oo = oracle.Oracle(inst, K, betas, synth.PHILOX_KEY, 0, 1, rng=rng, slots=(2 * q, 2 * q + 2))
+            oo.sweeps(sweeps)
+            res.append(oo)
+        t0 = time.perf_counter()
+        ts = [threading.Thread(target=work, args=(q,)) for q in range(threads)]
+        [t.start() for t in ts]
+        [t.join() for t in ts]
+        dt = time.perf_counter() - t0
+        attempts = n * reps * sweeps
+        sample = f"{reps} replicas x {sweeps} sweeps of the {cfg['kind']} instance (no exchange)"
+    else:
+        sweeps = max(kex or 1, int(target_s * threads / (per * n * K * threads)))
+        if kex:
+            sweeps = max(kex, (sweeps // kex) * kex)
+        t0 = time.perf_counter()
+        oracle.run_sharded(inst, K, betas, synth.PHILOX_KEY, 0, threads, sweeps, kex, rng=rng,
+                           threads=threads)
+        dt = time.perf_counter() - t0
+        attempts = n * K * threads * sweeps
+        sample = f"{threads} copies x {K} temps x {sweeps} sweeps (exchange every {kex})"
+    return {"value": attempts / dt, "unit": "attempts/s", "cores": threads, "kind": "oracle",
+            "sample": sample, "seconds": round(dt, 2), "host_cores_available": cores}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = workload_params(args.workload, args.sweeps)
+    vals = []
+    for s in range(args.warmup + args.steps):
+        r = cpu_oracle_sample(cfg, target_s=4.0)
+        if s >= args.warmup:
+            vals.append(r)
+    v = float(np.median([r["value"] for r in vals]))
+    cb = dict(vals[-1])
+    cb["value"] = v
+    json_line({
+        "impl": "reference", "metric": "spin-flip attempts/s", "value": v, "unit": "attempts/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": float(np.median([r["seconds"] for r in vals]) * 1e3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int8 spins / int64 energies (scalar C)", "data": "synthetic",
+        "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
+                   "note": "CPU oracle on host cores, bounded sample per step"},
+        "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": "attempts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    })
+
+
+# ------------------------------------------------------------------ our arm
+def roofline_entry(kernel_ms, attempts_per_launch, layout, clocks):
+    """Roofline of the dominant kernel.  Bit-packed sweeps are issue (ALU) bound: achieved
+    = warp instructions per launch (ncu-measured per attempt, profiles/inst_per_attempt.json,
+    times the live attempts per launch) / live CUDA-event launch time; peak = 148 SMs x 4
+    schedulers x 1 warp-instruction/cycle x max SM clock."""
+    peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
+    mhz = peaks.get("sm_max_mhz", 1965.0)
+    ipa = None
+    if os.path.exists(PROFILE_FILE):
+        ipa = json.load(open(PROFILE_FILE)).get(layout)
+    if layout == "i8":
+        # int8 per-lane sweeps: HBM bound; algorithmic bytes per attempt stated in DESIGN.md
+        bpa = ipa.get("alg_bytes_per_attempt", 5.11) if ipa else 5.11
+        ach = attempts_per_launch * bpa / (kernel_ms * 1e-3) / 1e9
+        peak = peaks.get("hbm_gbs", 6551.4)
+        return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": (ipa or {}).get("dram_bytes_per_attempt") and
+                ipa["dram_bytes_per_attempt"] * attempts_per_launch,
+                "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)"}
+    peak = 148 * 4 * mhz * 1e6 / 1e9  # Ginst/s (warp instructions)
+    if not ipa:
+        return {"bound": "alu", "achieved": None, "peak": peak, "unit": "Ginst/s", "frac": None,
+                "traffic": None, "note": "no ncu instruction count committed yet"}
+    ach = attempts_per_launch * ipa["warp_inst_per_attempt"] / (kernel_ms * 1e-3) / 1e9
+    traffic = ipa.get("dram_bytes_per_attempt")
+    return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "Ginst/s", "frac": ach / peak,
+            "traffic": traffic * attempts_per_launch if traffic is not None else None,
+            "peak_source": f"derived: 148 SMs x 4 issue/cycle x {mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+            "inst_per_attempt_source": ipa.get("source")}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_09275_b200 import Engine
+    from paper_2311_09275_b200.driver import merge_best_over_ranks
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = workload_params(args.workload, args.sweeps)
+    inst = synth.make_instance(cfg)
+    K, C = cfg["K"], cfg["C"]
+    betas = synth.beta_ladder(K)
+    Cg = C * world  # weak scaling: every rank runs a C-copy shard with distinct global ids
+    stream = torch.cuda.current_stream()
+    eng = Engine(inst, K, Cg, betas, seed=synth.PHILOX_KEY, copy_begin=rank * C,
+                 copy_end=(rank + 1) * C, layout=cfg["layout"], device=local,
+                 block_threads=args.threads, stream=stream.cuda_stream)
+    n, R = inst["n"], eng.R
+    sweeps, kex = cfg["sweeps"], cfg["k_ex"]
+    rounds = sweeps // kex if kex > 0 else 0
+    rem = sweeps - rounds * kex if kex > 0 else sweeps
+    attempts_step = n * R * sweeps
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    def step(kev=None):
+        launches = 0
+        for _ in range(rounds):
+            if kev is not None:
+                kev.append((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)))
+                kev[-1][0].record(stream)
+            eng.sweep(kex)
+            if kev is not None:
+                kev[-1][1].record(stream)
+            eng.exchange()
+            launches += 3
+        if rem:
+            if kev is not None:
+                kev.append((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)))
+                kev[-1][0].record(stream)
+            eng.sweep(rem)
+            if kev is not None:
+                kev[-1][1].record(stream)
+            eng.check_best()
+            launches += 2 if cfg["layout"] == "bits" else 1 + rem * eng.info.n_colours + 2
+        if cfg["layout"] == "i8" and rounds:
+            launches += rounds * (kex * eng.info.n_colours + 2 - 1)
+        rec = eng.best(spins=False)
+        if world > 1:
+            rec = merge_best_over_ranks(rec, None)
+        return launches, rec
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    total_ms, kernel_ms, nk, launches = 0.0, 0.0, 0, 0
+    clocks.start()
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the timed events)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        kev = []
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        nl, rec = step(kev)
+        b.record(stream)
+        torch.cuda.synchronize()
+        launches += nl
+        total_ms += a.elapsed_time(b)
+        kernel_ms += sum(x.elapsed_time(y) for x, y in kev)
+        nk += len(kev)
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = attempts_step * world * args.steps / (total_ms * 1e-3)
+    ms_step = total_ms / args.steps
+    avg_launch_ms = kernel_ms / max(nk, 1)
+    per_launch_attempts = n * R * (kex if kex > 0 else sweeps)
+    roof = roofline_entry(avg_launch_ms, per_launch_attempts, cfg["layout"], clk)
+    roof["kernel"] = "k_grid_bits" if (inst["kind"] == "grid" and cfg["layout"] == "bits") else \
+        ("k_csr_bits" if cfg["layout"] == "bits" else "k_csr_i8_phase")
+    roof["kernel_share_of_step"] = kernel_ms / max(total_ms * (1 if world == 1 else 1), 1e-9)
+    roof["avg_launch_ms"] = avg_launch_ms
+
+    # ---- end to end through the public API with host buffers, every step
+    e2e = None
+    if not args.no_e2e:
+        e2e_ms = 0.0
+        h2d = d2h = 0
+        Jr = torch.from_numpy(inst["J_right"]).pin_memory() if inst["kind"] == "grid" else None
+        for s in range(args.steps + 1):
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            e = Engine(inst, K, Cg, betas, seed=synth.PHILOX_KEY + s, copy_begin=rank * C,
+                       copy_end=(rank + 1) * C, layout=cfg["layout"], device=local,
+                       block_threads=args.threads, stream=stream.cuda_stream)
+            for _ in range(rounds):
+                e.sweep(kex)
+                e.exchange()
+            if rem:
+                e.sweep(rem)
+                e.check_best()
+            rec = e.best(spins=True)
+            E = e.energies()
+            b.record(stream)
+            torch.cuda.synchronize()
+            e.close()
+            if s > 0:  # first iteration warms the allocator
+                e2e_ms += a.elapsed_time(b)
+        if inst["kind"] == "grid":
+            h2d = 2 * n + 8 * K
+        else:
+            h2d = 8 * (n + 1) + inst["col"].nbytes + inst["w"].nbytes + 8 * K
+        d2h = 8 * R + n + 32
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": attempts_step * world * args.steps / (float(t.item()) * 1e-3),
+               "unit": "attempts/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "includes": "create (validate, tables, upload, init) + full schedule + best/energy readback"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_oracle_sample(cfg)
+
+    if rank == 0:
+        peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
+        bpa = 0.25 if cfg["layout"] == "bits" else 5.11
+        json_line({
+            "metric": "spin-flip attempts/s", "value": value, "unit": "attempts/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32" if cfg["layout"] == "bits" else ("f32" if cfg["kind"] == "regular" else "int32"),
+            "data": "synthetic",
+            "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
+                       "n": n, "replicas_per_gpu": R, "sweeps_per_step": sweeps, "exchange_every": kex,
+                       "parallelism": f"copies sharded over {world} GPU(s), weak scaling",
+                       "l2": "flushed between timed steps (state is SMEM/L2-resident by design)"},
+            "roofline": roof,
+            "hbm_frac": value / world * bpa / 1e9 / peaks.get("hbm_gbs", 6551.4),
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "best": {k: rec[k] for k in ("E", "slot", "sweep")},
+        })
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

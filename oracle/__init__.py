@@ -41,7 +41,8 @@ class _Run(C.Structure):
     _fields_ = [("n", C.c_int32), ("rp", C.c_void_p), ("col", C.c_void_p), ("wi", C.c_void_p),
                 ("wf", C.c_void_p), ("colour", C.c_void_p), ("ncol", C.c_int32),
                 ("seed", C.c_uint64), ("K", C.c_int32), ("copy_begin", C.c_int32),
-                ("copy_end", C.c_int32), ("beta", C.c_void_p), ("rng", C.c_int32)]
+                ("copy_end", C.c_int32), ("beta", C.c_void_p), ("rng", C.c_int32),
+                ("slot_lo", C.c_int64), ("slot_hi", C.c_int64)]
 
 
 def lib():
@@ -156,6 +157,7 @@ class Oracle:
     copy_end: int = 1
     rng: int = RNG_PLANE
     colour: np.ndarray | None = None
+    slots: tuple | None = None  # (lo, hi) global slot subset (no exchange), else whole copies
     t: int = 0
     e: int = 0
     best: Best = field(default_factory=Best)
@@ -184,8 +186,11 @@ class Oracle:
         self.ncol = int(self.colour.max()) + 1
         self.betas = np.ascontiguousarray(self.betas, np.float64)
         assert self.betas.size == self.K
-        self.R = (self.copy_end - self.copy_begin) * self.K
-        self.slot0 = self.copy_begin * self.K
+        if self.slots is not None:
+            self.slot0, self.R = int(self.slots[0]), int(self.slots[1] - self.slots[0])
+        else:
+            self.R = (self.copy_end - self.copy_begin) * self.K
+            self.slot0 = self.copy_begin * self.K
         self.s = np.zeros((self.R, self.n), np.int8)
         self.Ei = np.zeros(self.R, np.int64)
         self.walker = np.arange(self.slot0, self.slot0 + self.R, dtype=np.int64)
@@ -193,7 +198,8 @@ class Oracle:
                          _p(self.wi).value if self.wi is not None else None,
                          _p(self.wf).value if self.wf is not None else None,
                          _p(self.colour).value, self.ncol, self.seed & (2**64 - 1), self.K,
-                         self.copy_begin, self.copy_end, _p(self.betas).value, self.rng)
+                         self.copy_begin, self.copy_end, _p(self.betas).value, self.rng,
+                         self.slots[0] if self.slots else 0, self.slots[1] if self.slots else 0)
         lib().or_init(C.byref(self._run), _p(self.s))
         self.Ei[:] = self.energy_scratch() if self.wi is not None else 0
 
@@ -227,6 +233,8 @@ class Oracle:
     def exchange(self) -> int:
         if self.is_float:
             raise ValueError("exchange requires integer weights")
+        if self.slots is not None:
+            raise ValueError("slot subsets cannot exchange")
         acc = 0
         if self.K >= 2:
             acc = lib().or_exchange(C.byref(self._run), _p(self.s), _p(self.Ei), _p(self.walker),

@@ -206,15 +206,28 @@ typedef struct {
     int32_t copy_end;
     const double *beta; /* K, strictly increasing */
     int32_t rng;        /* RNG_PLANE or RNG_WORD */
+    int64_t slot_lo;    /* if slot_hi > slot_lo: simulate only global slots [slot_lo, slot_hi) */
+    int64_t slot_hi;    /*   (replicas are independent without exchange; no or_exchange then) */
 } or_run;
+
+static int64_t run_slot0(const or_run *R)
+{
+    return R->slot_hi > R->slot_lo ? R->slot_lo : (int64_t)R->copy_begin * R->K;
+}
+
+static int64_t run_nrep(const or_run *R)
+{
+    return R->slot_hi > R->slot_lo ? R->slot_hi - R->slot_lo
+                                   : (int64_t)(R->copy_end - R->copy_begin) * R->K;
+}
 
 /* Initial configuration ("uniform independent spins"):
  * s(r,i) = -1 iff bit (r & 31) of word 0 of Philox(i, 0, r>>5, INIT<<24). */
 void or_init(const or_run *R, int8_t *s)
 {
     int32_t n = R->n;
-    int64_t slot0 = (int64_t)R->copy_begin * R->K;
-    int64_t nrep = (int64_t)(R->copy_end - R->copy_begin) * R->K;
+    int64_t slot0 = run_slot0(R);
+    int64_t nrep = run_nrep(R);
     for (int64_t rl = 0; rl < nrep; ++rl) {
         int64_t r = slot0 + rl;
         for (int32_t i = 0; i < n; ++i) {
@@ -231,7 +244,7 @@ void or_init(const or_run *R, int8_t *s)
 void or_energy(const or_run *R, const int8_t *s, int64_t *Ei, double *Ef)
 {
     int32_t n = R->n;
-    int64_t nrep = (int64_t)(R->copy_end - R->copy_begin) * R->K;
+    int64_t nrep = run_nrep(R);
     for (int64_t rl = 0; rl < nrep; ++rl) {
         const int8_t *sr = s + rl * n;
         int64_t ei = 0;
@@ -293,8 +306,8 @@ static uint64_t word_u64(uint64_t seed, uint32_t i, uint32_t t, int64_t r)
 int64_t or_sweeps(const or_run *R, int8_t *s, int64_t *Ei, uint32_t t0, int32_t nsweeps)
 {
     int32_t n = R->n;
-    int64_t slot0 = (int64_t)R->copy_begin * R->K;
-    int64_t nrep = (int64_t)(R->copy_end - R->copy_begin) * R->K;
+    int64_t slot0 = run_slot0(R);
+    int64_t nrep = run_nrep(R);
     uint32_t planes[64];
     int64_t accepted = 0;
     for (int32_t ts = 0; ts < nsweeps; ++ts) {
@@ -371,6 +384,8 @@ int64_t or_exchange(const or_run *R, int8_t *s, int64_t *Ei, int64_t *walker, ui
     int32_t n = R->n;
     int32_t K = R->K;
     int64_t acc = 0;
+    if (R->slot_hi > R->slot_lo)
+        return -1; /* slot subsets carry no complete PT ladder */
     int8_t *tmp = (int8_t *)malloc((size_t)n);
     for (int32_t c = R->copy_begin; c < R->copy_end; ++c) {
         for (int32_t k = (int32_t)(e % 2u); k + 1 < K; k += 2) {

@@ -1,0 +1,1056 @@
+// abi.cu -- host runtime and C ABI of libising.so (see include/ising.h).
+//
+// Row a1 of SURVEY.md §8(a) (create / preprocess: validation, colouring,
+// colour reordering, threshold and plane tables, upload) plus the orchestration
+// of rows a2-a9 on the handle's CUDA stream.  Host tables follow the contract
+// of DESIGN.md §3.4: T = min(floor(exp(x) * 2^64), 2^64-1) with
+// x = -(beta_k * dE) for Metropolis and x = (beta_{k+1} - beta_k) * d for the
+// exchange.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace ising;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg)
+{
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what)
+{
+    return fail(e == cudaErrorMemoryAllocation ? ISING_E_OOM : ISING_E_CUDA,
+                std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                  \
+    do {                                          \
+        cudaError_t _e = (expr);                  \
+        if (_e != cudaSuccess)                    \
+            return cuda_fail(_e, #expr);          \
+    } while (0)
+
+uint64_t p64(double x)
+{
+    const double p = std::exp(x);
+    const double v = std::ldexp(p, 64);
+    if (v >= 18446744073709551616.0)
+        return std::numeric_limits<uint64_t>::max();
+    return (uint64_t)v;
+}
+
+uint64_t metropolis_threshold(double beta, int64_t dE) { return p64(-(beta * (double)dE)); }
+
+uint64_t exchange_threshold(double beta_lo, double beta_hi, int64_t d)
+{
+    return p64((beta_hi - beta_lo) * (double)d);
+}
+
+}  // namespace
+
+struct ising_handle {
+    int32_t kernel = 0;
+    int32_t n = 0, Lx = 0, Ly = 0, ncol = 0;
+    int64_t m = 0;
+    int32_t wtype = 0, layout = 0, rng = 0;
+    int64_t W_int = 0;
+    double W_f = 0.0;
+    uint64_t seed = 0;
+    RoundKeys rk{};
+    int32_t K = 0, C = 0, c0 = 0, c1 = 0, C_local = 0, G = 0, wpc = 0;
+    int64_t R = 0, slot0 = 0;
+    uint32_t g0 = 0;
+    std::vector<double> betas;
+    uint32_t t = 0, e = 0;
+    int32_t device = 0;
+    cudaStream_t st = nullptr;
+    int32_t threads = 1024;
+    size_t smem = 0;
+    uint32_t ymagic = 0;
+    int32_t cnt_levels = 8;
+    int32_t qmax = 0;
+    std::vector<int32_t> class_off;
+    // device buffers
+    uint32_t *d_state[2] = {nullptr, nullptr};
+    int cur = 0;
+    int8_t *d_s8 = nullptr;
+    int64_t *d_E = nullptr;
+    double *d_Ef = nullptr;
+    int64_t *d_walker = nullptr;
+    uint32_t *d_swapmask = nullptr;
+    uint32_t *d_jword = nullptr, *d_planes = nullptr;
+    int32_t *d_rp = nullptr, *d_col = nullptr, *d_wi = nullptr, *d_class_off = nullptr;
+    uint32_t *d_nbr = nullptr, *d_orig = nullptr, *d_o2i = nullptr;
+    float *d_wf = nullptr, *d_betaf = nullptr;
+    uint64_t *d_T = nullptr, *d_Tx = nullptr;
+    int64_t *d_Tx_off = nullptr;
+    int32_t *d_Tx_len = nullptr;
+    BestDev *d_best = nullptr;
+    int8_t *d_best_spins = nullptr, *d_tmp = nullptr;
+    void *d_scratch = nullptr;
+    size_t scratch_bytes = 0;
+    std::vector<void *> allocs;
+    std::vector<uint32_t> orig;  // internal -> original (CSR kernels)
+    std::vector<uint32_t> o2i;
+
+    template <class T>
+    cudaError_t alloc(T **p, size_t count)
+    {
+        *p = nullptr;
+        if (count == 0)
+            count = 1;
+        cudaError_t e = cudaMalloc((void **)p, count * sizeof(T));
+        if (e == cudaSuccess)
+            allocs.push_back((void *)*p);
+        return e;
+    }
+    ~ising_handle()
+    {
+        for (void *p : allocs)
+            cudaFree(p);
+    }
+};
+
+namespace {
+
+int validate_desc(const ising_run_desc *d)
+{
+    if (!d)
+        return fail(ISING_E_ARG, "desc is NULL");
+    if (d->n_temps < 1)
+        return fail(ISING_E_ARG, "n_temps must be >= 1");
+    if (d->n_copies < 1)
+        return fail(ISING_E_ARG, "n_copies must be >= 1");
+    if (d->copy_begin < 0 || d->copy_end > d->n_copies || d->copy_begin >= d->copy_end)
+        return fail(ISING_E_ARG, "bad copy shard [" + std::to_string(d->copy_begin) + ", " +
+                                     std::to_string(d->copy_end) + ")");
+    if (!d->betas)
+        return fail(ISING_E_ARG, "betas is NULL");
+    for (int k = 0; k < d->n_temps; ++k) {
+        if (!(d->betas[k] > 0.0) || !std::isfinite(d->betas[k]))
+            return fail(ISING_E_ARG, "beta[" + std::to_string(k) + "] must be finite and > 0");
+        if (k > 0 && !(d->betas[k] > d->betas[k - 1]))
+            return fail(ISING_E_ARG, "betas must be strictly increasing (at index " +
+                                         std::to_string(k) + ")");
+    }
+    if (d->layout != ISING_SPINS_BITS && d->layout != ISING_SPINS_I8)
+        return fail(ISING_E_ARG, "unknown layout");
+    if (d->layout == ISING_SPINS_BITS && d->rng != ISING_RNG_PLANE)
+        return fail(ISING_E_ARG, "BITS layout requires the PLANE RNG contract");
+    if (d->layout == ISING_SPINS_I8 && d->rng != ISING_RNG_WORD)
+        return fail(ISING_E_ARG, "I8 layout requires the WORD RNG contract");
+    if (d->layout == ISING_SPINS_BITS && (d->n_temps % 32 != 0 || d->n_temps > 256))
+        return fail(ISING_E_ARG, "BITS layout requires n_temps % 32 == 0 and <= 256");
+    if (d->layout == ISING_SPINS_I8 && d->n_temps % 4 != 0)
+        return fail(ISING_E_ARG, "I8 layout requires n_temps % 4 == 0");
+    if ((int64_t)d->n_copies * d->n_temps >= (int64_t)1 << 33)
+        return fail(ISING_E_ARG, "too many replicas");
+    if (d->block_threads != 0 && (d->block_threads < 32 || d->block_threads > 1024 ||
+                                  d->block_threads % 32 != 0))
+        return fail(ISING_E_ARG, "block_threads must be 0 or a multiple of 32 in [32, 1024]");
+    return ISING_OK;
+}
+
+void fill_run(ising_handle *h, const ising_run_desc *d)
+{
+    h->seed = d->seed;
+    h->rk = make_round_keys(d->seed);
+    h->K = d->n_temps;
+    h->C = d->n_copies;
+    h->c0 = d->copy_begin;
+    h->c1 = d->copy_end;
+    h->C_local = h->c1 - h->c0;
+    h->R = (int64_t)h->C_local * h->K;
+    h->slot0 = (int64_t)h->c0 * h->K;
+    h->G = (int32_t)(h->R / 32);
+    h->g0 = (uint32_t)(h->slot0 / 32);
+    h->wpc = (h->K + 31) / 32;
+    h->betas.assign(d->betas, d->betas + h->K);
+    h->layout = d->layout;
+    h->rng = d->rng;
+    h->device = d->device;
+    h->st = (cudaStream_t)d->stream;
+    h->threads = d->block_threads ? d->block_threads : 1024;
+}
+
+// Integer Metropolis table T[k][q] (q = dE/2 = 0..qmax; q = 0 unused).
+std::vector<uint64_t> accept_table(const std::vector<double> &betas, int32_t qmax)
+{
+    const size_t K = betas.size();
+    std::vector<uint64_t> T(K * (qmax + 1));
+    for (size_t k = 0; k < K; ++k) {
+        T[k * (qmax + 1)] = std::numeric_limits<uint64_t>::max();
+        for (int32_t q = 1; q <= qmax; ++q)
+            T[k * (qmax + 1) + q] = metropolis_threshold(betas[k], 2 * (int64_t)q);
+    }
+    return T;
+}
+
+// Plane tables: for word type wt (temperatures 32wt..32wt+31) and class q,
+// P[j] has bit b = bit (63-j) of T[32wt+b][q].
+void plane_table(const std::vector<double> &betas, const std::vector<int32_t> &qs,
+                 std::vector<uint32_t> &out)
+{
+    const int32_t KW = (int32_t)betas.size() / 32;
+    out.assign((size_t)KW * qs.size() * 64, 0u);
+    for (int32_t wt = 0; wt < KW; ++wt)
+        for (size_t qi = 0; qi < qs.size(); ++qi)
+            for (int b = 0; b < 32; ++b) {
+                const uint64_t T = metropolis_threshold(betas[32 * wt + b], 2 * (int64_t)qs[qi]);
+                for (int j = 0; j < 64; ++j)
+                    if ((T >> (63 - j)) & 1u)
+                        out[((size_t)wt * qs.size() + qi) * 64 + j] |= 1u << b;
+            }
+}
+
+int build_common_device(ising_handle *h, int64_t sum_abs_w)
+{
+    CK(cudaSetDevice(h->device));
+    CK(h->alloc(&h->d_E, h->R));
+    if (h->wtype == ISING_W_F32)
+        CK(h->alloc(&h->d_Ef, h->R));
+    CK(h->alloc(&h->d_walker, h->R));
+    CK(h->alloc(&h->d_swapmask, (size_t)h->C_local * h->wpc));
+    CK(h->alloc(&h->d_best, 1));
+    CK(h->alloc(&h->d_best_spins, h->n));
+    CK(h->alloc(&h->d_tmp, h->n));
+    std::vector<int64_t> walker(h->R);
+    std::iota(walker.begin(), walker.end(), h->slot0);
+    CK(cudaMemcpyAsync(h->d_walker, walker.data(), h->R * sizeof(int64_t), cudaMemcpyHostToDevice,
+                       h->st));
+    BestDev b{0, -1, -1, 0, 0};
+    CK(cudaMemcpyAsync(h->d_best, &b, sizeof(b), cudaMemcpyHostToDevice, h->st));
+    // exchange tables (integer weights): d from -1 down while the threshold is
+    // non-zero, capped by the largest possible energy difference 2*sum|w|.
+    if (h->wtype == ISING_W_I32 && h->K >= 2) {
+        std::vector<uint64_t> Tx;
+        std::vector<int64_t> off(h->K - 1);
+        std::vector<int32_t> len(h->K - 1);
+        const int64_t dmax = 2 * sum_abs_w;
+        for (int32_t k = 0; k + 1 < h->K; ++k) {
+            off[k] = (int64_t)Tx.size();
+            int64_t d = -1;
+            for (; -d <= dmax; --d) {
+                const uint64_t T = exchange_threshold(h->betas[k], h->betas[k + 1], d);
+                if (T == 0)
+                    break;
+                Tx.push_back(T);
+            }
+            len[k] = (int32_t)(-d - 1);
+        }
+        CK(h->alloc(&h->d_Tx, Tx.size()));
+        CK(h->alloc(&h->d_Tx_off, off.size()));
+        CK(h->alloc(&h->d_Tx_len, len.size()));
+        CK(cudaMemcpyAsync(h->d_Tx, Tx.data(), Tx.size() * 8, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(h->d_Tx_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(h->d_Tx_len, len.data(), len.size() * 4, cudaMemcpyHostToDevice, h->st));
+    }
+    return ISING_OK;
+}
+
+// Energies after a state change (set_spins / create).
+int refresh_energy(ising_handle *h)
+{
+    if (h->kernel == KER_GRID_BITS) {
+        GridBitsParams p{};
+        p.state_in = h->d_state[h->cur];
+        p.state_out = h->d_state[h->cur ^ 1];
+        p.jword = h->d_jword;
+        p.planes = h->d_planes;
+        p.E_out = h->d_E;
+        p.Lx = h->Lx; p.Ly = h->Ly; p.n = h->n; p.hx = h->Lx / 2; p.half = h->n / 2;
+        p.ymagic = h->ymagic;
+        p.words_per_copy = h->wpc;
+        p.g0 = h->g0;
+        p.t0 = h->t;
+        p.n_sweeps = 0;
+        p.cnt_levels = h->cnt_levels;
+        p.rk = h->rk;
+        CK(launch_grid_bits(p, h->G, h->threads, h->smem, h->st));
+        h->cur ^= 1;
+    } else if (h->kernel == KER_CSR_BITS) {
+        CsrBitsParams p{};
+        p.state_in = h->d_state[h->cur];
+        p.state_out = h->d_state[h->cur ^ 1];
+        p.rp = h->d_rp; p.nbr = h->d_nbr; p.orig = h->d_orig; p.class_off = h->d_class_off;
+        p.planes = h->d_planes; p.E_out = h->d_E;
+        p.n = h->n; p.ncol = h->ncol; p.qmax = h->qmax; p.m = h->m;
+        p.words_per_copy = h->wpc; p.g0 = h->g0; p.t0 = h->t; p.n_sweeps = 0; p.rk = h->rk;
+        CK(launch_csr_bits(p, h->G, h->threads, h->smem, h->st));
+        h->cur ^= 1;
+    } else {
+        CK(launch_energy_i8(h->d_s8, h->d_rp, h->d_col, h->d_wi, h->d_wf, h->n, (int32_t)h->R, h->d_E,
+                            h->d_Ef, h->d_scratch, h->scratch_bytes, h->st));
+    }
+    return ISING_OK;
+}
+
+// Validated CSR -> internal, colour-sorted CSR and device upload (CSR kernels).
+int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const void *w,
+                    int32_t wtype, const int32_t *colour, const ising_run_desc *desc,
+                    ising_handle **out)
+{
+    std::unique_ptr<ising_handle> h(new ising_handle());
+    h->n = n;
+    h->wtype = wtype;
+    fill_run(h.get(), desc);
+    const int64_t m2 = row_ptr[n];
+    if (m2 >= ((int64_t)1 << 31) - 1)
+        return fail(ISING_E_UNSUPPORTED, "more than 2^31-1 directed edges");
+    h->m = m2 / 2;
+    const int32_t *wi = wtype == ISING_W_I32 ? (const int32_t *)w : nullptr;
+    const float *wf = wtype == ISING_W_F32 ? (const float *)w : nullptr;
+
+    // per-vertex sum |w| guard and totals
+    int64_t qmax = 0, sum_abs = 0;
+    int32_t maxdeg = 0;
+    bool pm1 = true;
+    for (int32_t i = 0; i < n; ++i) {
+        int64_t s = 0;
+        maxdeg = std::max<int32_t>(maxdeg, (int32_t)(row_ptr[i + 1] - row_ptr[i]));
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+            if (wi) {
+                s += std::llabs((long long)wi[e]);
+                pm1 &= (wi[e] == 1 || wi[e] == -1);
+                if (col[e] > i)
+                    h->W_int += wi[e];
+            } else if (col[e] > i) {
+                h->W_f += (double)wf[e];
+            }
+        }
+        if (wi && s >= ((int64_t)1 << 30))
+            return fail(ISING_E_GRAPH, "sum of |w| at vertex " + std::to_string(i) + " >= 2^30");
+        qmax = std::max(qmax, s);
+        sum_abs += s;
+    }
+    sum_abs /= 2;
+    if (desc->layout == ISING_SPINS_BITS) {
+        if (!wi || !pm1)
+            return fail(ISING_E_UNSUPPORTED, "BITS layout needs integer weights in {-1,+1}");
+        if (maxdeg > 15)
+            return fail(ISING_E_UNSUPPORTED, "BITS layout supports degree <= 15");
+        h->kernel = KER_CSR_BITS;
+    } else {
+        h->kernel = KER_CSR_I8;
+    }
+    h->qmax = (int32_t)qmax;
+
+    // colouring
+    std::vector<int32_t> col_of(n);
+    if (colour) {
+        int32_t mx = -1;
+        for (int32_t i = 0; i < n; ++i) {
+            if (colour[i] < 0 || colour[i] >= (1 << 16))
+                return fail(ISING_E_GRAPH, "colour of vertex " + std::to_string(i) + " out of range");
+            mx = std::max(mx, colour[i]);
+            col_of[i] = colour[i];
+        }
+        for (int32_t i = 0; i < n; ++i)
+            for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
+                if (colour[col[e]] == colour[i])
+                    return fail(ISING_E_GRAPH, "improper colouring: vertices " + std::to_string(i) +
+                                                   " and " + std::to_string(col[e]) + " share colour");
+        std::vector<char> used(mx + 1, 0);
+        for (int32_t i = 0; i < n; ++i)
+            used[col_of[i]] = 1;
+        for (int32_t c = 0; c <= mx; ++c)
+            if (!used[c])
+                return fail(ISING_E_GRAPH, "colour ids must be 0..ncol-1 without gaps (missing " +
+                                               std::to_string(c) + ")");
+        h->ncol = mx + 1;
+    } else {
+        h->ncol = ising_greedy_colour(n, row_ptr, col, col_of.data());
+        if (h->ncol < 0)
+            return h->ncol;
+    }
+
+    // internal order: (colour, [degree for BITS], original id)
+    h->orig.resize(n);
+    std::iota(h->orig.begin(), h->orig.end(), 0u);
+    const bool by_deg = h->kernel == KER_CSR_BITS;
+    std::stable_sort(h->orig.begin(), h->orig.end(), [&](uint32_t a, uint32_t b) {
+        if (col_of[a] != col_of[b])
+            return col_of[a] < col_of[b];
+        if (by_deg) {
+            const int64_t da = row_ptr[a + 1] - row_ptr[a], db = row_ptr[b + 1] - row_ptr[b];
+            if (da != db)
+                return da < db;
+        }
+        return a < b;
+    });
+    h->o2i.resize(n);
+    for (int32_t v = 0; v < n; ++v)
+        h->o2i[h->orig[v]] = (uint32_t)v;
+    h->class_off.assign(h->ncol + 1, 0);
+    for (int32_t i = 0; i < n; ++i)
+        h->class_off[col_of[i] + 1]++;
+    for (int32_t c = 0; c < h->ncol; ++c)
+        h->class_off[c + 1] += h->class_off[c];
+
+    std::vector<int32_t> rp(n + 1, 0);
+    for (int32_t v = 0; v < n; ++v)
+        rp[v + 1] = rp[v] + (int32_t)(row_ptr[h->orig[v] + 1] - row_ptr[h->orig[v]]);
+    std::vector<int32_t> ci(m2);
+    std::vector<int32_t> wiv;
+    std::vector<float> wfv;
+    std::vector<uint32_t> nbr;
+    if (wi) wiv.resize(m2);
+    if (wf) wfv.resize(m2);
+    if (by_deg) nbr.resize(m2);
+    for (int32_t v = 0; v < n; ++v) {
+        const int32_t i = (int32_t)h->orig[v];
+        int32_t o = rp[v];
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e, ++o) {
+            ci[o] = (int32_t)h->o2i[col[e]];
+            if (wi) wiv[o] = wi[e];
+            if (wf) wfv[o] = wf[e];
+            if (by_deg) nbr[o] = (uint32_t)ci[o] | (wi[e] < 0 ? 0x80000000u : 0u);
+        }
+    }
+
+    int rc = build_common_device(h.get(), sum_abs);
+    if (rc)
+        return rc;
+    CK(h->alloc(&h->d_rp, n + 1));
+    CK(h->alloc(&h->d_orig, n));
+    CK(h->alloc(&h->d_o2i, n));
+    CK(h->alloc(&h->d_class_off, h->ncol + 1));
+    CK(cudaMemcpyAsync(h->d_rp, rp.data(), (n + 1) * 4, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(h->d_orig, h->orig.data(), (size_t)n * 4, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(h->d_o2i, h->o2i.data(), (size_t)n * 4, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(h->d_class_off, h->class_off.data(), (h->ncol + 1) * 4,
+                       cudaMemcpyHostToDevice, h->st));
+    if (by_deg) {
+        CK(h->alloc(&h->d_nbr, m2));
+        CK(cudaMemcpyAsync(h->d_nbr, nbr.data(), (size_t)m2 * 4, cudaMemcpyHostToDevice, h->st));
+        // planes for q = 1..qmax
+        std::vector<int32_t> qs(h->qmax);
+        std::iota(qs.begin(), qs.end(), 1);
+        std::vector<uint32_t> planes;
+        plane_table(h->betas, qs, planes);
+        CK(h->alloc(&h->d_planes, std::max<size_t>(planes.size(), 1)));
+        if (!planes.empty())
+            CK(cudaMemcpyAsync(h->d_planes, planes.data(), planes.size() * 4, cudaMemcpyHostToDevice,
+                               h->st));
+        h->smem = csr_bits_smem(n, h->qmax, h->wpc);
+        if (h->smem > 200 * 1024)
+            return fail(ISING_E_UNSUPPORTED,
+                        "BITS layout: n too large for a shared-memory resident word group");
+        CK(h->alloc(&h->d_state[0], (size_t)h->G * n));
+        CK(h->alloc(&h->d_state[1], (size_t)h->G * n));
+        CK(launch_init_bits(h->d_state[0], h->G, n, h->d_orig, h->g0, h->rk, h->st));
+    } else {
+        CK(h->alloc(&h->d_col, m2));
+        CK(cudaMemcpyAsync(h->d_col, ci.data(), (size_t)m2 * 4, cudaMemcpyHostToDevice, h->st));
+        if (wi) {
+            CK(h->alloc(&h->d_wi, m2));
+            CK(cudaMemcpyAsync(h->d_wi, wiv.data(), (size_t)m2 * 4, cudaMemcpyHostToDevice, h->st));
+            std::vector<uint64_t> T = accept_table(h->betas, h->qmax);
+            CK(h->alloc(&h->d_T, T.size()));
+            CK(cudaMemcpyAsync(h->d_T, T.data(), T.size() * 8, cudaMemcpyHostToDevice, h->st));
+        } else {
+            CK(h->alloc(&h->d_wf, m2));
+            CK(cudaMemcpyAsync(h->d_wf, wfv.data(), (size_t)m2 * 4, cudaMemcpyHostToDevice, h->st));
+            std::vector<float> bf(h->K);
+            for (int k = 0; k < h->K; ++k)
+                bf[k] = (float)h->betas[k];
+            CK(h->alloc(&h->d_betaf, h->K));
+            CK(cudaMemcpyAsync(h->d_betaf, bf.data(), h->K * 4, cudaMemcpyHostToDevice, h->st));
+        }
+        CK(h->alloc(&h->d_s8, (size_t)n * h->R));
+        h->scratch_bytes = energy_i8_scratch(n, (int32_t)h->R);
+        CK(h->alloc((char **)&h->d_scratch, h->scratch_bytes));
+        CK(launch_init_i8(h->d_s8, n, (int32_t)h->R, h->d_orig, h->slot0, h->rk, h->st));
+    }
+    rc = refresh_energy(h.get());
+    if (rc)
+        return rc;
+    CK(cudaStreamSynchronize(h->st));
+    *out = h.release();
+    return ISING_OK;
+}
+
+int launch_sweeps(ising_handle *h, int32_t ns)
+{
+    if (h->kernel == KER_GRID_BITS) {
+        GridBitsParams p{};
+        p.state_in = h->d_state[h->cur];
+        p.state_out = h->d_state[h->cur ^ 1];
+        p.jword = h->d_jword;
+        p.planes = h->d_planes;
+        p.E_out = h->d_E;
+        p.Lx = h->Lx; p.Ly = h->Ly; p.n = h->n; p.hx = h->Lx / 2; p.half = h->n / 2;
+        p.ymagic = h->ymagic;
+        p.words_per_copy = h->wpc;
+        p.g0 = h->g0;
+        p.t0 = h->t;
+        p.n_sweeps = ns;
+        p.cnt_levels = h->cnt_levels;
+        p.rk = h->rk;
+        CK(launch_grid_bits(p, h->G, h->threads, h->smem, h->st));
+        h->cur ^= 1;
+    } else if (h->kernel == KER_CSR_BITS) {
+        CsrBitsParams p{};
+        p.state_in = h->d_state[h->cur];
+        p.state_out = h->d_state[h->cur ^ 1];
+        p.rp = h->d_rp; p.nbr = h->d_nbr; p.orig = h->d_orig; p.class_off = h->d_class_off;
+        p.planes = h->d_planes; p.E_out = h->d_E;
+        p.n = h->n; p.ncol = h->ncol; p.qmax = h->qmax; p.m = h->m;
+        p.words_per_copy = h->wpc; p.g0 = h->g0; p.t0 = h->t; p.n_sweeps = ns; p.rk = h->rk;
+        CK(launch_csr_bits(p, h->G, h->threads, h->smem, h->st));
+        h->cur ^= 1;
+    } else {
+        CsrI8Params p{};
+        p.s = h->d_s8; p.rp = h->d_rp; p.col = h->d_col; p.wi = h->d_wi; p.wf = h->d_wf;
+        p.orig = h->d_orig; p.T = h->d_T; p.betaf = h->d_betaf; p.R = (int32_t)h->R; p.K = h->K;
+        p.slot0 = h->slot0; p.qmax = h->qmax; p.rk = h->rk;
+        const int32_t thr = h->threads > 256 ? 256 : h->threads;
+        for (int32_t s = 0; s < ns; ++s) {
+            p.t = h->t + (uint32_t)s;
+            for (int32_t c = 0; c < h->ncol; ++c) {
+                p.v_begin = h->class_off[c];
+                p.v_end = h->class_off[c + 1];
+                CK(launch_csr_i8_phase(p, thr, h->st));
+            }
+        }
+        if (ns > 0)
+            CK(launch_energy_i8(h->d_s8, h->d_rp, h->d_col, h->d_wi, h->d_wf, h->n, (int32_t)h->R,
+                                h->d_E, h->d_Ef, h->d_scratch, h->scratch_bytes, h->st));
+    }
+    h->t += (uint32_t)ns;
+    return ISING_OK;
+}
+
+ExchangeParams exchange_params(ising_handle *h)
+{
+    ExchangeParams p{};
+    p.E = h->d_E;
+    p.walker = h->d_walker;
+    p.swapmask = h->d_swapmask;
+    p.best = h->d_best;
+    p.best_spins = h->d_best_spins;
+    p.layout = h->layout;
+    p.state = h->d_state[h->cur];
+    p.s8 = h->d_s8;
+    p.perm_o2i = (h->kernel == KER_GRID_BITS) ? nullptr : h->d_o2i;
+    p.n = h->n;
+    p.K = h->K;
+    p.C_local = h->C_local;
+    p.words_per_copy = h->wpc;
+    p.slot0 = h->slot0;
+    p.R_local = h->R;
+    p.is_float = h->wtype == ISING_W_F32;
+    p.t = h->t;
+    p.e = h->e;
+    p.Tx = h->d_Tx;
+    p.Tx_off = h->d_Tx_off;
+    p.Tx_len = h->d_Tx_len;
+    p.rk = h->rk;
+    return p;
+}
+
+int do_exchange(ising_handle *h, const void *recs, int64_t n_recs, bool do_swap)
+{
+    if (do_swap && h->wtype == ISING_W_F32)
+        return fail(ISING_E_UNSUPPORTED, "replica exchange requires integer weights");
+    ExchangeParams p = exchange_params(h);
+    p.recs = (const ising_record *)recs;
+    p.n_recs = recs ? n_recs : 0;
+    p.do_best = 1;
+    p.do_swap = do_swap ? 1 : 0;
+    CK(launch_exchange(p, h->st));
+    if (do_swap && h->K >= 2) {
+        if (h->layout == ISING_SPINS_BITS)
+            CK(launch_swap_bits(h->d_state[h->cur], h->d_swapmask, h->n, h->C_local, h->wpc, h->st));
+        else
+            CK(launch_swap_i8(h->d_s8, h->d_swapmask, h->n, (int32_t)h->R, h->K, h->st));
+    }
+    if (do_swap)
+        h->e += 1;
+    return ISING_OK;
+}
+
+int check_handle(const ising_handle *h)
+{
+    if (!h)
+        return fail(ISING_E_ARG, "handle is NULL");
+    cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "cudaSetDevice");
+    return ISING_OK;
+}
+
+// Copy one local slot's configuration (original ids) into d_tmp.
+int slot_to_tmp(ising_handle *h, int64_t rl)
+{
+    if (h->layout == ISING_SPINS_BITS) {
+        CK(launch_extract_bits(h->d_state[h->cur], h->n, (int32_t)(rl / 32), (int32_t)(rl % 32),
+                               h->kernel == KER_GRID_BITS ? nullptr : h->d_o2i, h->d_tmp, h->st));
+    } else {
+        CK(cudaMemcpy2DAsync(h->d_tmp, 1, h->d_s8 + rl, (size_t)h->R, 1, h->n,
+                             cudaMemcpyDeviceToDevice, h->st));
+    }
+    return ISING_OK;
+}
+
+}  // namespace
+
+// =========================================================================== ABI
+extern "C" {
+
+const char *ising_last_error(void) { return g_err.c_str(); }
+
+const char *ising_version(void) { return "libising 0.1 (sm_100a)"; }
+
+uint64_t ising_threshold(double beta, int64_t dE) { return metropolis_threshold(beta, dE); }
+
+int ising_greedy_colour(int32_t n, const int64_t *row_ptr, const int32_t *col, int32_t *colour_out)
+{
+    if (n < 1 || !row_ptr || !col || !colour_out)
+        return fail(ISING_E_ARG, "greedy_colour: bad arguments");
+    int32_t maxdeg = 0;
+    for (int32_t i = 0; i < n; ++i)
+        maxdeg = std::max<int32_t>(maxdeg, (int32_t)(row_ptr[i + 1] - row_ptr[i]));
+    std::vector<int32_t> stamp(maxdeg + 2, -1);
+    int32_t ncol = 0;
+    for (int32_t i = 0; i < n; ++i)
+        colour_out[i] = -1;
+    for (int32_t i = 0; i < n; ++i) {
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+            const int32_t c = colour_out[col[e]];
+            if (c >= 0 && c <= maxdeg + 1)
+                stamp[c] = i;
+        }
+        int32_t c = 0;
+        while (stamp[c] == i)
+            ++c;
+        colour_out[i] = c;
+        ncol = std::max(ncol, c + 1);
+    }
+    return ncol;
+}
+
+int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_t *J_down,
+                      const ising_run_desc *desc, ising_handle **out)
+{
+    g_err.clear();
+    if (!out)
+        return fail(ISING_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (!J_right || !J_down)
+        return fail(ISING_E_ARG, "J_right/J_down is NULL");
+    if (Lx < 4 || Ly < 4 || (Lx & 1) || (Ly & 1))
+        return fail(ISING_E_ARG, "grid dims must be even and >= 4 (got " + std::to_string(Lx) + "x" +
+                                     std::to_string(Ly) + ")");
+    if ((int64_t)Lx * Ly >= ((int64_t)1 << 30))
+        return fail(ISING_E_ARG, "grid too large");
+    int rc = validate_desc(desc);
+    if (rc)
+        return rc;
+    const int32_t n = Lx * Ly;
+    for (int32_t i = 0; i < n; ++i) {
+        if (J_right[i] != 1 && J_right[i] != -1)
+            return fail(ISING_E_GRAPH, "J_right[" + std::to_string(i) + "] not in {-1,+1}");
+        if (J_down[i] != 1 && J_down[i] != -1)
+            return fail(ISING_E_GRAPH, "J_down[" + std::to_string(i) + "] not in {-1,+1}");
+    }
+    if (desc->layout == ISING_SPINS_I8) {
+        // generic CSR kernels: row order right, left, down, up; checkerboard colouring
+        std::vector<int64_t> rp(n + 1);
+        std::vector<int32_t> col(4 * (size_t)n), w(4 * (size_t)n), colour(n);
+        for (int32_t y = 0; y < Ly; ++y)
+            for (int32_t x = 0; x < Lx; ++x) {
+                const int32_t i = x + Lx * y;
+                const int32_t r = (x + 1) % Lx + Lx * y, l = (x + Lx - 1) % Lx + Lx * y;
+                const int32_t d = x + Lx * ((y + 1) % Ly), u = x + Lx * ((y + Ly - 1) % Ly);
+                rp[i] = 4 * (int64_t)i;
+                col[4 * i] = r; w[4 * i] = J_right[i];
+                col[4 * i + 1] = l; w[4 * i + 1] = J_right[l];
+                col[4 * i + 2] = d; w[4 * i + 2] = J_down[i];
+                col[4 * i + 3] = u; w[4 * i + 3] = J_down[u];
+                colour[i] = (x + y) & 1;
+            }
+        rp[n] = 4 * (int64_t)n;
+        rc = create_csr_impl(n, rp.data(), col.data(), w.data(), ISING_W_I32, colour.data(), desc,
+                             out);
+        if (rc == ISING_OK) {
+            (*out)->Lx = Lx;
+            (*out)->Ly = Ly;
+        }
+        return rc;
+    }
+
+    std::unique_ptr<ising_handle> h(new ising_handle());
+    h->kernel = KER_GRID_BITS;
+    h->n = n;
+    h->Lx = Lx;
+    h->Ly = Ly;
+    h->ncol = 2;
+    h->m = 2 * (int64_t)n;
+    h->wtype = ISING_W_I32;
+    fill_run(h.get(), desc);
+    for (int32_t i = 0; i < n; ++i)
+        h->W_int += J_right[i] + J_down[i];
+    h->smem = grid_bits_smem(n);
+    if (h->smem > 200 * 1024)
+        return fail(ISING_E_UNSUPPORTED, "BITS grid: lattice too large for shared memory (n=" +
+                                             std::to_string(n) + ")");
+    const int32_t hx = Lx / 2, half = n / 2;
+    h->ymagic = (uint32_t)((((uint64_t)1 << 32) + hx - 1) / hx);
+    for (int32_t l = 0; l < half; ++l)
+        if ((int32_t)(((uint64_t)l * h->ymagic) >> 32) != l / hx)
+            return fail(ISING_E_UNSUPPORTED, "grid index magic not exact");
+    const int32_t per_thread = 4 * ((half + h->threads - 1) / h->threads);
+    h->cnt_levels = 1;
+    while ((1 << h->cnt_levels) <= per_thread)
+        ++h->cnt_levels;
+    if (h->cnt_levels > 8)
+        return fail(ISING_E_UNSUPPORTED, "too many sites per thread for the energy counter");
+    // jword in colour-separated order
+    std::vector<uint32_t> jw(n);
+    for (int32_t c = 0; c < 2; ++c)
+        for (int32_t y = 0; y < Ly; ++y)
+            for (int32_t mm = 0; mm < hx; ++mm) {
+                const int32_t x = 2 * mm + ((c + y) & 1);
+                const int32_t i = x + Lx * y;
+                const int32_t l = (x + Lx - 1) % Lx + Lx * y, u = x + Lx * ((y + Ly - 1) % Ly);
+                uint32_t v = 0;
+                if (J_right[i] < 0) v |= 0x80u;
+                if (J_right[l] < 0) v |= 0x80u << 8;
+                if (J_down[i] < 0) v |= 0x80u << 16;
+                if (J_down[u] < 0) v |= 0x80u << 24;
+                jw[c * half + y * hx + mm] = v;
+            }
+    std::vector<uint32_t> planes;
+    plane_table(h->betas, {2, 4}, planes);
+    rc = build_common_device(h.get(), 2 * (int64_t)n);
+    if (rc)
+        return rc;
+    CK(h->alloc(&h->d_jword, n));
+    CK(h->alloc(&h->d_planes, planes.size()));
+    CK(cudaMemcpyAsync(h->d_jword, jw.data(), (size_t)n * 4, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(h->d_planes, planes.data(), planes.size() * 4, cudaMemcpyHostToDevice, h->st));
+    CK(h->alloc(&h->d_state[0], (size_t)h->G * n));
+    CK(h->alloc(&h->d_state[1], (size_t)h->G * n));
+    CK(launch_init_bits(h->d_state[0], h->G, n, nullptr, h->g0, h->rk, h->st));
+    rc = refresh_energy(h.get());
+    if (rc)
+        return rc;
+    CK(cudaStreamSynchronize(h->st));
+    *out = h.release();
+    return ISING_OK;
+}
+
+int ising_create_csr(int32_t n, const int64_t *row_ptr, const int32_t *col, const void *w,
+                     int32_t wtype, const int32_t *colour, const ising_run_desc *desc,
+                     ising_handle **out)
+{
+    g_err.clear();
+    if (!out)
+        return fail(ISING_E_ARG, "out is NULL");
+    *out = nullptr;
+    if (n < 1)
+        return fail(ISING_E_ARG, "n must be >= 1");
+    if (!row_ptr || !col || !w)
+        return fail(ISING_E_ARG, "row_ptr/col/w is NULL");
+    if (wtype != ISING_W_I32 && wtype != ISING_W_F32)
+        return fail(ISING_E_ARG, "unknown wtype");
+    int rc = validate_desc(desc);
+    if (rc)
+        return rc;
+    if (row_ptr[0] != 0)
+        return fail(ISING_E_GRAPH, "row_ptr[0] != 0");
+    for (int32_t i = 0; i < n; ++i)
+        if (row_ptr[i + 1] < row_ptr[i])
+            return fail(ISING_E_GRAPH, "row_ptr decreases at vertex " + std::to_string(i));
+    const int32_t *wi = wtype == ISING_W_I32 ? (const int32_t *)w : nullptr;
+    const float *wf = wtype == ISING_W_F32 ? (const float *)w : nullptr;
+    std::vector<int64_t> mark(n, -1);
+    for (int32_t i = 0; i < n; ++i) {
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+            const int32_t j = col[e];
+            if (j < 0 || j >= n)
+                return fail(ISING_E_GRAPH, "col[" + std::to_string(e) + "] = " + std::to_string(j) +
+                                               " out of range at vertex " + std::to_string(i));
+            if (j == i)
+                return fail(ISING_E_GRAPH, "self-loop at vertex " + std::to_string(i));
+            if (mark[j] == i)
+                return fail(ISING_E_GRAPH, "duplicate edge " + std::to_string(i) + "-" +
+                                               std::to_string(j));
+            mark[j] = i;
+            if (wf && !std::isfinite(wf[e]))
+                return fail(ISING_E_GRAPH, "non-finite weight at entry " + std::to_string(e));
+        }
+    }
+    // symmetry: (i, j, w) present iff (j, i, w)
+    for (int32_t i = 0; i < n; ++i) {
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+            const int32_t j = col[e];
+            bool found = false;
+            for (int64_t f = row_ptr[j]; f < row_ptr[j + 1]; ++f)
+                if (col[f] == i) {
+                    found = wi ? (wi[f] == wi[e]) : (wf[f] == wf[e]);
+                    break;
+                }
+            if (!found)
+                return fail(ISING_E_GRAPH, "asymmetric coupling " + std::to_string(i) + "-" +
+                                               std::to_string(j));
+        }
+    }
+    return create_csr_impl(n, row_ptr, col, w, wtype, colour, desc, out);
+}
+
+int ising_sweep(ising_handle *h, int32_t n_sweeps)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (n_sweeps < 0)
+        return fail(ISING_E_ARG, "n_sweeps < 0");
+    if ((uint64_t)h->t + (uint64_t)n_sweeps >= ((uint64_t)1 << 32))
+        return fail(ISING_E_ARG, "sweep counter would exceed 2^32");
+    return launch_sweeps(h, n_sweeps);
+}
+
+int ising_energy(ising_handle *h, void *out)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (!out)
+        return fail(ISING_E_ARG, "out is NULL");
+    if (h->wtype == ISING_W_F32)
+        CK(cudaMemcpyAsync(out, h->d_Ef, h->R * 8, cudaMemcpyDeviceToHost, h->st));
+    else
+        CK(cudaMemcpyAsync(out, h->d_E, h->R * 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return ISING_OK;
+}
+
+int ising_cut(ising_handle *h, void *out)
+{
+    int rc = ising_energy(h, out);
+    if (rc)
+        return rc;
+    if (h->wtype == ISING_W_F32) {
+        double *o = (double *)out;
+        for (int64_t r = 0; r < h->R; ++r)
+            o[r] = (h->W_f - o[r]) / 2.0;
+    } else {
+        int64_t *o = (int64_t *)out;
+        for (int64_t r = 0; r < h->R; ++r)
+            o[r] = (h->W_int - o[r]) / 2;
+    }
+    return ISING_OK;
+}
+
+int ising_exchange(ising_handle *h)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    return do_exchange(h, nullptr, 0, true);
+}
+
+int ising_exchange_begin(ising_handle *h, void *dev_send)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (!dev_send)
+        return fail(ISING_E_ARG, "dev_send is NULL");
+    CK(launch_records(h->d_E, (ising_record *)dev_send, h->R, h->slot0, h->st));
+    return ISING_OK;
+}
+
+int ising_exchange_end(ising_handle *h, const void *dev_recv, int64_t n_records)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (!dev_recv || n_records < 1)
+        return fail(ISING_E_ARG, "dev_recv is NULL or n_records < 1");
+    return do_exchange(h, dev_recv, n_records, true);
+}
+
+int ising_check_best(ising_handle *h, const void *dev_recv, int64_t n_records)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (dev_recv && n_records < 1)
+        return fail(ISING_E_ARG, "n_records < 1");
+    return do_exchange(h, dev_recv, dev_recv ? n_records : 0, false);
+}
+
+int ising_best(ising_handle *h, void *best_E, int64_t *slot, int64_t *sweep, int8_t *spins_out)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    BestDev b;
+    CK(cudaMemcpyAsync(&b, h->d_best, sizeof(b), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (b.slot < 0)
+        return fail(ISING_E_STATE, "no best-so-far check has run yet");
+    if (best_E)
+        std::memcpy(best_E, &b.energy, 8);
+    if (slot)
+        *slot = b.slot;
+    if (sweep)
+        *sweep = b.sweep;
+    if (spins_out) {
+        if (!b.owner)
+            return fail(ISING_E_STATE, "best configuration is held by another shard");
+        CK(cudaMemcpyAsync(spins_out, h->d_best_spins, h->n, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+    }
+    return ISING_OK;
+}
+
+int ising_get_spins(ising_handle *h, int64_t slot, int8_t *out)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (!out)
+        return fail(ISING_E_ARG, "out is NULL");
+    if (slot < h->slot0 || slot >= h->slot0 + h->R)
+        return fail(ISING_E_STATE, "slot " + std::to_string(slot) + " is not held by this handle");
+    rc = slot_to_tmp(h, slot - h->slot0);
+    if (rc)
+        return rc;
+    if (h->kernel == KER_CSR_I8) {
+        std::vector<int8_t> tmp(h->n);
+        CK(cudaMemcpyAsync(tmp.data(), h->d_tmp, h->n, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        for (int32_t i = 0; i < h->n; ++i)
+            out[i] = tmp[h->o2i[i]];
+    } else {
+        CK(cudaMemcpyAsync(out, h->d_tmp, h->n, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+    }
+    return ISING_OK;
+}
+
+int ising_set_spins(ising_handle *h, int64_t slot, const int8_t *in)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (!in)
+        return fail(ISING_E_ARG, "in is NULL");
+    if (slot < h->slot0 || slot >= h->slot0 + h->R)
+        return fail(ISING_E_STATE, "slot " + std::to_string(slot) + " is not held by this handle");
+    for (int32_t i = 0; i < h->n; ++i)
+        if (in[i] != 1 && in[i] != -1)
+            return fail(ISING_E_ARG, "spin " + std::to_string(i) + " not in {-1,+1}");
+    const int64_t rl = slot - h->slot0;
+    if (h->layout == ISING_SPINS_BITS) {
+        CK(cudaMemcpyAsync(h->d_tmp, in, h->n, cudaMemcpyHostToDevice, h->st));
+        CK(launch_insert_bits(h->d_state[h->cur], h->n, (int32_t)(rl / 32), (int32_t)(rl % 32),
+                              h->kernel == KER_GRID_BITS ? nullptr : h->d_o2i, h->d_tmp, h->st));
+    } else {
+        std::vector<int8_t> tmp(h->n);
+        for (int32_t v = 0; v < h->n; ++v)
+            tmp[v] = in[h->orig[v]];
+        CK(cudaMemcpyAsync(h->d_tmp, tmp.data(), h->n, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpy2DAsync(h->d_s8 + rl, (size_t)h->R, h->d_tmp, 1, 1, h->n,
+                             cudaMemcpyDeviceToDevice, h->st));
+        CK(cudaStreamSynchronize(h->st));
+    }
+    rc = refresh_energy(h);
+    if (rc)
+        return rc;
+    CK(cudaStreamSynchronize(h->st));
+    return ISING_OK;
+}
+
+int ising_get_walkers(ising_handle *h, int64_t *out)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (!out)
+        return fail(ISING_E_ARG, "out is NULL");
+    CK(cudaMemcpyAsync(out, h->d_walker, h->R * 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return ISING_OK;
+}
+
+int ising_info(const ising_handle *h, ising_info_t *out)
+{
+    if (!h || !out)
+        return fail(ISING_E_ARG, "NULL argument");
+    out->n = h->n;
+    out->n_colours = h->ncol;
+    out->n_edges = h->m;
+    out->n_temps = h->K;
+    out->n_copies = h->C;
+    out->copy_begin = h->c0;
+    out->copy_end = h->c1;
+    out->slot_begin = h->slot0;
+    out->n_slots = h->R;
+    out->layout = h->layout;
+    out->rng = h->rng;
+    out->wtype = h->wtype;
+    out->kernel = h->kernel;
+    out->sweeps_done = h->t;
+    out->exchanges_done = h->e;
+    out->W_int = h->W_int;
+    out->W_f64 = h->W_f;
+    return ISING_OK;
+}
+
+int ising_sync(ising_handle *h)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    CK(cudaStreamSynchronize(h->st));
+    return ISING_OK;
+}
+
+void ising_destroy(ising_handle *h)
+{
+    if (!h)
+        return;
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->st);
+    delete h;
+}
+
+int ising_debug_philox(int32_t device, const uint32_t *in, int32_t n, uint32_t *out_lib,
+                       uint32_t *out_curand)
+{
+    if (!in || !out_lib || !out_curand || n < 1)
+        return fail(ISING_E_ARG, "debug_philox: bad arguments");
+    CK(cudaSetDevice(device));
+    uint32_t *d_in = nullptr, *d_a = nullptr, *d_b = nullptr;
+    CK(cudaMalloc(&d_in, (size_t)n * 24));
+    CK(cudaMalloc(&d_a, (size_t)n * 16));
+    CK(cudaMalloc(&d_b, (size_t)n * 16));
+    CK(cudaMemcpy(d_in, in, (size_t)n * 24, cudaMemcpyHostToDevice));
+    CK(launch_debug_philox(d_in, n, d_a, d_b, nullptr));
+    CK(cudaMemcpy(out_lib, d_a, (size_t)n * 16, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_curand, d_b, (size_t)n * 16, cudaMemcpyDeviceToHost));
+    cudaFree(d_in);
+    cudaFree(d_a);
+    cudaFree(d_b);
+    return ISING_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,133 @@
+// internal.h -- handle layout and kernel launchers of libising (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/ising.h"
+#include "common.cuh"
+
+namespace ising {
+
+enum Kernel : int32_t { KER_GRID_BITS = 0, KER_CSR_BITS = 1, KER_CSR_I8 = 2 };
+
+// Best-so-far record kept in device memory (updated by the exchange kernel).
+struct BestDev {
+    int64_t energy;  // int64, or double bits
+    int64_t slot;    // global slot, -1 = none yet
+    int64_t sweep;
+    int32_t owner;   // 1 if this handle snapshotted the configuration
+    int32_t pad;
+};
+
+// ----------------------------------------------------------------- kernel params
+struct GridBitsParams {
+    const uint32_t *state_in;  // [G][n], original site order
+    uint32_t *state_out;
+    const uint32_t *jword;     // [n] colour-separated order: bytes right,left,down,up; 0x80 = J=-1
+    const uint32_t *planes;    // [K/32][2][64]: index 0 = dE 4, 1 = dE 8
+    int64_t *E_out;            // [R_local]
+    int32_t Lx, Ly, n, hx, half;
+    uint32_t ymagic;           // floor division by hx via umulhi
+    int32_t words_per_copy;    // K/32
+    uint32_t g0;               // global group of local group 0
+    uint32_t t0;
+    int32_t n_sweeps;
+    int32_t cnt_levels;        // bits of the per-thread energy counter
+    RoundKeys rk;
+};
+
+struct CsrBitsParams {
+    const uint32_t *state_in;  // [G][n] internal order
+    uint32_t *state_out;
+    const int32_t *rp;         // [n+1] internal
+    const uint32_t *nbr;       // [m2] internal neighbour id | (J==-1) << 31
+    const uint32_t *orig;      // [n] internal -> original id
+    const int32_t *class_off;  // [ncol+1]
+    const uint32_t *planes;    // [K/32][Qmax][64]  q = dE/2 = 1..Qmax
+    int64_t *E_out;
+    int32_t n, ncol, qmax;
+    int64_t m;                 // undirected edges
+    int32_t words_per_copy;
+    uint32_t g0, t0;
+    int32_t n_sweeps;
+    RoundKeys rk;
+};
+
+struct CsrI8Params {
+    int8_t *s;                 // [n][R] internal vertex order, replica-minor
+    const int32_t *rp;         // [n+1] internal
+    const int32_t *col;        // internal ids
+    const int32_t *wi;         // int weights or null
+    const float *wf;           // float weights or null
+    const uint32_t *orig;      // internal -> original id
+    const uint64_t *T;         // [K][qmax+1] integer thresholds (q = dE/2), int weights
+    const float *betaf;        // [K] float(beta_k), float weights
+    int32_t R;                 // local replicas (multiple of 4)
+    int32_t K;
+    int64_t slot0;             // first global slot
+    int32_t qmax;
+    int32_t v_begin, v_end;    // vertex class range (internal)
+    uint32_t t;
+    RoundKeys rk;
+};
+
+struct ExchangeParams {
+    int64_t *E;                // [R_local] (int64 or double bits)
+    int64_t *walker;           // [R_local]
+    uint32_t *swapmask;        // [C_local][ceil(K/32)]
+    BestDev *best;
+    int8_t *best_spins;        // [n] original order
+    const ising_record *recs;  // gathered records or null (local)
+    int64_t n_recs;
+    // configuration access for the snapshot
+    int32_t layout;            // 0 bits, 1 i8
+    const uint32_t *state;     // bits: [G][n] (grid: original order; csr: internal)
+    const int8_t *s8;          // i8: [n][R] internal
+    const uint32_t *perm_o2i;  // original -> internal id (null = identity)
+    int32_t n;
+    int32_t K, C_local, words_per_copy;
+    int64_t slot0, R_local;
+    int32_t is_float;
+    uint32_t t, e;
+    int32_t do_best, do_swap;
+    const uint64_t *Tx;        // exchange thresholds flat
+    const int64_t *Tx_off;     // [K-1] offset into Tx; entry for d<0 at Tx[off + (-d-1)]
+    const int32_t *Tx_len;     // [K-1]
+    RoundKeys rk;
+};
+
+// ----------------------------------------------------------------- launchers
+cudaError_t launch_init_bits(uint32_t *state, int32_t G, int32_t n, const uint32_t *orig,
+                             uint32_t g0, const RoundKeys &rk, cudaStream_t st);
+cudaError_t launch_init_i8(int8_t *s, int32_t n, int32_t R, const uint32_t *orig, int64_t slot0,
+                           const RoundKeys &rk, cudaStream_t st);
+cudaError_t launch_grid_bits(const GridBitsParams &p, int32_t G, int32_t threads, size_t smem,
+                             cudaStream_t st);
+size_t grid_bits_smem(int32_t n);
+cudaError_t launch_csr_bits(const CsrBitsParams &p, int32_t G, int32_t threads, size_t smem,
+                            cudaStream_t st);
+size_t csr_bits_smem(int32_t n, int32_t qmax, int32_t words_per_copy);
+cudaError_t launch_csr_i8_phase(const CsrI8Params &p, int32_t threads, cudaStream_t st);
+cudaError_t launch_energy_i8(const int8_t *s, const int32_t *rp, const int32_t *col,
+                             const int32_t *wi, const float *wf, int32_t n, int32_t R,
+                             int64_t *Ei, double *Ef, void *scratch, size_t scratch_bytes,
+                             cudaStream_t st);
+size_t energy_i8_scratch(int32_t n, int32_t R);
+cudaError_t launch_exchange(const ExchangeParams &p, cudaStream_t st);
+cudaError_t launch_swap_bits(uint32_t *state, const uint32_t *swapmask, int32_t n, int32_t C_local,
+                             int32_t words_per_copy, cudaStream_t st);
+cudaError_t launch_swap_i8(int8_t *s, const uint32_t *swapmask, int32_t n, int32_t R, int32_t K,
+                           cudaStream_t st);
+cudaError_t launch_records(const int64_t *E, ising_record *out, int64_t R, int64_t slot0,
+                           cudaStream_t st);
+cudaError_t launch_extract_bits(const uint32_t *state, int32_t n, int32_t gl, int32_t bit,
+                                const uint32_t *perm_o2i, int8_t *out, cudaStream_t st);
+cudaError_t launch_insert_bits(uint32_t *state, int32_t n, int32_t gl, int32_t bit,
+                               const uint32_t *perm_o2i, const int8_t *in, cudaStream_t st);
+cudaError_t launch_debug_philox(const uint32_t *in, int32_t n, uint32_t *out_lib,
+                                uint32_t *out_curand, cudaStream_t st);
+
+}  // namespace ising

@@ -1,0 +1,172 @@
+"""Run schedule of the hot path on top of libising.
+
+`Engine` owns one libising handle (one copy shard on one GPU).  `run_pt` drives
+the parallel-tempering schedule -- rounds of `k_ex` Metropolis sweeps, each
+followed by a best-so-far check and a replica exchange, plus a final check
+("exchanges replicas across temperatures"; P:59 sweeps as the unit
+of work; SPEC.md S:261-264/S:327 best-so-far, first reached wins).
+
+Multi-GPU: one process per GPU, copies sharded contiguously over ranks (copies
+are independent PT ladders).  Exchange decisions only need a
+copy's own energies, so they are local.  Two modes:
+  * gather=True  -- north-star mode: each exchange all-gathers the 16-byte
+    per-slot records (energy, global slot) over NCCL; every rank then applies the
+    same global best-so-far rule (exchange_end);
+  * gather=False -- each rank keeps its local best; one all-gather of the
+    per-rank best records at the end, merged by (E, sweep, slot).
+Both give the same record as a single process holding all copies (tests).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import ising as L
+
+
+class Engine:
+    """One libising handle.  inst: dict from synth.make_instance (grid or csr)."""
+
+    def __init__(self, inst: dict, K: int, C: int, betas, seed: int, copy_begin: int = 0,
+                 copy_end: int | None = None, layout: str = "bits", device: int = 0,
+                 colour=None, block_threads: int = 0, stream=None):
+        kw = dict(seed=seed, n_temps=K, n_copies=C, betas=betas, copy_begin=copy_begin,
+                  copy_end=C if copy_end is None else copy_end, layout=layout, device=device,
+                  block_threads=block_threads, stream=stream)
+        if inst["kind"] == "grid":
+            self.h = L.ising_create_grid(inst["Lx"], inst["Ly"], inst["J_right"], inst["J_down"], **kw)
+        else:
+            self.h = L.ising_create_csr(inst["n"], inst["row_ptr"], inst["col"], inst["w"],
+                                        colour=colour, **kw)
+        self.info = L.ising_info(self.h)
+        self.device = device
+        self.K, self.C = K, C
+        self.R = int(self.info.n_slots)
+        self.slot0 = int(self.info.slot_begin)
+        self.is_float = self.info.wtype == L.ISING_W_F32
+
+    # ---- hot path
+    def sweep(self, n: int):
+        L.ising_sweep(self.h, n)
+
+    def exchange(self):
+        L.ising_exchange(self.h)
+
+    def exchange_begin(self, send):
+        L.ising_exchange_begin(self.h, send.data_ptr())
+
+    def exchange_end(self, recv):
+        L.ising_exchange_end(self.h, recv.data_ptr(), recv.shape[0])
+
+    def check_best(self, recv=None):
+        if recv is None:
+            L.ising_check_best(self.h)
+        else:
+            L.ising_check_best(self.h, recv.data_ptr(), recv.shape[0])
+
+    def record_buffers(self, world: int):
+        import torch
+        dev = torch.device("cuda", self.device)
+        send = torch.empty((self.R, 2), dtype=torch.int64, device=dev)
+        recv = torch.empty((self.R * world, 2), dtype=torch.int64, device=dev)
+        return send, recv
+
+    # ---- readback
+    def energies(self):
+        return L.ising_energy(self.h)
+
+    def cuts(self):
+        return L.ising_cut(self.h)
+
+    def best(self, spins: bool = True):
+        try:
+            return L.ising_best(self.h, spins=spins)
+        except L.IsingError as e:
+            if e.code == L.ISING_E_STATE and spins:
+                return L.ising_best(self.h, spins=False)
+            raise
+
+    def spins(self, slot: int):
+        return L.ising_get_spins(self.h, slot)
+
+    def set_spins(self, slot: int, s):
+        L.ising_set_spins(self.h, slot, s)
+
+    def walkers(self):
+        return L.ising_get_walkers(self.h)
+
+    def sync(self):
+        L.ising_sync(self.h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            L.ising_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def shard(C: int, world: int, rank: int):
+    """Contiguous copy shard of `rank` (copies split as evenly as possible)."""
+    return (C * rank) // world, (C * (rank + 1)) // world
+
+
+def best_key(rec):
+    return (rec["E"], rec["sweep"], rec["slot"])
+
+
+def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True):
+    """PT schedule: rounds of k_ex sweeps + (best check, exchange); final check.
+
+    k_ex <= 0 -> plain Metropolis (no exchange), one best check at the end.
+    Returns the global best record {E, slot, sweep} (same on every rank)."""
+    import torch.distributed as dist  # only needed for group != None
+    world = dist.get_world_size(group) if group is not None else 1
+    multi = world > 1
+    done = 0
+    if multi and gather:
+        send, recv = engine.record_buffers(world)
+    if k_ex > 0:
+        while done + k_ex <= sweeps:
+            engine.sweep(k_ex)
+            done += k_ex
+            if multi and gather:
+                engine.exchange_begin(send)
+                dist.all_gather_into_tensor(recv, send, group=group)
+                engine.exchange_end(recv)
+            else:
+                engine.exchange()
+    if done < sweeps or k_ex <= 0:
+        engine.sweep(sweeps - done)
+        if multi and gather:
+            engine.exchange_begin(send)
+            dist.all_gather_into_tensor(recv, send, group=group)
+            engine.check_best(recv)
+        else:
+            engine.check_best()
+    rec = engine.best(spins=False)
+    if multi and not gather:
+        rec = merge_best_over_ranks(rec, group)
+    return {k: rec[k] for k in ("E", "slot", "sweep")}
+
+
+def merge_best_over_ranks(rec, group):
+    """All-gather the per-rank best records and keep the lexicographic min (E, sweep, slot)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    E = rec["E"]
+    is_float = isinstance(E, float)
+    mine = torch.tensor([[float(E) if is_float else int(E), rec["sweep"], rec["slot"]]],
+                        dtype=torch.float64 if is_float else torch.int64, device=dev)
+    allr = torch.empty((world, 3), dtype=mine.dtype, device=dev)
+    dist.all_gather_into_tensor(allr, mine, group=group)
+    rows = allr.cpu().numpy()
+    order = np.lexsort((rows[:, 2], rows[:, 1], rows[:, 0]))
+    r = rows[order[0]]
+    return dict(E=float(r[0]) if is_float else int(r[0]), sweep=int(r[1]), slot=int(r[2]))

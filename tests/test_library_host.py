@@ -1,0 +1,97 @@
+"""Host-side checks of libising.so that need no GPU: the library loads, exports every
+symbol include/ising.h declares, its host tables/colouring agree with the oracle's
+independent implementation, and create() validates inputs before touching a device."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from paper_2311_09275_b200 import ising as L
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "ising.h")).read()
+    return sorted(set(re.findall(r"ISING_API[^;(]*?\b(ising_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = L.lib()
+    names = header_functions()
+    assert len(names) >= 20
+    for nm in names:
+        assert hasattr(lib, nm), nm
+    assert set(names) == set(L.EXPORTED)
+    assert "sm_100a" in L.ising_version()
+
+
+def test_threshold_table_matches_oracle():
+    for beta in synth.beta_ladder(64)[::5]:
+        for dE in (2, 4, 6, 8, 10, 20):
+            assert L.ising_threshold(beta, dE) == oracle.threshold_int(beta, dE)
+
+
+def test_greedy_colouring_matches_oracle():
+    u, v = synth.gnm(3000, 2999, 70)
+    rp, col, _ = synth.edges_to_csr(3000, u, v, np.ones(u.size, np.int32))
+    a, na = L.ising_greedy_colour(3000, rp, col)
+    b, nb = oracle.greedy_colour(3000, rp, col)
+    assert na == nb and np.array_equal(a, b)
+
+
+def _desc(**kw):
+    d = dict(seed=1, n_temps=32, n_copies=1, betas=synth.beta_ladder(32), layout="bits", device=0)
+    d.update(kw)
+    return d
+
+
+def _code(fn, *a, **kw):
+    with pytest.raises(L.IsingError) as ei:
+        fn(*a, **kw)
+    return ei.value.code, str(ei.value)
+
+
+def test_create_validation_errors():
+    Jr, Jd = synth.torus_pm1(8, 8, 1)
+    assert _code(L.ising_create_grid, 7, 8, Jr, Jd, **_desc())[0] == L.ISING_E_ARG
+    assert _code(L.ising_create_grid, 2, 8, Jr[:16], Jd[:16], **_desc())[0] == L.ISING_E_ARG
+    bad = Jr.copy(); bad[5] = 0
+    c, msg = _code(L.ising_create_grid, 8, 8, bad, Jd, **_desc())
+    assert c == L.ISING_E_GRAPH and "J_right[5]" in msg
+    assert _code(L.ising_create_grid, 8, 8, Jr, Jd, **_desc(n_temps=48, betas=synth.beta_ladder(48)))[0] == L.ISING_E_ARG
+    b = synth.beta_ladder(32); b[3] = b[2]
+    assert _code(L.ising_create_grid, 8, 8, Jr, Jd, **_desc(betas=b))[0] == L.ISING_E_ARG
+    assert _code(L.ising_create_grid, 8, 8, Jr, Jd, **_desc(copy_begin=1, copy_end=1))[0] == L.ISING_E_ARG
+    # CSR invariants
+    rp = np.array([0, 1, 2], np.int64)
+    assert _code(L.ising_create_csr, 2, rp, np.array([0, 0], np.int32), np.array([1, 1], np.int32), **_desc())[0] == L.ISING_E_GRAPH  # self-loop
+    assert _code(L.ising_create_csr, 2, rp, np.array([1, 0], np.int32), np.array([1, -1], np.int32), **_desc())[0] == L.ISING_E_GRAPH  # asymmetric w
+    assert _code(L.ising_create_csr, 2, rp, np.array([1, 5], np.int32), np.array([1, 1], np.int32), **_desc())[0] == L.ISING_E_GRAPH  # range
+    rp3 = np.array([0, 2, 3, 4], np.int64)
+    assert _code(L.ising_create_csr, 3, rp3, np.array([1, 1, 0, 0], np.int32), np.ones(4, np.int32), **_desc())[0] == L.ISING_E_GRAPH  # duplicate
+    # improper colouring
+    c, msg = _code(L.ising_create_csr, 2, rp, np.array([1, 0], np.int32), np.array([1, 1], np.int32),
+                   colour=np.array([0, 0], np.int32), **_desc())
+    assert c == L.ISING_E_GRAPH and "colour" in msg
+    # weights other than +-1 are not supported by the bit-packed kernels
+    assert _code(L.ising_create_csr, 2, rp, np.array([1, 0], np.int32), np.array([2, 2], np.int32), **_desc())[0] == L.ISING_E_UNSUPPORTED
+    # I8 needs K % 4 == 0; BITS needs K % 32 == 0
+    assert _code(L.ising_create_csr, 2, rp, np.array([1, 0], np.int32), np.array([2, 2], np.int32),
+                 **_desc(layout="i8", n_temps=6, betas=synth.beta_ladder(6)))[0] == L.ISING_E_ARG
+
+
+def test_no_cpu_fallback_without_gpu():
+    """A valid create on a box without a usable GPU fails loudly (no CPU path)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present")
+    except ImportError:
+        pass
+    Jr, Jd = synth.torus_pm1(8, 8, 1)
+    c, msg = _code(L.ising_create_grid, 8, 8, Jr, Jd, **_desc())
+    assert c in (L.ISING_E_CUDA, L.ISING_E_OOM)
