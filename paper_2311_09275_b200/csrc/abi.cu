@@ -91,7 +91,8 @@ struct ising_handle {
     double *d_Ef = nullptr;
     int64_t *d_walker = nullptr;
     uint32_t *d_swapmask = nullptr;
-    uint32_t *d_jword = nullptr, *d_planes = nullptr;
+    uint8_t *d_jbyte = nullptr;
+    uint32_t *d_planes = nullptr;
     int32_t *d_rp = nullptr, *d_col = nullptr, *d_wi = nullptr, *d_class_off = nullptr;
     uint32_t *d_nbr = nullptr, *d_orig = nullptr, *d_o2i = nullptr;
     float *d_wf = nullptr, *d_betaf = nullptr;
@@ -268,7 +269,8 @@ int refresh_energy(ising_handle *h)
         GridBitsParams p{};
         p.state_in = h->d_state[h->cur];
         p.state_out = h->d_state[h->cur ^ 1];
-        p.jword = h->d_jword;
+        p.jbyte = h->d_jbyte;
+        p.qcap = grid_bits_qcap(h->n);
         p.planes = h->d_planes;
         p.E_out = h->d_E;
         p.Lx = h->Lx; p.Ly = h->Ly; p.n = h->n; p.hx = h->Lx / 2; p.half = h->n / 2;
@@ -489,7 +491,8 @@ int launch_sweeps(ising_handle *h, int32_t ns)
         GridBitsParams p{};
         p.state_in = h->d_state[h->cur];
         p.state_out = h->d_state[h->cur ^ 1];
-        p.jword = h->d_jword;
+        p.jbyte = h->d_jbyte;
+        p.qcap = grid_bits_qcap(h->n);
         p.planes = h->d_planes;
         p.E_out = h->d_E;
         p.Lx = h->Lx; p.Ly = h->Ly; p.n = h->n; p.hx = h->Lx / 2; p.half = h->n / 2;
@@ -705,7 +708,7 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
     for (int32_t i = 0; i < n; ++i)
         h->W_int += J_right[i] + J_down[i];
     h->smem = grid_bits_smem(n);
-    if (h->smem > 200 * 1024)
+    if (n > 65536 || grid_bits_qcap(n) < 1 || h->smem > 200 * 1024)
         return fail(ISING_E_UNSUPPORTED, "BITS grid: lattice too large for shared memory (n=" +
                                              std::to_string(n) + ")");
     const int32_t hx = Lx / 2, half = n / 2;
@@ -713,35 +716,35 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
     for (int32_t l = 0; l < half; ++l)
         if ((int32_t)(((uint64_t)l * h->ymagic) >> 32) != l / hx)
             return fail(ISING_E_UNSUPPORTED, "grid index magic not exact");
-    const int32_t per_thread = 4 * ((half + h->threads - 1) / h->threads);
-    h->cnt_levels = 1;
-    while ((1 << h->cnt_levels) <= per_thread)
-        ++h->cnt_levels;
-    if (h->cnt_levels > 8)
-        return fail(ISING_E_UNSUPPORTED, "too many sites per thread for the energy counter");
-    // jword in colour-separated order
-    std::vector<uint32_t> jw(n);
+    // 2-D thread mapping of k_grid_bits: column of a class row per thread, rows in passes
+    if (hx > h->threads)
+        return fail(ISING_E_UNSUPPORTED, "BITS grid needs block_threads >= Lx/2");
+    const int32_t rpp = h->threads / hx, npass = (Ly + rpp - 1) / rpp;
+    if (npass > 31)
+        return fail(ISING_E_UNSUPPORTED, "BITS grid: too many rows per thread (Ly/(threads/(Lx/2)) > 31)");
+    // J bytes in colour-separated order: bit 0..3 = (right, left, down, up) bond has J = -1
+    std::vector<uint8_t> jb(n);
     for (int32_t c = 0; c < 2; ++c)
         for (int32_t y = 0; y < Ly; ++y)
             for (int32_t mm = 0; mm < hx; ++mm) {
                 const int32_t x = 2 * mm + ((c + y) & 1);
                 const int32_t i = x + Lx * y;
                 const int32_t l = (x + Lx - 1) % Lx + Lx * y, u = x + Lx * ((y + Ly - 1) % Ly);
-                uint32_t v = 0;
-                if (J_right[i] < 0) v |= 0x80u;
-                if (J_right[l] < 0) v |= 0x80u << 8;
-                if (J_down[i] < 0) v |= 0x80u << 16;
-                if (J_down[u] < 0) v |= 0x80u << 24;
-                jw[c * half + y * hx + mm] = v;
+                uint8_t v = 0;
+                if (J_right[i] < 0) v |= 1;
+                if (J_right[l] < 0) v |= 2;
+                if (J_down[i] < 0) v |= 4;
+                if (J_down[u] < 0) v |= 8;
+                jb[c * half + y * hx + mm] = v;
             }
     std::vector<uint32_t> planes;
     plane_table(h->betas, {2, 4}, planes);
     rc = build_common_device(h.get(), 2 * (int64_t)n);
     if (rc)
         return rc;
-    CK(h->alloc(&h->d_jword, n));
+    CK(h->alloc(&h->d_jbyte, n));
     CK(h->alloc(&h->d_planes, planes.size()));
-    CK(cudaMemcpyAsync(h->d_jword, jw.data(), (size_t)n * 4, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(h->d_jbyte, jb.data(), (size_t)n, cudaMemcpyHostToDevice, h->st));
     CK(cudaMemcpyAsync(h->d_planes, planes.data(), planes.size() * 4, cudaMemcpyHostToDevice, h->st));
     CK(h->alloc(&h->d_state[0], (size_t)h->G * n));
     CK(h->alloc(&h->d_state[1], (size_t)h->G * n));

@@ -26,7 +26,7 @@ struct BestDev {
 struct GridBitsParams {
     const uint32_t *state_in;  // [G][n], original site order
     uint32_t *state_out;
-    const uint32_t *jword;     // [n] colour-separated order: bytes right,left,down,up; 0x80 = J=-1
+    const uint8_t *jbyte;      // [n] colour-separated order: bit 0..3 = right,left,down,up has J=-1
     const uint32_t *planes;    // [K/32][2][64]: index 0 = dE 4, 1 = dE 8
     int64_t *E_out;            // [R_local]
     int32_t Lx, Ly, n, hx, half;
@@ -36,6 +36,7 @@ struct GridBitsParams {
     uint32_t t0;
     int32_t n_sweeps;
     int32_t cnt_levels;        // bits of the per-thread energy counter
+    int32_t qcap;              // capacity of the shared-memory tail queue
     RoundKeys rk;
 };
 
@@ -107,6 +108,7 @@ cudaError_t launch_init_i8(int8_t *s, int32_t n, int32_t R, const uint32_t *orig
 cudaError_t launch_grid_bits(const GridBitsParams &p, int32_t G, int32_t threads, size_t smem,
                              cudaStream_t st);
 size_t grid_bits_smem(int32_t n);
+int32_t grid_bits_qcap(int32_t n);
 cudaError_t launch_csr_bits(const CsrBitsParams &p, int32_t G, int32_t threads, size_t smem,
                             cudaStream_t st);
 size_t csr_bits_smem(int32_t n, int32_t qmax, int32_t words_per_copy);

@@ -4,11 +4,10 @@
 // spin-glass tori, Table I).  One CTA owns one 32-replica word
 // group g (32 consecutive global slots = 32 temperatures of one copy) for all
 // n sites and keeps it resident in shared memory for a whole ising_sweep call:
-// load -> n_sweeps x {colour 0, colour 1} with __syncthreads between phases ->
-// energy of the 32 replicas -> store.  Shared memory holds the spins in
-// colour-separated order (each colour class contiguous per row), so lane l of
-// a warp touches word l of a row: conflict-free LDS/STS for the site and all
-// four neighbours.
+// load -> n_sweeps x {colour 0, colour 1} -> energy of the 32 replicas -> store.
+// Shared memory holds the spins in colour-separated order (each colour class
+// contiguous per row), so lane l of a warp touches word l of a row:
+// conflict-free LDS/STS for the site and all four neighbours.
 //
 // Per (site, word) -- 32 attempts at once, bit b = slot 32g+b:
 //   a_b   = ~(s_i ^ s_j ^ J_b)                 unsatisfied-bond bits (J_b s_i s_j = +1)
@@ -16,70 +15,219 @@
 //   m8/m4 = lanes with dE = 8 / 4 (u = 0 / 1); all other lanes flip (dE <= 0).
 //   PLANE contract: U64 bit (63-j) = bit b of word (j&3) of
 //       Philox(i, t, g, PLANE<<24 | j>>2); accept iff U64 < T[beta_k][dE].
-//   The comparison runs MSB plane first over the 32 undecided lanes D:
-//       lt |= D & ~u_j & t_j;  D &= ~(u_j ^ t_j)
+//   The comparison runs MSB plane first over the undecided lanes D:
+//       acc |= D & ~u_j & t_j;  D &= ~(u_j ^ t_j)
 //   and stops when D is empty (the first differing bit fixes U < T), so the
-//   result is exactly the 64-bit comparison.
-//   t_j (threshold plane j of the word's 32 temperatures) comes from the host
-//   plane table P[wt][dE][j]; slot temperatures never change (exchanges move
+//   result is exactly the 64-bit comparison.  t_j (threshold
+//   plane j of the word's 32 temperatures) comes from the host plane table
+//   P[wt][dE][j]; slot temperatures never change (exchanges move
 //   configurations), so the table is fixed for the whole run.
+//
+// Work compaction of the RNG tail: a colour phase runs in two
+// stages.  Stage 1: every site draws planes 0..7 (two Philox calls); ~89% of
+// words are then decided and written.  The rest are pushed to a shared-memory
+// queue and stage 2 finishes them with all 32 lanes of a warp busy, instead of
+// leaving most lanes of a warp idle while one lane draws its 3rd/4th call.
+// Philox rounds 0-1 are partially hoisted: the parts that depend only on the
+// CTA's group g, the sweep t or the site i are computed once, not per call.
 #include "internal.h"
 
 namespace ising {
 
-size_t grid_bits_smem(int32_t n) { return (size_t)(2 * n + 128) * sizeof(uint32_t); }
-
 namespace {
+
+constexpr uint32_t kM0 = 0xD2511F53u, kM1 = 0xCD9E8D57u;
+constexpr int kCntLevels = 12;  // per-thread counter + 5 butterfly levels
+constexpr int kQItemBytes = 20;
 
 struct GridGeom {
     int32_t Lx, Ly, hx, half;
     uint32_t ymagic;
 };
 
-// Neighbour words of colour-c site with class index l; returns the four
-// unsatisfied-bond masks and the original site id.
-__device__ __forceinline__ void grid_unsat(const uint32_t *S, const uint32_t *JW, const GridGeom &G,
-                                           int c, int l, uint32_t own, uint32_t &a0, uint32_t &a1,
-                                           uint32_t &a2, uint32_t &a3, uint32_t &i_orig)
+// Uniform (per CTA, per sweep) parts of Philox rounds 0-1 for counter
+// (i, t, g, PLANE<<24 | j4).
+struct PlaneUniform {
+    uint32_t U0;    // lo(M1*g) ^ K0_1
+    uint32_t L0r1;  // lo(M0*A),  A = hi(M1*g) ^ t ^ K0_0
+    uint32_t H0r1;  // hi(M0*A)
+};
+
+__device__ __forceinline__ PlaneUniform plane_uniform(uint32_t g, uint32_t t, const RoundKeys &rk)
 {
-    const int y = (int)__umulhi((uint32_t)l, G.ymagic);
-    const int m = l - y * G.hx;
+    const uint32_t H1g = __umulhi(kM1, g), L1g = kM1 * g;
+    const uint32_t A = H1g ^ t ^ rk.k[0];
+    PlaneUniform u;
+    u.U0 = L1g ^ rk.k[2];
+    u.L0r1 = kM0 * A;
+    u.H0r1 = __umulhi(kM0, A);
+    return u;
+}
+
+// Per-site parts: sA = hi(M0*i) ^ (PLANE<<24) ^ K1_0, sB = H0r1 ^ lo(M0*i) ^ K1_1.
+__device__ __forceinline__ void plane_site(uint32_t i, const PlaneUniform &u, const RoundKeys &rk,
+                                           uint32_t &sA, uint32_t &sB)
+{
+    const uint32_t H0 = __umulhi(kM0, i), L0 = kM0 * i;
+    sA = H0 ^ (ST_PLANE << 24) ^ rk.k[1];
+    sB = u.H0r1 ^ L0 ^ rk.k[3];
+}
+
+// Philox4x32-10 of counter (i, t, g, PLANE<<24 | j4) from the hoisted parts.
+__device__ __forceinline__ uint4 philox_plane(uint32_t sA, uint32_t sB, uint32_t j4,
+                                              const PlaneUniform &u, const RoundKeys &rk)
+{
+    const uint32_t X = sA ^ j4;  // round-0 output word 2 (j4 < 2^24)
+    uint32_t c0 = __umulhi(kM1, X) ^ u.U0;
+    uint32_t c1 = kM1 * X;
+    uint32_t c2 = sB;
+    uint32_t c3 = u.L0r1;
+#pragma unroll
+    for (int r = 2; r < 10; ++r) {
+        const uint32_t lo0 = kM0 * c0, hi0 = __umulhi(kM0, c0);
+        const uint32_t lo1 = kM1 * c2, hi1 = __umulhi(kM1, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ rk.k[2 * r];
+        const uint32_t n2 = hi0 ^ c3 ^ rk.k[2 * r + 1];
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+__device__ __forceinline__ uint32_t mux(uint32_t m, uint32_t a, uint32_t b) { return (m & a) | (~m & b); }
+
+// Planes 4*j4 .. 4*j4+3 of the lazy MSB-first comparison.  Lanes in D have
+// dE = 8 (m8 set) or dE = 4 (m8 clear); P4/P8 are the word type's planes.
+__device__ __forceinline__ void plane_call(uint32_t sA, uint32_t sB, uint32_t j4, const PlaneUniform &u,
+                                           const RoundKeys &rk, const uint32_t *P, uint32_t m8,
+                                           uint32_t &D, uint32_t &acc)
+{
+    const uint4 w = philox_plane(sA, sB, j4, u, rk);
+    const uint4 q4 = *reinterpret_cast<const uint4 *>(P + 4 * j4);
+    const uint4 q8 = *reinterpret_cast<const uint4 *>(P + 64 + 4 * j4);
+    const uint32_t t0 = mux(m8, q8.x, q4.x);
+    const uint32_t y0 = D & ~w.x & t0;
+    D &= ~(w.x ^ t0);
+    const uint32_t t1 = mux(m8, q8.y, q4.y);
+    const uint32_t y1 = D & ~w.y & t1;
+    D &= ~(w.y ^ t1);
+    acc |= y0 | y1;
+    const uint32_t t2 = mux(m8, q8.z, q4.z);
+    const uint32_t y2 = D & ~w.z & t2;
+    D &= ~(w.z ^ t2);
+    const uint32_t t3 = mux(m8, q8.w, q4.w);
+    const uint32_t y3 = D & ~w.w & t3;
+    D &= ~(w.w ^ t3);
+    acc |= y2 | y3;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt()
+{
+    uint32_t r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+// Bit-sliced addition of two L-bit vertical numbers (no overflow beyond L bits:
+// the caller sizes L for the warp total).
+template <int L>
+__device__ __forceinline__ void vsum_xor(uint32_t (&c)[L], int off)
+{
+    uint32_t carry = 0u;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, c[l], off);
+        const uint32_t s = c[l] ^ o ^ carry;
+        carry = (c[l] & o) | (carry & (c[l] ^ o));
+        c[l] = s;
+    }
+}
+
+// Site geometry of one thread in the 2-D mapping (column m of a colour class,
+// rows ty, ty + rpp, ...).
+struct ThreadGeom {
+    int m, mL, mR;  // class column and its wrapped neighbours
+    int ty;
+    bool active;
+};
+
+__device__ __forceinline__ void site_unsat(const uint32_t *S, const uint8_t *JB, const GridGeom &G,
+                                           const ThreadGeom &T, int c, int y, uint32_t own,
+                                           uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3,
+                                           uint32_t &i_orig)
+{
     const int par = (c + y) & 1;
-    const int x = 2 * m + par;
-    const int mr = par ? (m + 1 == G.hx ? 0 : m + 1) : m;
-    const int ml = par ? m : (m == 0 ? G.hx - 1 : m - 1);
     const int yd = (y + 1 == G.Ly) ? 0 : y + 1;
     const int yu = (y == 0) ? G.Ly - 1 : y - 1;
-    const int ob = (1 - c) * G.half;
-    const uint32_t xr = S[ob + y * G.hx + mr];
-    const uint32_t xl = S[ob + y * G.hx + ml];
-    const uint32_t xd = S[ob + yd * G.hx + m];
-    const uint32_t xu = S[ob + yu * G.hx + m];
-    const uint32_t jw = JW[c * G.half + l];
+    const uint32_t *So = S + (1 - c) * G.half;
+    const int row = y * G.hx;
+    const uint32_t xr = So[row + (par ? T.mR : T.m)];
+    const uint32_t xl = So[row + (par ? T.m : T.mL)];
+    const uint32_t xd = So[yd * G.hx + T.m];
+    const uint32_t xu = So[yu * G.hx + T.m];
+    const uint32_t jw = (uint32_t)JB[c * G.half + row + T.m] * 0x10204080u;
     a0 = ~(own ^ xr ^ byte_sign_mask<0>(jw));
     a1 = ~(own ^ xl ^ byte_sign_mask<1>(jw));
     a2 = ~(own ^ xd ^ byte_sign_mask<2>(jw));
     a3 = ~(own ^ xu ^ byte_sign_mask<3>(jw));
-    i_orig = (uint32_t)(x + G.Lx * y);
+    i_orig = (uint32_t)(2 * T.m + par + G.Lx * y);
 }
-
-constexpr int kCntLevels = 8;
 
 }  // namespace
 
+int32_t grid_bits_qcap(int32_t n)
+{
+    const size_t base = (size_t)4 * n + (((size_t)n + 15) & ~(size_t)15) + 512;
+    const size_t half = (size_t)n / 2;
+    size_t qcap = half < 4096 ? half : 4096;
+    const size_t budget = 200 * 1024;
+    if (base + qcap * kQItemBytes > budget)
+        qcap = base < budget ? (budget - base) / kQItemBytes : 0;
+    return (int32_t)qcap;
+}
+
+size_t grid_bits_smem(int32_t n)
+{
+    // S (4n) + JB (n, padded to 16) + planes (512) + queue
+    return (size_t)4 * n + (((size_t)n + 15) & ~(size_t)15) + 512 +
+           (size_t)grid_bits_qcap(n) * kQItemBytes;
+}
+
 __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
 {
-    extern __shared__ uint32_t sm[];
+    extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t Ucnt[32];
+    __shared__ int32_t wcount[33];
+    __shared__ int32_t wprefix[33];
     const int n = p.n;
-    GridGeom G{p.Lx, p.Ly, p.hx, p.half, p.ymagic};
+    const GridGeom G{p.Lx, p.Ly, p.hx, p.half, p.ymagic};
     uint32_t *S = sm;
-    uint32_t *JW = sm + n;
-    uint32_t *P = sm + 2 * n;  // P[0..63]: dE=4 planes, P[64..127]: dE=8 planes
+    uint8_t *JB = reinterpret_cast<uint8_t *>(sm + n);
+    uint32_t *P = reinterpret_cast<uint32_t *>(JB + ((n + 15) & ~15));  // P[0..63] dE=4, P[64..127] dE=8
+    uint32_t *Q = P + 128;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = nt >> 5;
+    const int qcap = p.qcap;
+    const int wcap = qcap / nwarps;  // per-warp queue region
+    uint32_t *q_idx = Q, *q_own = Q + qcap, *q_D = Q + 2 * qcap, *q_acc = Q + 3 * qcap,
+             *q_m8 = Q + 4 * qcap;
+    const int wq0 = warp * wcap;
+
     const int gl = blockIdx.x;
     const uint32_t g = p.g0 + (uint32_t)gl;
     const int wt = (int)(g % (uint32_t)p.words_per_copy);
-    const int tid = threadIdx.x, nt = blockDim.x;
+
+    // 2-D thread mapping: column m = tid % hx of a class row, rows ty + k*rpp
+    const int rpp = nt / G.hx;  // rows per pass (host guarantees >= 1)
+    const int npass = (G.Ly + rpp - 1) / rpp;
+    ThreadGeom T;
+    T.ty = tid / G.hx;
+    T.m = tid - T.ty * G.hx;
+    T.mL = T.m == 0 ? G.hx - 1 : T.m - 1;
+    T.mR = T.m + 1 == G.hx ? 0 : T.m + 1;
+    T.active = T.ty < rpp;
 
     // ---- load: original order -> colour-separated order
     const uint32_t *src = p.state_in + (size_t)gl * n;
@@ -88,7 +236,7 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
         S[((x + y) & 1) * G.half + y * G.hx + (x >> 1)] = src[i];
     }
     for (int l = tid; l < n; l += nt)
-        JW[l] = p.jword[l];
+        JB[l] = p.jbyte[l];
     for (int j = tid; j < 128; j += nt)
         P[j] = p.planes[wt * 128 + j];
     if (tid < 32)
@@ -98,39 +246,101 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
     // ---- sweeps
     for (int s = 0; s < p.n_sweeps; ++s) {
         const uint32_t t = p.t0 + (uint32_t)s;
+        const PlaneUniform U = plane_uniform(g, t, p.rk);
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) {
             uint32_t *Sc = S + c * G.half;
-            for (int l = tid; l < G.half; l += nt) {
-                const uint32_t own = Sc[l];
-                uint32_t a0, a1, a2, a3, i_orig;
-                grid_unsat(S, JW, G, c, l, own, a0, a1, a2, a3, i_orig);
-                const uint32_t s01 = a0 ^ a1, c01 = a0 & a1;
-                const uint32_t s23 = a2 ^ a3, c23 = a2 & a3;
-                const uint32_t m8 = ~(s01 | c01 | s23 | c23);  // u = 0 -> dE = 8
-                const uint32_t m4 = (s01 ^ s23) & ~(c01 | c23); // u = 1 -> dE = 4
-                uint32_t D = m8 | m4, lt = 0;
-                if (D) {
-                    uint32_t j4 = 0;
-                    do {
-                        const uint4 w = philox(i_orig, t, g, (ST_PLANE << 24) | j4, p.rk);
-                        const uint4 q4 = *reinterpret_cast<const uint4 *>(P + 4 * j4);
-                        const uint4 q8 = *reinterpret_cast<const uint4 *>(P + 64 + 4 * j4);
-#define PLANE_STEP(U, T4, T8)                                   \
-    {                                                           \
-        const uint32_t tj = (m4 & (T4)) | (m8 & (T8));          \
-        lt |= D & ~(U) & tj;                                    \
-        D &= ~((U) ^ tj);                                       \
-    }
-                        PLANE_STEP(w.x, q4.x, q8.x)
-                        PLANE_STEP(w.y, q4.y, q8.y)
-                        PLANE_STEP(w.z, q4.z, q8.z)
-                        PLANE_STEP(w.w, q4.w, q8.w)
-#undef PLANE_STEP
-                        ++j4;
-                    } while (D && j4 < 16u);
+            // stage 1: planes 0..7 for every site; undecided words go to this warp's queue
+            int wq = 0;  // warp-uniform
+            for (int pass = 0; pass < npass; ++pass) {
+                const int y = T.ty + pass * rpp;
+                const bool valid = T.active && y < G.Ly;
+                const int l = y * G.hx + T.m;
+                uint32_t own = 0, D = 0, acc = 0, m8 = 0, i_orig = 0;
+                if (valid) {
+                    own = Sc[l];
+                    uint32_t a0, a1, a2, a3;
+                    site_unsat(S, JB, G, T, c, y, own, a0, a1, a2, a3, i_orig);
+                    const uint32_t s01 = a0 ^ a1, c01 = a0 & a1;
+                    const uint32_t s23 = a2 ^ a3, c23 = a2 & a3;
+                    m8 = ~(s01 | c01 | s23 | c23);                   // u = 0 -> dE = 8
+                    const uint32_t m4 = (s01 ^ s23) & ~(c01 | c23);  // u = 1 -> dE = 4
+                    D = m8 | m4;
+                    acc = ~D;  // dE <= 0 always flips
+                    if (D) {
+                        uint32_t sA, sB;
+                        plane_site(i_orig, U, p.rk, sA, sB);
+                        plane_call(sA, sB, 0u, U, p.rk, P, m8, D, acc);
+                        if (D)
+                            plane_call(sA, sB, 1u, U, p.rk, P, m8, D, acc);
+                    }
                 }
-                Sc[l] = own ^ (~(m8 | m4) | lt);
+                const bool need = D != 0u;
+                const uint32_t pm = __ballot_sync(0xFFFFFFFFu, need);
+                const int slot = wq + __popc(pm & lanemask_lt());
+                wq += __popc(pm);
+                if (need && slot < wcap) {
+                    const int qs = wq0 + slot;
+                    q_idx[qs] = (uint32_t)l | (i_orig << 16);
+                    q_own[qs] = own;
+                    q_D[qs] = D;
+                    q_acc[qs] = acc;
+                    q_m8[qs] = m8;
+                } else if (valid) {
+                    if (need) {  // this warp's queue region is full: finish inline
+                        uint32_t sA, sB;
+                        plane_site(i_orig, U, p.rk, sA, sB);
+                        uint32_t j4 = 2;
+                        do {
+                            plane_call(sA, sB, j4, U, p.rk, P, m8, D, acc);
+                            ++j4;
+                        } while (D && j4 < 16u);
+                    }
+                    Sc[l] = own ^ acc;
+                }
+            }
+            if (lane == 0)
+                wcount[warp] = min(wq, wcap);
+            __syncthreads();
+            if (warp == 0) {  // exclusive prefix over the warp regions
+                int v = lane < nwarps ? wcount[lane] : 0;
+                int incl = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= o)
+                        incl += u;
+                }
+                wprefix[lane] = incl - v;
+                if (lane == 31)
+                    wprefix[32] = incl;
+            }
+            __syncthreads();
+            // stage 2: the queued tail, one word per thread, all lanes busy
+            const int nq = wprefix[32];
+            for (int q = tid; q < nq; q += nt) {
+                int lo = 0, hi = nwarps;  // find region w: wprefix[w] <= q < wprefix[w+1]
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (wprefix[mid] <= q)
+                        lo = mid;
+                    else
+                        hi = mid;
+                }
+                const int qs = lo * wcap + (q - wprefix[lo]);
+                const uint32_t idx = q_idx[qs];
+                const int l = (int)(idx & 0xFFFFu);
+                const uint32_t i_orig = idx >> 16;
+                uint32_t D = q_D[qs], acc = q_acc[qs];
+                const uint32_t m8 = q_m8[qs];
+                uint32_t sA, sB;
+                plane_site(i_orig, U, p.rk, sA, sB);
+                uint32_t j4 = 2;
+                do {
+                    plane_call(sA, sB, j4, U, p.rk, P, m8, D, acc);
+                    ++j4;
+                } while (D && j4 < 16u);
+                Sc[l] = q_own[qs] ^ acc;
             }
             __syncthreads();
         }
@@ -144,27 +354,25 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
         for (int l = 0; l < kCntLevels; ++l)
             cnt[l] = 0;
         const uint32_t *S1 = S + G.half;
-        for (int l = tid; l < G.half; l += nt) {
-            uint32_t a0, a1, a2, a3, i_orig;
-            grid_unsat(S, JW, G, 1, l, S1[l], a0, a1, a2, a3, i_orig);
-            vadd(cnt, a0);
-            vadd(cnt, a1);
-            vadd(cnt, a2);
-            vadd(cnt, a3);
-        }
-        const int lane = tid & 31;
-        int32_t acc = 0;
-#pragma unroll
-        for (int l = 0; l < kCntLevels; ++l) {
-            if (l >= p.cnt_levels)
-                continue;
-#pragma unroll 4
-            for (int b = 0; b < 32; ++b) {
-                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (cnt[l] >> b) & 1u);
-                if (lane == b)
-                    acc += __popc(bal) << l;
+        for (int pass = 0; pass < npass; ++pass) {
+            const int y = T.ty + pass * rpp;
+            if (T.active && y < G.Ly) {
+                uint32_t a0, a1, a2, a3, i_orig;
+                site_unsat(S, JB, G, T, 1, y, S1[y * G.hx + T.m], a0, a1, a2, a3, i_orig);
+                vadd(cnt, a0);
+                vadd(cnt, a1);
+                vadd(cnt, a2);
+                vadd(cnt, a3);
             }
         }
+        // warp total by a butterfly of bit-sliced additions, then lane b reads bit b
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+            vsum_xor(cnt, off);
+        int32_t acc = 0;
+#pragma unroll
+        for (int l = 0; l < kCntLevels; ++l)
+            acc += (int32_t)((cnt[l] >> lane) & 1u) << l;
         atomicAdd(&Ucnt[lane], acc);
         __syncthreads();
         if (tid < 32)
