@@ -211,7 +211,7 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
-def roofline_entry(kernel_ms, attempts_per_launch, layout, clocks):
+def roofline_entry(kernel_ms, attempts_per_launch, layout, clocks, workload="c2"):
     """Roofline of the dominant kernel.  Bit-packed sweeps are issue (ALU) bound: achieved
     = warp instructions per launch (ncu-measured per attempt, profiles/inst_per_attempt.json,
     times the live attempts per launch) / live CUDA-event launch time; peak = 148 SMs x 4
@@ -220,7 +220,7 @@ def roofline_entry(kernel_ms, attempts_per_launch, layout, clocks):
     mhz = peaks.get("sm_max_mhz", 1965.0)
     ipa = None
     if os.path.exists(PROFILE_FILE):
-        ipa = json.load(open(PROFILE_FILE)).get(layout)
+        ipa = json.load(open(PROFILE_FILE)).get(workload)
     if layout == "i8":
         # int8 per-lane sweeps: HBM bound; algorithmic bytes per attempt stated in DESIGN.md
         bpa = ipa.get("alg_bytes_per_attempt", 5.11) if ipa else 5.11
@@ -327,7 +327,7 @@ def run_ours(args):
     ms_step = total_ms / args.steps
     avg_launch_ms = kernel_ms / max(nk, 1)
     per_launch_attempts = n * R * (kex if kex > 0 else sweeps)
-    roof = roofline_entry(avg_launch_ms, per_launch_attempts, cfg["layout"], clk)
+    roof = roofline_entry(avg_launch_ms, per_launch_attempts, cfg["layout"], clk, args.workload)
     roof["kernel"] = "k_grid_bits" if (inst["kind"] == "grid" and cfg["layout"] == "bits") else \
         ("k_csr_bits" if cfg["layout"] == "bits" else "k_csr_i8_phase")
     roof["kernel_share_of_step"] = kernel_ms / max(total_ms * (1 if world == 1 else 1), 1e-9)

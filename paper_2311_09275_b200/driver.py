@@ -118,13 +118,28 @@ def best_key(rec):
     return (rec["E"], rec["sweep"], rec["slot"])
 
 
+def all_gather(recv, send, group=None):
+    """all_gather_into_tensor where the backend has it (NCCL), list all_gather otherwise."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(recv, send, group=group)
+        return
+    world = dist.get_world_size(group)
+    parts = list(torch.chunk(recv, world, dim=0))
+    bufs = [torch.empty_like(p) for p in parts]
+    dist.all_gather(bufs, send, group=group)
+    for p, b in zip(parts, bufs):
+        p.copy_(b)
+
+
 def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True):
     """PT schedule: rounds of k_ex sweeps + (best check, exchange); final check.
 
     k_ex <= 0 -> plain Metropolis (no exchange), one best check at the end.
     Returns the global best record {E, slot, sweep} (same on every rank)."""
-    import torch.distributed as dist  # only needed for group != None
-    world = dist.get_world_size(group) if group is not None else 1
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
     multi = world > 1
     done = 0
     if multi and gather:
@@ -135,7 +150,7 @@ def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True):
             done += k_ex
             if multi and gather:
                 engine.exchange_begin(send)
-                dist.all_gather_into_tensor(recv, send, group=group)
+                all_gather(recv, send, group)
                 engine.exchange_end(recv)
             else:
                 engine.exchange()
@@ -143,7 +158,7 @@ def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True):
         engine.sweep(sweeps - done)
         if multi and gather:
             engine.exchange_begin(send)
-            dist.all_gather_into_tensor(recv, send, group=group)
+            all_gather(recv, send, group)
             engine.check_best(recv)
         else:
             engine.check_best()
@@ -165,7 +180,7 @@ def merge_best_over_ranks(rec, group):
     mine = torch.tensor([[float(E) if is_float else int(E), rec["sweep"], rec["slot"]]],
                         dtype=torch.float64 if is_float else torch.int64, device=dev)
     allr = torch.empty((world, 3), dtype=mine.dtype, device=dev)
-    dist.all_gather_into_tensor(allr, mine, group=group)
+    all_gather(allr, mine, group)
     rows = allr.cpu().numpy()
     order = np.lexsort((rows[:, 2], rows[:, 1], rows[:, 0]))
     r = rows[order[0]]
