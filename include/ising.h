@@ -225,6 +225,11 @@ ISING_API const char *ising_version(void);
 ISING_API int ising_debug_philox(int32_t device, const uint32_t *in, int32_t n, uint32_t *out_lib,
                        uint32_t *out_curand);
 
+/* Exhaustive check of the fast float decision used by the I8 kernel: the maximum over
+ * every float x in [-64, 0] of |ex2.approx(x log2e + 32) / (cexp32(x) 2^32) - 1|.  The
+ * kernel's 2^-12 margin is exact-decision-safe when this is < 2^-13.  Syncs. */
+ISING_API int ising_debug_exp_bound(int32_t device, float *worst_rel);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,6 +94,7 @@ struct ising_handle {
     uint8_t *d_jbyte = nullptr;
     uint32_t *d_planes = nullptr;
     int32_t *d_rp = nullptr, *d_col = nullptr, *d_wi = nullptr, *d_class_off = nullptr;
+    int32_t *d_ell_col = nullptr, *d_ell_w = nullptr;
     uint32_t *d_nbr = nullptr, *d_orig = nullptr, *d_o2i = nullptr;
     float *d_wf = nullptr, *d_betaf = nullptr;
     uint64_t *d_T = nullptr, *d_Tx = nullptr;
@@ -460,17 +461,41 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
         if (wi) {
             CK(h->alloc(&h->d_wi, m2));
             CK(cudaMemcpyAsync(h->d_wi, wiv.data(), (size_t)m2 * 4, cudaMemcpyHostToDevice, h->st));
-            std::vector<uint64_t> T = accept_table(h->betas, h->qmax);
+            // per LOCAL replica r (temperature k = (slot0 + r) mod K): T_r[r][q], q = dE/2
+            std::vector<uint64_t> Tk = accept_table(h->betas, h->qmax);
+            std::vector<uint64_t> T((size_t)h->R * (h->qmax + 1));
+            for (int64_t r = 0; r < h->R; ++r) {
+                const int32_t k = (int32_t)((h->slot0 + r) % h->K);
+                std::copy(Tk.begin() + (size_t)k * (h->qmax + 1), Tk.begin() + (size_t)(k + 1) * (h->qmax + 1),
+                          T.begin() + (size_t)r * (h->qmax + 1));
+            }
             CK(h->alloc(&h->d_T, T.size()));
             CK(cudaMemcpyAsync(h->d_T, T.data(), T.size() * 8, cudaMemcpyHostToDevice, h->st));
         } else {
             CK(h->alloc(&h->d_wf, m2));
             CK(cudaMemcpyAsync(h->d_wf, wfv.data(), (size_t)m2 * 4, cudaMemcpyHostToDevice, h->st));
-            std::vector<float> bf(h->K);
-            for (int k = 0; k < h->K; ++k)
-                bf[k] = (float)h->betas[k];
-            CK(h->alloc(&h->d_betaf, h->K));
-            CK(cudaMemcpyAsync(h->d_betaf, bf.data(), h->K * 4, cudaMemcpyHostToDevice, h->st));
+            std::vector<float> bf(h->R);
+            for (int64_t r = 0; r < h->R; ++r)
+                bf[r] = (float)h->betas[(h->slot0 + r) % h->K];
+            CK(h->alloc(&h->d_betaf, h->R));
+            CK(cudaMemcpyAsync(h->d_betaf, bf.data(), h->R * 4, cudaMemcpyHostToDevice, h->st));
+        }
+        if (maxdeg <= 4) {
+            // padded 4-wide neighbour table (row order kept, pad col = -1, w = 0)
+            std::vector<int32_t> ec((size_t)n * 4, -1), ew((size_t)n * 4, 0);
+            for (int32_t v = 0; v < n; ++v)
+                for (int32_t u = 0; u < rp[v + 1] - rp[v]; ++u) {
+                    ec[(size_t)v * 4 + u] = ci[rp[v] + u];
+                    if (wi)
+                        ew[(size_t)v * 4 + u] = wiv[rp[v] + u];
+                    else
+                        std::memcpy(&ew[(size_t)v * 4 + u], &wfv[rp[v] + u], 4);
+                }
+            CK(h->alloc(&h->d_ell_col, ec.size()));
+            CK(h->alloc(&h->d_ell_w, ew.size()));
+            CK(cudaMemcpyAsync(h->d_ell_col, ec.data(), ec.size() * 4, cudaMemcpyHostToDevice, h->st));
+            CK(cudaMemcpyAsync(h->d_ell_w, ew.data(), ew.size() * 4, cudaMemcpyHostToDevice, h->st));
+            CK(cudaStreamSynchronize(h->st));  // host vectors die at scope end
         }
         CK(h->alloc(&h->d_s8, (size_t)n * h->R));
         h->scratch_bytes = energy_i8_scratch(n, (int32_t)h->R);
@@ -519,6 +544,15 @@ int launch_sweeps(ising_handle *h, int32_t ns)
         CsrI8Params p{};
         p.s = h->d_s8; p.rp = h->d_rp; p.col = h->d_col; p.wi = h->d_wi; p.wf = h->d_wf;
         p.orig = h->d_orig; p.T = h->d_T; p.betaf = h->d_betaf; p.R = (int32_t)h->R; p.K = h->K;
+        p.nq = (int32_t)(h->R / 4);
+        p.ell_col = h->d_ell_col;
+        p.ell_w = h->d_ell_w;
+        const int32_t tpv = (int32_t)(h->R % 8 == 0 ? h->R / 8 : h->R / 4);  // threads per vertex
+        p.nq_shift = -1;
+        for (int sh = 0; sh < 31; ++sh)
+            if ((1 << sh) == tpv)
+                p.nq_shift = sh;
+
         p.slot0 = h->slot0; p.qmax = h->qmax; p.rk = h->rk;
         const int32_t thr = h->threads > 256 ? 256 : h->threads;
         for (int32_t s = 0; s < ns; ++s) {
@@ -1053,6 +1087,22 @@ int ising_debug_philox(int32_t device, const uint32_t *in, int32_t n, uint32_t *
     cudaFree(d_in);
     cudaFree(d_a);
     cudaFree(d_b);
+    return ISING_OK;
+}
+
+int ising_debug_exp_bound(int32_t device, float *worst_rel)
+{
+    if (!worst_rel)
+        return fail(ISING_E_ARG, "worst_rel is NULL");
+    CK(cudaSetDevice(device));
+    uint32_t *d = nullptr;
+    CK(cudaMalloc(&d, 4));
+    CK(cudaMemset(d, 0, 4));
+    CK(launch_debug_exp_bound(d, nullptr));
+    uint32_t bits = 0;
+    CK(cudaMemcpy(&bits, d, 4, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    std::memcpy(worst_rel, &bits, 4);
     return ISING_OK;
 }
 

@@ -61,12 +61,16 @@ struct CsrI8Params {
     int8_t *s;                 // [n][R] internal vertex order, replica-minor
     const int32_t *rp;         // [n+1] internal
     const int32_t *col;        // internal ids
+    const int32_t *ell_col;    // [n][4] padded neighbour table (pad -1) or null (CSR path)
+    const int32_t *ell_w;      // [n][4] weights (int32 or float bits), pad 0
     const int32_t *wi;         // int weights or null
     const float *wf;           // float weights or null
     const uint32_t *orig;      // internal -> original id
-    const uint64_t *T;         // [K][qmax+1] integer thresholds (q = dE/2), int weights
-    const float *betaf;        // [K] float(beta_k), float weights
+    const uint64_t *T;         // [R][qmax+1] integer thresholds per LOCAL replica (q = dE/2)
+    const float *betaf;        // [R] float(beta_k) per LOCAL replica, float weights
     int32_t R;                 // local replicas (multiple of 4)
+    int32_t nq;                // R / 4
+    int32_t nq_shift;          // log2(threads per vertex) if a power of two, else -1
     int32_t K;
     int64_t slot0;             // first global slot
     int32_t qmax;
@@ -129,6 +133,7 @@ cudaError_t launch_extract_bits(const uint32_t *state, int32_t n, int32_t gl, in
                                 const uint32_t *perm_o2i, int8_t *out, cudaStream_t st);
 cudaError_t launch_insert_bits(uint32_t *state, int32_t n, int32_t gl, int32_t bit,
                                const uint32_t *perm_o2i, const int8_t *in, cudaStream_t st);
+cudaError_t launch_debug_exp_bound(uint32_t *out, cudaStream_t st);
 cudaError_t launch_debug_philox(const uint32_t *in, int32_t n, uint32_t *out_lib,
                                 uint32_t *out_curand, cudaStream_t st);
 

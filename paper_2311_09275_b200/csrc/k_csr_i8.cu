@@ -53,108 +53,256 @@ __device__ __forceinline__ uint64_t thr_f32(float betaf, float dE)
     return __float2ull_rz(v);
 }
 
-template <bool FLOAT>
-__device__ __forceinline__ void field4(const CsrI8Params &p, int32_t v, int32_t q, int32_t (&hi)[4],
-                                       float (&hf)[4])
+// Fast, exact decision of (hi:lo) < floor(cexp32(x) 2^64) for x = -(beta dE) < 0 from the
+// 32-bit word hi alone when it is far from the threshold: e = ex2.approx
+// estimate of cexp32(x) 2^32 with relative error <= 2^-13 (verified exhaustively over all
+// float x in [-64, 0] by tests/test_gpu_parity.py::test_exp_bracket_bound); margin 2^-12.
+// Returns 1 = accept, 0 = reject, -1 = undecided (caller evaluates the exact threshold).
+__device__ __forceinline__ int fast_decide(float x, uint32_t hi)
 {
-    const int32_t e0 = p.rp[v], e1 = p.rp[v + 1];
-    for (int32_t e = e0; e < e1; ++e) {
-        const int32_t j = __ldg(p.col + e);
-        const char4 nb = reinterpret_cast<const char4 *>(p.s + (size_t)j * p.R)[q];
-        if (FLOAT) {
-            const float w = __ldg(p.wf + e);
-            hf[0] = __fadd_rn(hf[0], nb.x > 0 ? w : -w);
-            hf[1] = __fadd_rn(hf[1], nb.y > 0 ? w : -w);
-            hf[2] = __fadd_rn(hf[2], nb.z > 0 ? w : -w);
-            hf[3] = __fadd_rn(hf[3], nb.w > 0 ? w : -w);
-        } else {
-            const int32_t w = __ldg(p.wi + e);
-            hi[0] += w * nb.x;
-            hi[1] += w * nb.y;
-            hi[2] += w * nb.z;
-            hi[3] += w * nb.w;
-        }
-    }
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fadd_rn(__fmul_rn(x, 0x1.715476p+0f), 32.0f)));
+    const float hf = __uint2float_rn(hi);
+    const bool in_range = x >= -64.0f;  // below -64 the contract threshold is exactly 0
+    const bool acc = in_range && __fadd_rn(hf, 2.0f) <= __fmul_rn(e, 1.0f - 0x1p-12f);
+    const bool rej = !in_range || hf >= __fmul_rn(e, 1.0f + 0x1p-12f);
+    return acc ? 1 : (rej ? 0 : -1);
 }
 
 }  // namespace
 
-template <bool FLOAT>
-__global__ void __launch_bounds__(256) k_csr_i8_phase(const CsrI8Params p)
+// Exhaustive check of the fast-decision bound: max over all float x in [-64, 0] of
+// |ex2.approx(x log2e + 32) / (cexp32(x) 2^32) - 1|, as float bits in *out (atomicMax).
+__global__ void k_debug_exp_bound(uint32_t *out)
 {
-    const int32_t nq = p.R >> 2;
-    const int64_t total = (int64_t)(p.v_end - p.v_begin) * nq;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t v = p.v_begin + (int32_t)(idx / nq);
-        const int32_t q = (int32_t)(idx % nq);
-        char4 *own_p = reinterpret_cast<char4 *>(p.s + (size_t)v * p.R) + q;
-        const char4 own = *own_p;
-        int32_t hi[4] = {0, 0, 0, 0};
-        float hf[4] = {0.f, 0.f, 0.f, 0.f};
-        field4<FLOAT>(p, v, q, hi, hf);
-        const int8_t sv[4] = {own.x, own.y, own.z, own.w};
-        bool flip[4];
-        uint64_t T[4];
-        bool need = false;
-        const int64_t r0 = p.slot0 + 4 * (int64_t)q;
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const int32_t k = (int32_t)((4 * q + a) % p.K);
-            if (FLOAT) {
-                const float dE = sv[a] > 0 ? __fmul_rn(-2.0f, hf[a]) : __fmul_rn(2.0f, hf[a]);
-                flip[a] = dE <= 0.0f;
-                T[a] = flip[a] ? 0ull : thr_f32(p.betaf[k], dE);
-            } else {
-                const int64_t dE = -2 * (int64_t)sv[a] * (int64_t)hi[a];
-                flip[a] = dE <= 0;
-                T[a] = flip[a] ? 0ull : __ldg(p.T + (size_t)k * (p.qmax + 1) + (dE >> 1));
-            }
-            need |= !flip[a];
+    const uint32_t lo = 0x80000000u, hi = 0xC2800000u;  // -0 .. -64
+    float worst = 0.f;
+    for (uint64_t b = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= hi;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        const float x = __uint_as_float((uint32_t)b);
+        float e;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fadd_rn(__fmul_rn(x, 0x1.715476p+0f), 32.0f)));
+        const float c = __fmul_rn(cexp32(x), 0x1p32f);
+        const float rel = fabsf(e / c - 1.0f);
+        worst = fmaxf(worst, rel);
+    }
+    atomicMax(out, __float_as_uint(worst));
+}
+
+cudaError_t launch_debug_exp_bound(uint32_t *out, cudaStream_t st)
+{
+    k_debug_exp_bound<<<148 * 8, 256, 0, st>>>(out);
+    return cudaGetLastError();
+}
+
+// One thread = (vertex of the current colour class, W words = 4W consecutive replicas).
+// ELL: neighbours from the padded 4-wide table (one 16-byte load per vertex, pad = -1)
+// instead of row_ptr -> col -> spins, so a neighbour-row load depends on one load only.
+template <bool FLOAT, bool ELL, int W>
+__global__ void __launch_bounds__(256, 4) k_csr_i8_phase(const CsrI8Params p)
+{
+    const uint32_t rw = (uint32_t)p.R >> 2;  // 32-bit words per vertex row
+    const uint32_t ntv = rw / W;             // threads per vertex
+    const uint32_t total = (uint32_t)(p.v_end - p.v_begin) * ntv;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t *s32 = reinterpret_cast<const uint32_t *>(p.s);
+    for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+        const uint32_t vv = p.nq_shift >= 0 ? idx >> p.nq_shift : idx / ntv;
+        const uint32_t o = idx - vv * ntv;
+        const int32_t v = p.v_begin + (int32_t)vv;
+        const uint32_t wbase = (uint32_t)v * rw + o * W;  // first own word
+        uint32_t own[W];
+        if (W == 2) {
+            const uint2 t2 = *reinterpret_cast<const uint2 *>(s32 + wbase);
+            own[0] = t2.x;
+            own[W - 1] = t2.y;
+        } else {
+            own[0] = s32[wbase];
         }
-        if (need) {
-            const uint32_t io = __ldg(p.orig + v);
-            const uint32_t quad = (uint32_t)(r0 >> 2);
-            const uint4 h4 = philox(io, p.t, quad, ST_WORD_HI << 24, p.rk);
-            const uint32_t hw[4] = {h4.x, h4.y, h4.z, h4.w};
-            bool tie = false;
+        float hf[4 * W];
+        int32_t hi[4 * W];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                if (!flip[a]) {
-                    const uint32_t th = (uint32_t)(T[a] >> 32);
-                    flip[a] = hw[a] < th;
-                    tie |= hw[a] == th;
+        for (int a = 0; a < 4 * W; ++a) {
+            hf[a] = 0.f;
+            hi[a] = 0;
+        }
+        auto accumulate = [&](const uint32_t (&nb)[W], uint32_t wb) {
+#pragma unroll
+            for (int w = 0; w < W; ++w)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    if (FLOAT) {
+                        // term = s_j > 0 ? w : -w == w with its sign bit xor-ed by s_j's sign bit
+                        const uint32_t sb = (nb[w] << (24 - 8 * b)) & 0x80000000u;
+                        hf[4 * w + b] = __fadd_rn(hf[4 * w + b], __uint_as_float(wb ^ sb));
+                    } else {
+                        hi[4 * w + b] += (int32_t)wb * (int32_t)(int8_t)(nb[w] >> (8 * b));
+                    }
+                }
+        };
+        auto load_nb = [&](int32_t j, uint32_t (&nb)[W]) {
+            const uint32_t a = (uint32_t)j * rw + o * W;
+            if (W == 2) {
+                const uint2 t2 = __ldg(reinterpret_cast<const uint2 *>(s32 + a));
+                nb[0] = t2.x;
+                nb[W - 1] = t2.y;
+            } else {
+                nb[0] = __ldg(s32 + a);
+            }
+        };
+        if (ELL) {
+            const int4 c = __ldg(reinterpret_cast<const int4 *>(p.ell_col) + v);
+            const int4 wv = __ldg(reinterpret_cast<const int4 *>(p.ell_w) + v);
+            const int32_t cs[4] = {c.x, c.y, c.z, c.w};
+            const uint32_t ws[4] = {(uint32_t)wv.x, (uint32_t)wv.y, (uint32_t)wv.z, (uint32_t)wv.w};
+            uint32_t nbv[4][W];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (cs[u] >= 0)
+                    load_nb(cs[u], nbv[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (cs[u] >= 0)  // row order: ELL slots keep the CSR order, pads at the end
+                    accumulate(nbv[u], ws[u]);
+        } else {
+            const int32_t e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
+            for (int32_t eb = e0; eb < e1; eb += 4) {
+                const int32_t cnt = e1 - eb < 4 ? e1 - eb : 4;
+                uint32_t nbv[4][W];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (u < cnt)
+                        load_nb(__ldg(p.col + eb + u), nbv[u]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (u < cnt)
+                        accumulate(nbv[u], FLOAT ? __float_as_uint(__ldg(p.wf + eb + u))
+                                                 : (uint32_t)__ldg(p.wi + eb + u));
+            }
+        }
+        uint32_t fm[W];
+        const uint32_t io = __ldg(p.orig + v);
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const uint32_t r0 = 4u * (o * W + w);  // local replica of byte 0 of this word
+            const uint32_t quad = (uint32_t)(p.slot0 >> 2) + o * W + w;
+            bool flip[4];
+            if (FLOAT) {
+                float dEv[4], x[4];
+                bool need = false;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    // dE = -2 s h: flip h's sign by the own spin's sign bit, times -2 (exact)
+                    const uint32_t sbit = (own[w] << (24 - 8 * b)) & 0x80000000u;
+                    dEv[b] = __fmul_rn(-2.0f, __uint_as_float(__float_as_uint(hf[4 * w + b]) ^ sbit));
+                    flip[b] = dEv[b] <= 0.0f;
+                    x[b] = -__fmul_rn(__ldg(p.betaf + r0 + b), dEv[b]);
+                    need |= !flip[b];
+                }
+                if (need) {
+                    const uint4 h4 = philox(io, p.t, quad, ST_WORD_HI << 24, p.rk);
+                    const uint32_t hw[4] = {h4.x, h4.y, h4.z, h4.w};
+                    int dec[4];
+                    bool undecided = false;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        dec[b] = flip[b] ? 1 : fast_decide(x[b], hw[b]);
+                        undecided |= dec[b] < 0;
+                    }
+                    if (undecided) {  // rare: exact contract threshold; lo word only on a hi tie
+                        uint64_t T[4];
+                        bool tie = false;
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            T[b] = 0;
+                            if (dec[b] < 0) {
+                                T[b] = thr_f32(__ldg(p.betaf + r0 + b), dEv[b]);
+                                const uint32_t th = (uint32_t)(T[b] >> 32);
+                                dec[b] = hw[b] < th ? 1 : (hw[b] > th ? 0 : -1);
+                                tie |= dec[b] < 0;
+                            }
+                        }
+                        if (tie) {
+                            const uint4 l4 = philox(io, p.t, quad, ST_WORD_LO << 24, p.rk);
+                            const uint32_t lw[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+                            for (int b = 0; b < 4; ++b)
+                                if (dec[b] < 0)
+                                    dec[b] = lw[b] < (uint32_t)T[b] ? 1 : 0;
+                        }
+                    }
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        flip[b] = dec[b] == 1;
+                }
+            } else {
+                uint64_t T[4];
+                bool need = false;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int32_t sv = (int32_t)(int8_t)(own[w] >> (8 * b));
+                    const int32_t dE = -2 * sv * hi[4 * w + b];  // |h| < 2^30
+                    flip[b] = dE <= 0;
+                    T[b] = 0;
+                    if (!flip[b]) {
+                        T[b] = __ldg(p.T + (size_t)(r0 + b) * (p.qmax + 1) + (dE >> 1));
+                        need = true;
+                    }
+                }
+                if (need) {
+                    const uint4 h4 = philox(io, p.t, quad, ST_WORD_HI << 24, p.rk);
+                    const uint32_t hw[4] = {h4.x, h4.y, h4.z, h4.w};
+                    bool tie = false;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        if (!flip[b]) {
+                            const uint32_t th = (uint32_t)(T[b] >> 32);
+                            flip[b] = hw[b] < th;
+                            tie |= hw[b] == th;
+                        }
+                    }
+                    if (tie) {
+                        const uint4 l4 = philox(io, p.t, quad, ST_WORD_LO << 24, p.rk);
+                        const uint32_t lw[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+                            if (!flip[b] && hw[b] == (uint32_t)(T[b] >> 32))
+                                flip[b] = lw[b] < (uint32_t)T[b];
+                    }
                 }
             }
-            if (tie) {
-                const uint4 l4 = philox(io, p.t, quad, ST_WORD_LO << 24, p.rk);
-                const uint32_t lw[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-                    if (!flip[a] && hw[a] == (uint32_t)(T[a] >> 32))
-                        flip[a] = lw[a] < (uint32_t)T[a];
-            }
+            // +1 (0x01) <-> -1 (0xFF): xor the byte with 0xFE
+            fm[w] = (flip[0] ? 0x000000FEu : 0u) | (flip[1] ? 0x0000FE00u : 0u) |
+                    (flip[2] ? 0x00FE0000u : 0u) | (flip[3] ? 0xFE000000u : 0u);
         }
-        char4 out;
-        out.x = flip[0] ? -own.x : own.x;
-        out.y = flip[1] ? -own.y : own.y;
-        out.z = flip[2] ? -own.z : own.z;
-        out.w = flip[3] ? -own.w : own.w;
-        *own_p = out;
+        uint32_t *dst = const_cast<uint32_t *>(s32) + wbase;
+        if (W == 2)
+            *reinterpret_cast<uint2 *>(dst) = make_uint2(own[0] ^ fm[0], own[W - 1] ^ fm[W - 1]);
+        else
+            dst[0] = own[0] ^ fm[0];
     }
 }
 
 cudaError_t launch_csr_i8_phase(const CsrI8Params &p, int32_t threads, cudaStream_t st)
 {
-    const int64_t total = (int64_t)(p.v_end - p.v_begin) * (p.R >> 2);
+    const int32_t W = (p.R % 8 == 0) ? 2 : 1;
+    const int64_t total = (int64_t)(p.v_end - p.v_begin) * (p.R / (4 * W));
     if (total <= 0)
         return cudaSuccess;
+    if (total >= ((int64_t)1 << 32))
+        return cudaErrorInvalidValue;
     const int64_t want = (total + threads - 1) / threads;
-    const unsigned blocks = (unsigned)(want < 148 * 64 ? want : 148 * 64);
-    if (p.wf)
-        k_csr_i8_phase<true><<<blocks, threads, 0, st>>>(p);
-    else
-        k_csr_i8_phase<false><<<blocks, threads, 0, st>>>(p);
+    const unsigned blocks = (unsigned)(want < 148 * 32 ? want : 148 * 32);
+    const bool ell = p.ell_col != nullptr;
+#define LAUNCH(F, E, WW) k_csr_i8_phase<F, E, WW><<<blocks, threads, 0, st>>>(p)
+    if (p.wf) {
+        if (ell) { if (W == 2) LAUNCH(true, true, 2); else LAUNCH(true, true, 1); }
+        else { if (W == 2) LAUNCH(true, false, 2); else LAUNCH(true, false, 1); }
+    } else {
+        if (ell) { if (W == 2) LAUNCH(false, true, 2); else LAUNCH(false, true, 1); }
+        else { if (W == 2) LAUNCH(false, false, 2); else LAUNCH(false, false, 1); }
+    }
+#undef LAUNCH
     return cudaGetLastError();
 }
 

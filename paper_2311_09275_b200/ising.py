@@ -26,7 +26,7 @@ EXPORTED = [
     "ising_exchange", "ising_exchange_begin", "ising_exchange_end", "ising_check_best",
     "ising_best", "ising_get_spins", "ising_set_spins", "ising_get_walkers", "ising_info",
     "ising_sync", "ising_last_error", "ising_destroy", "ising_greedy_colour", "ising_threshold",
-    "ising_version", "ising_debug_philox",
+    "ising_version", "ising_debug_philox", "ising_debug_exp_bound",
 ]
 
 
@@ -93,6 +93,7 @@ def lib(build_if_missing: bool = True):
         "ising_threshold": ([C.c_double, i64], C.c_uint64),
         "ising_version": ([], C.c_char_p),
         "ising_debug_philox": ([i32, vp, i32, vp, vp], C.c_int),
+        "ising_debug_exp_bound": ([i32, C.POINTER(C.c_float)], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -272,3 +273,9 @@ def ising_debug_philox(tuples, device: int = 0):
     o2 = np.zeros((n, 4), np.uint32)
     _check(lib().ising_debug_philox(device, _ptr(a), n, _ptr(o1), _ptr(o2)))
     return o1, o2
+
+
+def ising_debug_exp_bound(device: int = 0) -> float:
+    out = C.c_float()
+    _check(lib().ising_debug_exp_bound(device, C.byref(out)))
+    return out.value

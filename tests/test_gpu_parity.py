@@ -188,6 +188,14 @@ def _regular_inst(n, seed):
     return dict(kind="csr", n=n, row_ptr=rp, col=col, w=ww.astype(np.float32))
 
 
+def test_exp_bracket_bound():
+    """The I8 kernel decides float-weight attempts from the 32-bit hi word with a 2^-12
+    relative margin around an ex2.approx estimate; exact-decision safety needs the estimate
+    within 2^-13 of the contract exponential for EVERY float x in [-64, 0] (exhaustive)."""
+    worst = L.ising_debug_exp_bound()
+    assert worst < 2.0 ** -14, worst
+
+
 def test_float_int8_parity_small():
     inst = _regular_inst(3000, 21)
     betas = synth.beta_ladder(16)
