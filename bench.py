@@ -269,28 +269,33 @@ def run_ours(args):
     attempts_step = n * R * sweeps
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
+    fused = inst["kind"] == "grid" and cfg["layout"] == "bits" and kex > 0
+
+    def timed(kev, fn, *a):
+        if kev is None:
+            return fn(*a)
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record(stream)
+        fn(*a)
+        ev[1].record(stream)
+        kev.append(ev)
+
     def step(kev=None):
+        """One pass of the whole hot path over the workload; returns (our launches, best)."""
         launches = 0
-        for _ in range(rounds):
-            if kev is not None:
-                kev.append((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)))
-                kev[-1][0].record(stream)
-            eng.sweep(kex)
-            if kev is not None:
-                kev[-1][1].record(stream)
-            eng.exchange()
-            launches += 3
+        if fused:
+            # all rounds in ONE k_grid_bits launch (clusters exchange through DSMEM) + merge
+            timed(kev, eng.run, rounds, kex)
+            launches += 2
+        else:
+            for _ in range(rounds):
+                timed(kev, eng.sweep, kex)
+                eng.exchange()
+                launches += (1 if cfg["layout"] == "bits" else kex * eng.info.n_colours + 2) + 2
         if rem:
-            if kev is not None:
-                kev.append((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)))
-                kev[-1][0].record(stream)
-            eng.sweep(rem)
-            if kev is not None:
-                kev[-1][1].record(stream)
+            timed(kev, eng.sweep, rem)
             eng.check_best()
-            launches += 2 if cfg["layout"] == "bits" else 1 + rem * eng.info.n_colours + 2
-        if cfg["layout"] == "i8" and rounds:
-            launches += rounds * (kex * eng.info.n_colours + 2 - 1)
+            launches += (1 if cfg["layout"] == "bits" else rem * eng.info.n_colours + 2) + 1
         rec = eng.best(spins=False)
         if world > 1:
             rec = merge_best_over_ranks(rec, None)
@@ -326,7 +331,7 @@ def run_ours(args):
     value = attempts_step * world * args.steps / (total_ms * 1e-3)
     ms_step = total_ms / args.steps
     avg_launch_ms = kernel_ms / max(nk, 1)
-    per_launch_attempts = n * R * (kex if kex > 0 else sweeps)
+    per_launch_attempts = n * R * (rounds * kex if fused else (kex if kex > 0 else sweeps))
     roof = roofline_entry(avg_launch_ms, per_launch_attempts, cfg["layout"], clk, args.workload)
     roof["kernel"] = "k_grid_bits" if (inst["kind"] == "grid" and cfg["layout"] == "bits") else \
         ("k_csr_bits" if cfg["layout"] == "bits" else "k_csr_i8_phase")
@@ -347,9 +352,12 @@ def run_ours(args):
             e = Engine(inst, K, Cg, betas, seed=synth.PHILOX_KEY + s, copy_begin=rank * C,
                        copy_end=(rank + 1) * C, layout=cfg["layout"], device=local,
                        block_threads=args.threads, stream=stream.cuda_stream)
-            for _ in range(rounds):
-                e.sweep(kex)
-                e.exchange()
+            if fused:
+                e.run(rounds, kex)
+            else:
+                for _ in range(rounds):
+                    e.sweep(kex)
+                    e.exchange()
             if rem:
                 e.sweep(rem)
                 e.check_best()

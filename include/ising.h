@@ -154,6 +154,13 @@ ISING_API int ising_energy(ising_handle *h, void *out);
 /* Per-local-slot cuts (W - E)/2 (syncs); int64 or double like ising_energy. */
 ISING_API int ising_cut(ising_handle *h, void *out);
 
+/* n_rounds x (k_ex sweeps, then ising_exchange) in as few launches as possible (async).
+ * Identical results to calling ising_sweep(h, k_ex); ising_exchange(h) n_rounds times.
+ * Bit-packed tori run the whole sequence in ONE launch: clusters of K/32 CTAs (one copy
+ * each) keep the copy on chip and exchange energies and boundary bit planes through
+ * distributed shared memory.  Errors: ISING_E_UNSUPPORTED for float weights. */
+ISING_API int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex);
+
 /* Local PT step (async, single process): best-so-far check over the local slots,
  * then exchange number e among adjacent temperatures k, k+1 with k = e%2, e%2+2,
  * ...: d = E(c,k+1) - E(c,k); swap the two configurations iff d >= 0 or

@@ -101,6 +101,8 @@ struct ising_handle {
     int64_t *d_Tx_off = nullptr;
     int32_t *d_Tx_len = nullptr;
     BestDev *d_best = nullptr;
+    int64_t *d_copy_best = nullptr;  // fused PT launches: per-copy best (E, slot, sweep)
+    int8_t *d_snap = nullptr;        // fused PT launches: per-copy best configuration
     int8_t *d_best_spins = nullptr, *d_tmp = nullptr;
     void *d_scratch = nullptr;
     size_t scratch_bytes = 0;
@@ -263,26 +265,40 @@ int build_common_device(ising_handle *h, int64_t sum_abs_w)
     return ISING_OK;
 }
 
+// k_grid_bits launch: n_rounds x (k_ex sweeps [+ best check + exchange if pt]).
+GridBitsParams grid_params(ising_handle *h, int32_t n_rounds, int32_t k_ex, bool pt)
+{
+    GridBitsParams p{};
+    p.state_in = h->d_state[h->cur];
+    p.state_out = h->d_state[h->cur ^ 1];
+    p.jbyte = h->d_jbyte;
+    p.qcap = grid_bits_qcap(h->n);
+    p.planes = h->d_planes;
+    p.E_out = h->d_E;
+    p.Lx = h->Lx; p.Ly = h->Ly; p.n = h->n; p.hx = h->Lx / 2; p.half = h->n / 2;
+    p.ymagic = h->ymagic;
+    p.words_per_copy = h->wpc;
+    p.g0 = h->g0;
+    p.t0 = h->t;
+    p.n_rounds = n_rounds;
+    p.k_ex = k_ex;
+    p.pt = pt ? 1 : 0;
+    p.e0 = h->e;
+    p.walker = h->d_walker;
+    p.copy_best = h->d_copy_best;
+    p.snap = h->d_snap;
+    p.Tx = h->d_Tx;
+    p.Tx_off = h->d_Tx_off;
+    p.Tx_len = h->d_Tx_len;
+    p.rk = h->rk;
+    return p;
+}
+
 // Energies after a state change (set_spins / create).
 int refresh_energy(ising_handle *h)
 {
     if (h->kernel == KER_GRID_BITS) {
-        GridBitsParams p{};
-        p.state_in = h->d_state[h->cur];
-        p.state_out = h->d_state[h->cur ^ 1];
-        p.jbyte = h->d_jbyte;
-        p.qcap = grid_bits_qcap(h->n);
-        p.planes = h->d_planes;
-        p.E_out = h->d_E;
-        p.Lx = h->Lx; p.Ly = h->Ly; p.n = h->n; p.hx = h->Lx / 2; p.half = h->n / 2;
-        p.ymagic = h->ymagic;
-        p.words_per_copy = h->wpc;
-        p.g0 = h->g0;
-        p.t0 = h->t;
-        p.n_sweeps = 0;
-        p.cnt_levels = h->cnt_levels;
-        p.rk = h->rk;
-        CK(launch_grid_bits(p, h->G, h->threads, h->smem, h->st));
+        CK(launch_grid_bits(grid_params(h, 1, 0, false), h->G, h->threads, h->smem, h->st));
         h->cur ^= 1;
     } else if (h->kernel == KER_CSR_BITS) {
         CsrBitsParams p{};
@@ -513,22 +529,7 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
 int launch_sweeps(ising_handle *h, int32_t ns)
 {
     if (h->kernel == KER_GRID_BITS) {
-        GridBitsParams p{};
-        p.state_in = h->d_state[h->cur];
-        p.state_out = h->d_state[h->cur ^ 1];
-        p.jbyte = h->d_jbyte;
-        p.qcap = grid_bits_qcap(h->n);
-        p.planes = h->d_planes;
-        p.E_out = h->d_E;
-        p.Lx = h->Lx; p.Ly = h->Ly; p.n = h->n; p.hx = h->Lx / 2; p.half = h->n / 2;
-        p.ymagic = h->ymagic;
-        p.words_per_copy = h->wpc;
-        p.g0 = h->g0;
-        p.t0 = h->t;
-        p.n_sweeps = ns;
-        p.cnt_levels = h->cnt_levels;
-        p.rk = h->rk;
-        CK(launch_grid_bits(p, h->G, h->threads, h->smem, h->st));
+        CK(launch_grid_bits(grid_params(h, 1, ns, false), h->G, h->threads, h->smem, h->st));
         h->cur ^= 1;
     } else if (h->kernel == KER_CSR_BITS) {
         CsrBitsParams p{};
@@ -782,6 +783,8 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
     CK(cudaMemcpyAsync(h->d_planes, planes.data(), planes.size() * 4, cudaMemcpyHostToDevice, h->st));
     CK(h->alloc(&h->d_state[0], (size_t)h->G * n));
     CK(h->alloc(&h->d_state[1], (size_t)h->G * n));
+    CK(h->alloc(&h->d_copy_best, (size_t)h->C_local * 3));
+    CK(h->alloc(&h->d_snap, (size_t)h->C_local * n));
     CK(launch_init_bits(h->d_state[0], h->G, n, nullptr, h->g0, h->rk, h->st));
     rc = refresh_energy(h.get());
     if (rc)
@@ -890,6 +893,40 @@ int ising_cut(ising_handle *h, void *out)
         int64_t *o = (int64_t *)out;
         for (int64_t r = 0; r < h->R; ++r)
             o[r] = (h->W_int - o[r]) / 2;
+    }
+    return ISING_OK;
+}
+
+int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (n_rounds < 0 || k_ex < 1)
+        return fail(ISING_E_ARG, "n_rounds < 0 or k_ex < 1");
+    if ((uint64_t)h->t + (uint64_t)n_rounds * (uint64_t)k_ex >= ((uint64_t)1 << 32))
+        return fail(ISING_E_ARG, "sweep counter would exceed 2^32");
+    if (h->wtype == ISING_W_F32)
+        return fail(ISING_E_UNSUPPORTED, "replica exchange requires integer weights");
+    if (n_rounds == 0)
+        return ISING_OK;
+    if (h->kernel == KER_GRID_BITS && h->K >= 2) {
+        // one launch: clusters of K/32 CTAs (one copy each) run all rounds on chip
+        CK(launch_grid_bits(grid_params(h, n_rounds, k_ex, true), h->G, h->threads, h->smem, h->st));
+        h->cur ^= 1;
+        CK(launch_merge_copy_best(h->d_copy_best, h->d_snap, h->C_local, h->n, h->d_best,
+                                  h->d_best_spins, h->st));
+        h->t += (uint32_t)(n_rounds * k_ex);
+        h->e += (uint32_t)n_rounds;
+        return ISING_OK;
+    }
+    for (int32_t r = 0; r < n_rounds; ++r) {
+        rc = launch_sweeps(h, k_ex);
+        if (rc)
+            return rc;
+        rc = do_exchange(h, nullptr, 0, true);
+        if (rc)
+            return rc;
     }
     return ISING_OK;
 }

@@ -34,9 +34,18 @@ struct GridBitsParams {
     int32_t words_per_copy;    // K/32
     uint32_t g0;               // global group of local group 0
     uint32_t t0;
-    int32_t n_sweeps;
-    int32_t cnt_levels;        // bits of the per-thread energy counter
+    int32_t n_rounds;          // rounds of k_ex sweeps in this launch
+    int32_t k_ex;              // sweeps per round
     int32_t qcap;              // capacity of the shared-memory tail queue
+    // fused PT (pt = 1, launched as clusters of words_per_copy CTAs = one copy each)
+    int32_t pt;
+    uint32_t e0;               // exchange index of the first round
+    int64_t *walker;           // [R_local] walker ids (read + written)
+    int64_t *copy_best;        // [C_local][3] per-copy best (E, slot, sweep) of this launch
+    int8_t *snap;              // [C_local][n] per-copy best configuration (original order)
+    const uint64_t *Tx;
+    const int64_t *Tx_off;
+    const int32_t *Tx_len;
     RoundKeys rk;
 };
 
@@ -123,6 +132,8 @@ cudaError_t launch_energy_i8(const int8_t *s, const int32_t *rp, const int32_t *
                              cudaStream_t st);
 size_t energy_i8_scratch(int32_t n, int32_t R);
 cudaError_t launch_exchange(const ExchangeParams &p, cudaStream_t st);
+cudaError_t launch_merge_copy_best(const int64_t *copy_best, const int8_t *snap, int32_t C_local,
+                                   int32_t n, BestDev *best, int8_t *best_spins, cudaStream_t st);
 cudaError_t launch_swap_bits(uint32_t *state, const uint32_t *swapmask, int32_t n, int32_t C_local,
                              int32_t words_per_copy, cudaStream_t st);
 cudaError_t launch_swap_i8(int8_t *s, const uint32_t *swapmask, int32_t n, int32_t R, int32_t K,

@@ -191,6 +191,52 @@ cudaError_t launch_exchange(const ExchangeParams &p, cudaStream_t st)
     return cudaGetLastError();
 }
 
+// Merge the per-copy best records of a fused PT launch into the handle's best record:
+// lexicographic min over copies of (E, sweep, slot) -- the order in which the sequential
+// schedule would have met them -- then strict improvement over the previous record.
+__global__ void k_merge_copy_best(const int64_t *copy_best, const int8_t *snap, int32_t C_local,
+                                  int32_t n, BestDev *best, int8_t *best_spins)
+{
+    __shared__ int32_t s_win;
+    if (threadIdx.x == 0) {
+        int32_t win = -1;
+        for (int32_t c = 0; c < C_local; ++c) {
+            const int64_t *r = copy_best + 3 * c;
+            if (r[1] < 0)
+                continue;
+            if (win < 0)
+                win = c;
+            else {
+                const int64_t *w = copy_best + 3 * win;
+                if (r[0] < w[0] || (r[0] == w[0] && (r[2] < w[2] || (r[2] == w[2] && r[1] < w[1]))))
+                    win = c;
+            }
+        }
+        BestDev b = *best;
+        if (win >= 0 && (b.slot < 0 || copy_best[3 * win] < b.energy)) {
+            b.energy = copy_best[3 * win];
+            b.slot = copy_best[3 * win + 1];
+            b.sweep = copy_best[3 * win + 2];
+            b.owner = 1;
+            *best = b;
+        } else {
+            win = -1;
+        }
+        s_win = win;
+    }
+    __syncthreads();
+    if (s_win >= 0)
+        for (int32_t i = threadIdx.x; i < n; i += blockDim.x)
+            best_spins[i] = snap[(size_t)s_win * n + i];
+}
+
+cudaError_t launch_merge_copy_best(const int64_t *copy_best, const int8_t *snap, int32_t C_local,
+                                   int32_t n, BestDev *best, int8_t *best_spins, cudaStream_t st)
+{
+    k_merge_copy_best<<<1, 1024, 0, st>>>(copy_best, snap, C_local, n, best, best_spins);
+    return cudaGetLastError();
+}
+
 // Move configurations of accepted pairs: slots k and k+1 of a copy are bits k and
 // k+1 of the copy's K-bit string (words_per_copy words per site).  Delta swap.
 template <int KW>

@@ -30,7 +30,11 @@
 // leaving most lanes of a warp idle while one lane draws its 3rd/4th call.
 // Philox rounds 0-1 are partially hoisted: the parts that depend only on the
 // CTA's group g, the sweep t or the site i are computed once, not per call.
+#include <cooperative_groups.h>
+
 #include "internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace ising {
 
@@ -179,7 +183,8 @@ __device__ __forceinline__ void site_unsat(const uint32_t *S, const uint8_t *JB,
 
 int32_t grid_bits_qcap(int32_t n)
 {
-    const size_t base = (size_t)4 * n + (((size_t)n + 15) & ~(size_t)15) + 512;
+    const size_t base = (size_t)4 * n + (((size_t)n + 15) & ~(size_t)15) + 512 +
+                        (size_t)8 * ((n + 31) / 32);
     const size_t half = (size_t)n / 2;
     size_t qcap = half < 4096 ? half : 4096;
     const size_t budget = 200 * 1024;
@@ -190,9 +195,9 @@ int32_t grid_bits_qcap(int32_t n)
 
 size_t grid_bits_smem(int32_t n)
 {
-    // S (4n) + JB (n, padded to 16) + planes (512) + queue
+    // S (4n) + JB (n, padded to 16) + planes (512) + queue + 2 boundary bit planes
     return (size_t)4 * n + (((size_t)n + 15) & ~(size_t)15) + 512 +
-           (size_t)grid_bits_qcap(n) * kQItemBytes;
+           (size_t)grid_bits_qcap(n) * kQItemBytes + (size_t)8 * ((n + 31) / 32);
 }
 
 __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
@@ -201,6 +206,13 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
     __shared__ int32_t Ucnt[32];
     __shared__ int32_t wcount[33];
     __shared__ int32_t wprefix[33];
+    // fused PT rounds (cluster of words_per_copy CTAs = one copy): the copy's energies,
+    // walker ids, swap mask and best record, held identically by every CTA of the cluster
+    __shared__ int64_t Ecopy[256];
+    __shared__ int64_t Wcopy[256];
+    __shared__ uint32_t Mswap[8];
+    __shared__ int64_t bestE, bestSlot, bestSweep;
+    __shared__ int32_t s_kmin, s_improve;
     const int n = p.n;
     const GridGeom G{p.Lx, p.Ly, p.hx, p.half, p.ymagic};
     uint32_t *S = sm;
@@ -213,11 +225,19 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
     const int wcap = qcap / nwarps;  // per-warp queue region
     uint32_t *q_idx = Q, *q_own = Q + qcap, *q_D = Q + 2 * qcap, *q_acc = Q + 3 * qcap,
              *q_m8 = Q + 4 * qcap;
+    const int nbw = (n + 31) / 32;
+    uint32_t *B0 = Q + 5 * qcap;  // boundary bit planes for cross-word swaps (PT mode)
+    uint32_t *B31 = B0 + nbw;
     const int wq0 = warp * wcap;
 
     const int gl = blockIdx.x;
     const uint32_t g = p.g0 + (uint32_t)gl;
-    const int wt = (int)(g % (uint32_t)p.words_per_copy);
+    const int KW = p.words_per_copy;
+    const int wt = (int)(g % (uint32_t)KW);
+    const int K = 32 * KW;
+    const bool pt = p.pt != 0;
+    const int c_local = gl / KW;
+    const uint32_t c_global = g / (uint32_t)KW;
 
     // 2-D thread mapping: column m = tid % hx of a class row, rows ty + k*rpp
     const int rpp = nt / G.hx;  // rows per pass (host guarantees >= 1)
@@ -239,165 +259,313 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
         JB[l] = p.jbyte[l];
     for (int j = tid; j < 128; j += nt)
         P[j] = p.planes[wt * 128 + j];
-    if (tid < 32)
-        Ucnt[tid] = 0;
+    if (pt) {
+        for (int k = tid; k < K; k += nt)
+            Wcopy[k] = p.walker[(size_t)c_local * K + k];
+        if (tid == 0) {
+            bestE = INT64_MAX;
+            bestSlot = -1;
+            bestSweep = -1;
+        }
+    }
     __syncthreads();
 
-    // ---- sweeps
-    for (int s = 0; s < p.n_sweeps; ++s) {
-        const uint32_t t = p.t0 + (uint32_t)s;
-        const PlaneUniform U = plane_uniform(g, t, p.rk);
+    for (int round = 0; round < p.n_rounds; ++round) {
+        // ---- k_ex sweeps
+        for (int s = 0; s < p.k_ex; ++s) {
+            const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + s);
+            const PlaneUniform U = plane_uniform(g, t, p.rk);
 #pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-            uint32_t *Sc = S + c * G.half;
-            // stage 1: planes 0..7 for every site; undecided words go to this warp's queue
-            int wq = 0;  // warp-uniform
+            for (int c = 0; c < 2; ++c) {
+                uint32_t *Sc = S + c * G.half;
+                // stage 1: planes 0..7 for every site; undecided words go to this warp's queue
+                int wq = 0;  // warp-uniform
+                for (int pass = 0; pass < npass; ++pass) {
+                    const int y = T.ty + pass * rpp;
+                    const bool valid = T.active && y < G.Ly;
+                    const int l = y * G.hx + T.m;
+                    uint32_t own = 0, D = 0, acc = 0, m8 = 0, i_orig = 0;
+                    if (valid) {
+                        own = Sc[l];
+                        uint32_t a0, a1, a2, a3;
+                        site_unsat(S, JB, G, T, c, y, own, a0, a1, a2, a3, i_orig);
+                        const uint32_t s01 = a0 ^ a1, c01 = a0 & a1;
+                        const uint32_t s23 = a2 ^ a3, c23 = a2 & a3;
+                        m8 = ~(s01 | c01 | s23 | c23);                   // u = 0 -> dE = 8
+                        const uint32_t m4 = (s01 ^ s23) & ~(c01 | c23);  // u = 1 -> dE = 4
+                        D = m8 | m4;
+                        acc = ~D;  // dE <= 0 always flips
+                        if (D) {
+                            uint32_t sA, sB;
+                            plane_site(i_orig, U, p.rk, sA, sB);
+                            plane_call(sA, sB, 0u, U, p.rk, P, m8, D, acc);
+                            if (D)
+                                plane_call(sA, sB, 1u, U, p.rk, P, m8, D, acc);
+                        }
+                    }
+                    const bool need = D != 0u;
+                    const uint32_t pm = __ballot_sync(0xFFFFFFFFu, need);
+                    const int slot = wq + __popc(pm & lanemask_lt());
+                    wq += __popc(pm);
+                    if (need && slot < wcap) {
+                        const int qs = wq0 + slot;
+                        q_idx[qs] = (uint32_t)l | (i_orig << 16);
+                        q_own[qs] = own;
+                        q_D[qs] = D;
+                        q_acc[qs] = acc;
+                        q_m8[qs] = m8;
+                    } else if (valid) {
+                        if (need) {  // this warp's queue region is full: finish inline
+                            uint32_t sA, sB;
+                            plane_site(i_orig, U, p.rk, sA, sB);
+                            uint32_t j4 = 2;
+                            do {
+                                plane_call(sA, sB, j4, U, p.rk, P, m8, D, acc);
+                                ++j4;
+                            } while (D && j4 < 16u);
+                        }
+                        Sc[l] = own ^ acc;
+                    }
+                }
+                if (lane == 0)
+                    wcount[warp] = min(wq, wcap);
+                __syncthreads();
+                if (warp == 0) {  // exclusive prefix over the warp regions
+                    const int v = lane < nwarps ? wcount[lane] : 0;
+                    int incl = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                        if (lane >= o)
+                            incl += u;
+                    }
+                    wprefix[lane] = incl - v;
+                    if (lane == 31)
+                        wprefix[32] = incl;
+                }
+                __syncthreads();
+                // stage 2: the queued tail, one word per thread, all lanes busy
+                const int nq = wprefix[32];
+                for (int q = tid; q < nq; q += nt) {
+                    int lo = 0, hi = nwarps;  // region w: wprefix[w] <= q < wprefix[w+1]
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (wprefix[mid] <= q)
+                            lo = mid;
+                        else
+                            hi = mid;
+                    }
+                    const int qs = lo * wcap + (q - wprefix[lo]);
+                    const uint32_t idx = q_idx[qs];
+                    const int l = (int)(idx & 0xFFFFu);
+                    const uint32_t i_orig = idx >> 16;
+                    uint32_t D = q_D[qs], acc = q_acc[qs];
+                    const uint32_t m8 = q_m8[qs];
+                    uint32_t sA, sB;
+                    plane_site(i_orig, U, p.rk, sA, sB);
+                    uint32_t j4 = 2;
+                    do {
+                        plane_call(sA, sB, j4, U, p.rk, P, m8, D, acc);
+                        ++j4;
+                    } while (D && j4 < 16u);
+                    Sc[l] = q_own[qs] ^ acc;
+                }
+                __syncthreads();
+            }
+        }
+
+        // ---- energy: every bond joins a colour-0 and a colour-1 site, so the four
+        // bonds of the colour-1 sites count each bond exactly once.  E = 2U - 2n.
+        {
+            if (tid < 32)
+                Ucnt[tid] = 0;
+            uint32_t cnt[kCntLevels];
+#pragma unroll
+            for (int l = 0; l < kCntLevels; ++l)
+                cnt[l] = 0;
+            const uint32_t *S1 = S + G.half;
             for (int pass = 0; pass < npass; ++pass) {
                 const int y = T.ty + pass * rpp;
-                const bool valid = T.active && y < G.Ly;
-                const int l = y * G.hx + T.m;
-                uint32_t own = 0, D = 0, acc = 0, m8 = 0, i_orig = 0;
-                if (valid) {
-                    own = Sc[l];
-                    uint32_t a0, a1, a2, a3;
-                    site_unsat(S, JB, G, T, c, y, own, a0, a1, a2, a3, i_orig);
-                    const uint32_t s01 = a0 ^ a1, c01 = a0 & a1;
-                    const uint32_t s23 = a2 ^ a3, c23 = a2 & a3;
-                    m8 = ~(s01 | c01 | s23 | c23);                   // u = 0 -> dE = 8
-                    const uint32_t m4 = (s01 ^ s23) & ~(c01 | c23);  // u = 1 -> dE = 4
-                    D = m8 | m4;
-                    acc = ~D;  // dE <= 0 always flips
-                    if (D) {
-                        uint32_t sA, sB;
-                        plane_site(i_orig, U, p.rk, sA, sB);
-                        plane_call(sA, sB, 0u, U, p.rk, P, m8, D, acc);
-                        if (D)
-                            plane_call(sA, sB, 1u, U, p.rk, P, m8, D, acc);
-                    }
-                }
-                const bool need = D != 0u;
-                const uint32_t pm = __ballot_sync(0xFFFFFFFFu, need);
-                const int slot = wq + __popc(pm & lanemask_lt());
-                wq += __popc(pm);
-                if (need && slot < wcap) {
-                    const int qs = wq0 + slot;
-                    q_idx[qs] = (uint32_t)l | (i_orig << 16);
-                    q_own[qs] = own;
-                    q_D[qs] = D;
-                    q_acc[qs] = acc;
-                    q_m8[qs] = m8;
-                } else if (valid) {
-                    if (need) {  // this warp's queue region is full: finish inline
-                        uint32_t sA, sB;
-                        plane_site(i_orig, U, p.rk, sA, sB);
-                        uint32_t j4 = 2;
-                        do {
-                            plane_call(sA, sB, j4, U, p.rk, P, m8, D, acc);
-                            ++j4;
-                        } while (D && j4 < 16u);
-                    }
-                    Sc[l] = own ^ acc;
+                if (T.active && y < G.Ly) {
+                    uint32_t a0, a1, a2, a3, i_orig;
+                    site_unsat(S, JB, G, T, 1, y, S1[y * G.hx + T.m], a0, a1, a2, a3, i_orig);
+                    vadd(cnt, a0);
+                    vadd(cnt, a1);
+                    vadd(cnt, a2);
+                    vadd(cnt, a3);
                 }
             }
-            if (lane == 0)
-                wcount[warp] = min(wq, wcap);
-            __syncthreads();
-            if (warp == 0) {  // exclusive prefix over the warp regions
-                int v = lane < nwarps ? wcount[lane] : 0;
-                int incl = v;
+            // warp total by a butterfly of bit-sliced additions, then lane b reads bit b
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                    if (lane >= o)
-                        incl += u;
-                }
-                wprefix[lane] = incl - v;
-                if (lane == 31)
-                    wprefix[32] = incl;
-            }
-            __syncthreads();
-            // stage 2: the queued tail, one word per thread, all lanes busy
-            const int nq = wprefix[32];
-            for (int q = tid; q < nq; q += nt) {
-                int lo = 0, hi = nwarps;  // find region w: wprefix[w] <= q < wprefix[w+1]
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (wprefix[mid] <= q)
-                        lo = mid;
-                    else
-                        hi = mid;
-                }
-                const int qs = lo * wcap + (q - wprefix[lo]);
-                const uint32_t idx = q_idx[qs];
-                const int l = (int)(idx & 0xFFFFu);
-                const uint32_t i_orig = idx >> 16;
-                uint32_t D = q_D[qs], acc = q_acc[qs];
-                const uint32_t m8 = q_m8[qs];
-                uint32_t sA, sB;
-                plane_site(i_orig, U, p.rk, sA, sB);
-                uint32_t j4 = 2;
-                do {
-                    plane_call(sA, sB, j4, U, p.rk, P, m8, D, acc);
-                    ++j4;
-                } while (D && j4 < 16u);
-                Sc[l] = q_own[qs] ^ acc;
-            }
+            for (int off = 16; off > 0; off >>= 1)
+                vsum_xor(cnt, off);
+            int32_t acc = 0;
+#pragma unroll
+            for (int l = 0; l < kCntLevels; ++l)
+                acc += (int32_t)((cnt[l] >> lane) & 1u) << l;
+            __syncthreads();  // Ucnt zeroed
+            atomicAdd(&Ucnt[lane], acc);
             __syncthreads();
         }
-    }
+        if (!pt)
+            continue;
 
-    // ---- energy: every bond joins a colour-0 and a colour-1 site, so the four
-    // bonds of the colour-1 sites count each bond exactly once.  E = 2U - 2n.
-    {
-        uint32_t cnt[kCntLevels];
-#pragma unroll
-        for (int l = 0; l < kCntLevels; ++l)
-            cnt[l] = 0;
-        const uint32_t *S1 = S + G.half;
-        for (int pass = 0; pass < npass; ++pass) {
-            const int y = T.ty + pass * rpp;
-            if (T.active && y < G.Ly) {
-                uint32_t a0, a1, a2, a3, i_orig;
-                site_unsat(S, JB, G, T, 1, y, S1[y * G.hx + T.m], a0, a1, a2, a3, i_orig);
-                vadd(cnt, a0);
-                vadd(cnt, a1);
-                vadd(cnt, a2);
-                vadd(cnt, a3);
-            }
+        // ---- fused PT step for this copy (a7/a8): same result as ising_exchange
+        cg::cluster_group cluster = cg::this_cluster();
+        cluster.sync();  // every CTA's Ucnt complete
+        if (tid < K) {
+            const int32_t *rem = cluster.map_shared_rank(Ucnt, tid >> 5);
+            Ecopy[tid] = 2 * (int64_t)rem[tid & 31] - 2 * (int64_t)n;
         }
-        // warp total by a butterfly of bit-sliced additions, then lane b reads bit b
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1)
-            vsum_xor(cnt, off);
-        int32_t acc = 0;
-#pragma unroll
-        for (int l = 0; l < kCntLevels; ++l)
-            acc += (int32_t)((cnt[l] >> lane) & 1u) << l;
-        atomicAdd(&Ucnt[lane], acc);
+        if (tid < KW)
+            Mswap[tid] = 0u;
         __syncthreads();
-        if (tid < 32)
-            p.E_out[(size_t)gl * 32 + tid] = 2 * (int64_t)Ucnt[tid] - 2 * (int64_t)n;
+        const uint32_t t_now = p.t0 + (uint32_t)((round + 1) * p.k_ex);
+        const uint32_t e_now = p.e0 + (uint32_t)round;
+        if (warp == 0) {  // best-so-far of the copy: argmin, ties -> lowest slot
+            int64_t bE = INT64_MAX;
+            int bk = -1;
+            for (int k = lane; k < K; k += 32)
+                if (bk < 0 || Ecopy[k] < bE) {
+                    bE = Ecopy[k];
+                    bk = k;
+                }
+            for (int o = 16; o > 0; o >>= 1) {
+                const int64_t oE = __shfl_down_sync(0xFFFFFFFFu, bE, o);
+                const int ok = __shfl_down_sync(0xFFFFFFFFu, bk, o);
+                if (ok >= 0 && (bk < 0 || oE < bE || (oE == bE && ok < bk))) {
+                    bE = oE;
+                    bk = ok;
+                }
+            }
+            if (lane == 0) {
+                s_improve = bE < bestE;
+                s_kmin = bk;
+                if (bE < bestE) {
+                    bestE = bE;
+                    bestSlot = (int64_t)c_global * K + bk;
+                    bestSweep = t_now;
+                }
+            }
+        }
+        __syncthreads();
+        if (s_improve && (s_kmin >> 5) == wt) {  // the owning CTA snapshots the configuration
+            const int bit = s_kmin & 31;
+            int8_t *dst = p.snap + (size_t)c_local * n;
+            for (int i = tid; i < n; i += nt) {
+                const int y = i / p.Lx, x = i - y * p.Lx;
+                dst[i] = ((S[((x + y) & 1) * G.half + y * G.hx + (x >> 1)] >> bit) & 1u) ? -1 : 1;
+            }
+        }
+        // exchange e_now: pairs (k, k+1), k = e%2 + 2j (decided identically in every CTA)
+        const int par = (int)(e_now & 1u);
+        const int npairs = (K - par) / 2;
+        if (tid < npairs) {
+            const int k = par + 2 * tid;
+            const int64_t d = Ecopy[k + 1] - Ecopy[k];
+            bool accept = d >= 0;
+            if (!accept) {
+                const int64_t j = -d - 1;
+                if (j < p.Tx_len[k]) {
+                    const uint4 w = philox((uint32_t)k, e_now, c_global, ST_EXCH << 24, p.rk);
+                    const uint64_t Ux = ((uint64_t)w.x << 32) | (uint64_t)w.y;
+                    accept = Ux < p.Tx[p.Tx_off[k] + j];
+                }
+            }
+            if (accept) {
+                atomicOr(&Mswap[k >> 5], 1u << (k & 31));
+                const int64_t te = Ecopy[k];
+                Ecopy[k] = Ecopy[k + 1];
+                Ecopy[k + 1] = te;
+                const int64_t tw = Wcopy[k];
+                Wcopy[k] = Wcopy[k + 1];
+                Wcopy[k + 1] = tw;
+            }
+        }
+        __syncthreads();
+        // move the configurations: within-word pairs by a delta swap; the cross-word pair
+        // (32wt-1, 32wt) / (32wt+31, 32wt+32) through the neighbours' boundary bit planes
+        const uint32_t Min = Mswap[wt] & 0x7FFFFFFFu;
+        const bool cross_lo = wt > 0 && ((Mswap[wt - 1] >> 31) & 1u);
+        const bool cross_hi = wt + 1 < KW && ((Mswap[wt] >> 31) & 1u);
+        bool any_cross = false;
+        for (int q = 0; q + 1 < KW; ++q)
+            any_cross |= (Mswap[q] >> 31) & 1u;
+        if (any_cross) {  // uniform over the cluster
+            for (int b = warp * 32; b < nbw * 32; b += nt) {
+                const int l = b + lane;
+                const uint32_t w = l < n ? S[l] : 0u;
+                const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, w & 1u);
+                const uint32_t b31 = __ballot_sync(0xFFFFFFFFu, w >> 31);
+                if (lane == 0) {
+                    B0[b >> 5] = b0;
+                    B31[b >> 5] = b31;
+                }
+            }
+            cluster.sync();
+            const uint32_t *nB31 = cross_lo ? cluster.map_shared_rank(B31, wt - 1) : B31;
+            const uint32_t *nB0 = cross_hi ? cluster.map_shared_rank(B0, wt + 1) : B0;
+            for (int l = tid; l < n; l += nt) {
+                uint32_t w = S[l];
+                const uint32_t tt = (w ^ (w >> 1)) & Min;
+                w ^= tt ^ (tt << 1);
+                if (cross_lo)
+                    w = (w & ~1u) | ((nB31[l >> 5] >> (l & 31)) & 1u);
+                if (cross_hi)
+                    w = (w & 0x7FFFFFFFu) | (((nB0[l >> 5] >> (l & 31)) & 1u) << 31);
+                S[l] = w;
+            }
+        } else if (Min) {
+            for (int l = tid; l < n; l += nt) {
+                uint32_t w = S[l];
+                const uint32_t tt = (w ^ (w >> 1)) & Min;
+                S[l] = w ^ tt ^ (tt << 1);
+            }
+        }
+        __syncthreads();
     }
 
-    // ---- store: colour-separated -> original order
+    // ---- outputs
+    if (tid < 32) {
+        p.E_out[(size_t)gl * 32 + tid] =
+            pt && p.n_rounds > 0 ? Ecopy[32 * wt + tid] : 2 * (int64_t)Ucnt[tid] - 2 * (int64_t)n;
+        if (pt)
+            p.walker[(size_t)c_local * K + 32 * wt + tid] = Wcopy[32 * wt + tid];
+    }
+    if (pt && wt == 0 && tid == 0) {
+        p.copy_best[3 * c_local + 0] = bestE;
+        p.copy_best[3 * c_local + 1] = bestSlot;
+        p.copy_best[3 * c_local + 2] = bestSweep;
+    }
     uint32_t *dst = p.state_out + (size_t)gl * n;
     for (int i = tid; i < n; i += nt) {
         const int y = i / p.Lx, x = i - y * p.Lx;
         dst[i] = S[((x + y) & 1) * G.half + y * G.hx + (x >> 1)];
     }
+    if (pt)
+        cg::this_cluster().sync();  // no CTA exits while a peer may still read its shared memory
 }
 
 cudaError_t launch_grid_bits(const GridBitsParams &p, int32_t G, int32_t threads, size_t smem,
                              cudaStream_t st)
 {
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_grid_bits, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess)
-            return e;
-    }
-    k_grid_bits<<<G, threads, smem, st>>>(p);
-    return cudaGetLastError();
+    cudaError_t e = cudaFuncSetAttribute(k_grid_bits, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess)
+        return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.pt ? (unsigned)p.words_per_copy : 1u;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_grid_bits, p);
 }
 
 }  // namespace ising

@@ -51,6 +51,10 @@ class Engine:
     def exchange(self):
         L.ising_exchange(self.h)
 
+    def run(self, n_rounds: int, k_ex: int):
+        """n_rounds x (k_ex sweeps + exchange); one fused launch on bit-packed tori."""
+        L.ising_run(self.h, n_rounds, k_ex)
+
     def exchange_begin(self, send):
         L.ising_exchange_begin(self.h, send.data_ptr())
 
@@ -133,10 +137,12 @@ def all_gather(recv, send, group=None):
         p.copy_(b)
 
 
-def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True):
+def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True, fused: bool = True):
     """PT schedule: rounds of k_ex sweeps + (best check, exchange); final check.
 
     k_ex <= 0 -> plain Metropolis (no exchange), one best check at the end.
+    fused: local exchanges go through Engine.run (one launch for all rounds where the
+    kernel supports it); the record gather of north-star mode needs per-round calls.
     Returns the global best record {E, slot, sweep} (same on every rank)."""
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -144,6 +150,11 @@ def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True):
     done = 0
     if multi and gather:
         send, recv = engine.record_buffers(world)
+    if k_ex > 0 and fused and not (multi and gather) and hasattr(engine, "run"):
+        rounds = sweeps // k_ex
+        if rounds:
+            engine.run(rounds, k_ex)
+            done = rounds * k_ex
     if k_ex > 0:
         while done + k_ex <= sweeps:
             engine.sweep(k_ex)

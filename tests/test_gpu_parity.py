@@ -73,9 +73,39 @@ def test_grid_bits_parity(Lx, Ly, K, C, sweeps, kex, threads):
     inst = grid(Lx, Ly, 1000 + Lx * Ly)
     betas = synth.beta_ladder(K)
     eng = Engine(inst, K, C, betas, seed=KEY, layout="bits", block_threads=threads)
-    run_pt(eng, sweeps, kex)
+    run_pt(eng, sweeps, kex, fused=False)
     o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=oracle.RNG_PLANE).run(sweeps, kex)
     compare_copies(eng, o)
+
+
+@pytest.mark.parametrize("Lx,Ly,K,C,sweeps,kex", [
+    (16, 16, 64, 2, 100, 10),    # clusters of 2 CTAs
+    (6, 4, 32, 3, 33, 7),        # cluster of 1, tail sweeps after the fused rounds
+    (10, 8, 96, 2, 40, 5),       # clusters of 3 (cross-word pairs at both ends of word 1)
+    (12, 20, 256, 1, 60, 3),     # cluster of 8
+])
+def test_fused_pt_launch_parity(Lx, Ly, K, C, sweeps, kex):
+    """ising_run (one launch, cluster exchange through DSMEM) == oracle, bit for bit."""
+    inst = grid(Lx, Ly, 77 + Lx * Ly)
+    betas = synth.beta_ladder(K)
+    eng = Engine(inst, K, C, betas, seed=KEY, layout="bits")
+    rec = run_pt(eng, sweeps, kex, fused=True)
+    o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=oracle.RNG_PLANE).run(sweeps, kex)
+    compare_copies(eng, o)
+    assert (rec["E"], rec["slot"], rec["sweep"]) == (o.best.E, o.best.slot, o.best.sweep)
+    # split into two fused calls + per-round calls: same state
+    eng2 = Engine(inst, K, C, betas, seed=KEY, layout="bits")
+    eng2.run(2, kex)
+    for _ in range(sweeps // kex - 2):
+        eng2.sweep(kex)
+        eng2.exchange()
+    if sweeps % kex:
+        eng2.sweep(sweeps % kex)
+        eng2.check_best()
+    assert np.array_equal(eng2.energies(), eng.energies())
+    assert np.array_equal(eng2.walkers(), eng.walkers())
+    b1, b2 = eng.best(), eng2.best()
+    assert (b1["E"], b1["slot"], b1["sweep"]) == (b2["E"], b2["slot"], b2["sweep"])
 
 
 def test_grid_bits_block_size_invariance():
