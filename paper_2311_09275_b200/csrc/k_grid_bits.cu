@@ -77,10 +77,13 @@ __device__ __forceinline__ void plane_site(uint32_t i, const PlaneUniform &u, co
     sB = u.H0r1 ^ L0 ^ rk.k[3];
 }
 
-// Philox4x32-10 of counter (i, t, g, PLANE<<24 | j4) from the hoisted parts.
+// Philox4x32-10 of counter (i, t, g, PLANE<<24 | j4) from the hoisted parts.  Round
+// keys are re-derived from the 64-bit key (k0 + r W0, k1 + r W1): kernel-uniform values
+// the compiler keeps in uniform registers instead of reloading them per call.
 __device__ __forceinline__ uint4 philox_plane(uint32_t sA, uint32_t sB, uint32_t j4,
                                               const PlaneUniform &u, const RoundKeys &rk)
 {
+    const uint32_t k0 = rk.k[0], k1 = rk.k[1];
     const uint32_t X = sA ^ j4;  // round-0 output word 2 (j4 < 2^24)
     uint32_t c0 = __umulhi(kM1, X) ^ u.U0;
     uint32_t c1 = kM1 * X;
@@ -90,8 +93,8 @@ __device__ __forceinline__ uint4 philox_plane(uint32_t sA, uint32_t sB, uint32_t
     for (int r = 2; r < 10; ++r) {
         const uint32_t lo0 = kM0 * c0, hi0 = __umulhi(kM0, c0);
         const uint32_t lo1 = kM1 * c2, hi1 = __umulhi(kM1, c2);
-        const uint32_t n0 = hi1 ^ c1 ^ rk.k[2 * r];
-        const uint32_t n2 = hi0 ^ c3 ^ rk.k[2 * r + 1];
+        const uint32_t n0 = hi1 ^ c1 ^ (k0 + (uint32_t)r * 0x9E3779B9u);
+        const uint32_t n2 = hi0 ^ c3 ^ (k1 + (uint32_t)r * 0xBB67AE85u);
         c0 = n0;
         c1 = lo1;
         c2 = n2;
@@ -125,6 +128,32 @@ __device__ __forceinline__ void plane_call(uint32_t sA, uint32_t sB, uint32_t j4
     const uint32_t y3 = D & ~w.w & t3;
     D &= ~(w.w ^ t3);
     acc |= y2 | y3;
+}
+
+// Planes 0..7 (calls j4 = 0 and 1) with both Philox evaluations interleaved.
+__device__ __forceinline__ void plane_call2(uint32_t sA, uint32_t sB, const PlaneUniform &u,
+                                            const RoundKeys &rk, const uint32_t *P, uint32_t m8,
+                                            uint32_t &D, uint32_t &acc)
+{
+    const uint4 w0 = philox_plane(sA, sB, 0u, u, rk);
+    const uint4 w1 = philox_plane(sA, sB, 1u, u, rk);
+    const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    const uint4 a4 = *reinterpret_cast<const uint4 *>(P);
+    const uint4 b4 = *reinterpret_cast<const uint4 *>(P + 4);
+    const uint4 a8 = *reinterpret_cast<const uint4 *>(P + 64);
+    const uint4 b8 = *reinterpret_cast<const uint4 *>(P + 68);
+    const uint32_t t4[8] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
+    const uint32_t t8[8] = {a8.x, a8.y, a8.z, a8.w, b8.x, b8.y, b8.z, b8.w};
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+        const uint32_t ta = mux(m8, t8[j], t4[j]);
+        const uint32_t ya = D & ~ws[j] & ta;
+        D &= ~(ws[j] ^ ta);
+        const uint32_t tb = mux(m8, t8[j + 1], t4[j + 1]);
+        const uint32_t yb = D & ~ws[j + 1] & tb;
+        D &= ~(ws[j + 1] ^ tb);
+        acc |= ya | yb;
+    }
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt()
@@ -295,12 +324,10 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
                         const uint32_t m4 = (s01 ^ s23) & ~(c01 | c23);  // u = 1 -> dE = 4
                         D = m8 | m4;
                         acc = ~D;  // dE <= 0 always flips
-                        if (D) {
+                        if (D) {  // planes 0..7: both calls issued together (two independent chains)
                             uint32_t sA, sB;
                             plane_site(i_orig, U, p.rk, sA, sB);
-                            plane_call(sA, sB, 0u, U, p.rk, P, m8, D, acc);
-                            if (D)
-                                plane_call(sA, sB, 1u, U, p.rk, P, m8, D, acc);
+                            plane_call2(sA, sB, U, p.rk, P, m8, D, acc);
                         }
                     }
                     const bool need = D != 0u;
