@@ -294,6 +294,30 @@ GridBitsParams grid_params(ising_handle *h, int32_t n_rounds, int32_t k_ex, bool
     return p;
 }
 
+CsrBitsParams csr_params(ising_handle *h, int32_t n_rounds, int32_t k_ex, bool pt)
+{
+    CsrBitsParams p{};
+    p.state_in = h->d_state[h->cur];
+    p.state_out = h->d_state[h->cur ^ 1];
+    p.rp = h->d_rp; p.nbr = h->d_nbr; p.orig = h->d_orig; p.class_off = h->d_class_off;
+    p.planes = h->d_planes; p.E_out = h->d_E;
+    p.n = h->n; p.ncol = h->ncol; p.qmax = h->qmax; p.m = h->m;
+    p.words_per_copy = h->wpc; p.g0 = h->g0; p.t0 = h->t;
+    p.n_rounds = n_rounds;
+    p.k_ex = k_ex;
+    p.qcap = csr_bits_qcap(h->n, h->qmax);
+    p.pt = pt ? 1 : 0;
+    p.e0 = h->e;
+    p.walker = h->d_walker;
+    p.copy_best = h->d_copy_best;
+    p.snap = h->d_snap;
+    p.Tx = h->d_Tx;
+    p.Tx_off = h->d_Tx_off;
+    p.Tx_len = h->d_Tx_len;
+    p.rk = h->rk;
+    return p;
+}
+
 // Energies after a state change (set_spins / create).
 int refresh_energy(ising_handle *h)
 {
@@ -301,14 +325,7 @@ int refresh_energy(ising_handle *h)
         CK(launch_grid_bits(grid_params(h, 1, 0, false), h->G, h->threads, h->smem, h->st));
         h->cur ^= 1;
     } else if (h->kernel == KER_CSR_BITS) {
-        CsrBitsParams p{};
-        p.state_in = h->d_state[h->cur];
-        p.state_out = h->d_state[h->cur ^ 1];
-        p.rp = h->d_rp; p.nbr = h->d_nbr; p.orig = h->d_orig; p.class_off = h->d_class_off;
-        p.planes = h->d_planes; p.E_out = h->d_E;
-        p.n = h->n; p.ncol = h->ncol; p.qmax = h->qmax; p.m = h->m;
-        p.words_per_copy = h->wpc; p.g0 = h->g0; p.t0 = h->t; p.n_sweeps = 0; p.rk = h->rk;
-        CK(launch_csr_bits(p, h->G, h->threads, h->smem, h->st));
+        CK(launch_csr_bits(csr_params(h, 1, 0, false), h->G, h->threads, h->smem, h->st));
         h->cur ^= 1;
     } else {
         CK(launch_energy_i8(h->d_s8, h->d_rp, h->d_col, h->d_wi, h->d_wf, h->n, (int32_t)h->R, h->d_E,
@@ -470,6 +487,8 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
                         "BITS layout: n too large for a shared-memory resident word group");
         CK(h->alloc(&h->d_state[0], (size_t)h->G * n));
         CK(h->alloc(&h->d_state[1], (size_t)h->G * n));
+        CK(h->alloc(&h->d_copy_best, (size_t)h->C_local * 3));
+        CK(h->alloc(&h->d_snap, (size_t)h->C_local * n));
         CK(launch_init_bits(h->d_state[0], h->G, n, h->d_orig, h->g0, h->rk, h->st));
     } else {
         CK(h->alloc(&h->d_col, m2));
@@ -532,14 +551,7 @@ int launch_sweeps(ising_handle *h, int32_t ns)
         CK(launch_grid_bits(grid_params(h, 1, ns, false), h->G, h->threads, h->smem, h->st));
         h->cur ^= 1;
     } else if (h->kernel == KER_CSR_BITS) {
-        CsrBitsParams p{};
-        p.state_in = h->d_state[h->cur];
-        p.state_out = h->d_state[h->cur ^ 1];
-        p.rp = h->d_rp; p.nbr = h->d_nbr; p.orig = h->d_orig; p.class_off = h->d_class_off;
-        p.planes = h->d_planes; p.E_out = h->d_E;
-        p.n = h->n; p.ncol = h->ncol; p.qmax = h->qmax; p.m = h->m;
-        p.words_per_copy = h->wpc; p.g0 = h->g0; p.t0 = h->t; p.n_sweeps = ns; p.rk = h->rk;
-        CK(launch_csr_bits(p, h->G, h->threads, h->smem, h->st));
+        CK(launch_csr_bits(csr_params(h, 1, ns, false), h->G, h->threads, h->smem, h->st));
         h->cur ^= 1;
     } else {
         CsrI8Params p{};
@@ -910,9 +922,12 @@ int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
         return fail(ISING_E_UNSUPPORTED, "replica exchange requires integer weights");
     if (n_rounds == 0)
         return ISING_OK;
-    if (h->kernel == KER_GRID_BITS && h->K >= 2) {
+    if ((h->kernel == KER_GRID_BITS || h->kernel == KER_CSR_BITS) && h->K >= 2) {
         // one launch: clusters of K/32 CTAs (one copy each) run all rounds on chip
-        CK(launch_grid_bits(grid_params(h, n_rounds, k_ex, true), h->G, h->threads, h->smem, h->st));
+        if (h->kernel == KER_GRID_BITS)
+            CK(launch_grid_bits(grid_params(h, n_rounds, k_ex, true), h->G, h->threads, h->smem, h->st));
+        else
+            CK(launch_csr_bits(csr_params(h, n_rounds, k_ex, true), h->G, h->threads, h->smem, h->st));
         h->cur ^= 1;
         CK(launch_merge_copy_best(h->d_copy_best, h->d_snap, h->C_local, h->n, h->d_best,
                                   h->d_best_spins, h->st));

@@ -62,7 +62,16 @@ struct CsrBitsParams {
     int64_t m;                 // undirected edges
     int32_t words_per_copy;
     uint32_t g0, t0;
-    int32_t n_sweeps;
+    int32_t n_rounds, k_ex;    // n_rounds x k_ex sweeps in this launch
+    int32_t qcap;
+    int32_t pt;                // fused PT (clusters of words_per_copy CTAs)
+    uint32_t e0;
+    int64_t *walker;
+    int64_t *copy_best;
+    int8_t *snap;
+    const uint64_t *Tx;
+    const int64_t *Tx_off;
+    const int32_t *Tx_len;
     RoundKeys rk;
 };
 
@@ -125,6 +134,7 @@ int32_t grid_bits_qcap(int32_t n);
 cudaError_t launch_csr_bits(const CsrBitsParams &p, int32_t G, int32_t threads, size_t smem,
                             cudaStream_t st);
 size_t csr_bits_smem(int32_t n, int32_t qmax, int32_t words_per_copy);
+int32_t csr_bits_qcap(int32_t n, int32_t qmax);
 cudaError_t launch_csr_i8_phase(const CsrI8Params &p, int32_t threads, cudaStream_t st);
 cudaError_t launch_energy_i8(const int8_t *s, const int32_t *rp, const int32_t *col,
                              const int32_t *wi, const float *wf, int32_t n, int32_t R,

@@ -1,169 +1,364 @@
 // k_csr_bits.cu -- multi-spin-coded Metropolis sweeps on a +-1 CSR graph (sm_100a).
 //
-// Rows a3-a6 of SURVEY.md §8(a) for the sparse-random-graph workload (C3: G70
+// Rows a3-a7 of SURVEY.md §8(a) for the sparse-random-graph workload (C3: G70
 // stand-in, "Unweighted MaxCut on sparse random graph", encoded
-// J = +1 in CSR with a greedy colouring).  Same structure as k_grid_bits: one
-// CTA owns one 32-replica word group resident in shared memory for a whole
-// ising_sweep call; colour classes are contiguous in the internal vertex order
-// (and sorted by degree inside a class so a warp mostly sees one degree); the
-// CSR itself (~120 KB for C3) is read through the L1/read-only path.
+// J = +1 in CSR with a greedy colouring).  Same structure as k_grid_bits: one CTA
+// owns one 32-replica word group resident in shared memory for a whole launch;
+// colour classes are contiguous in the internal vertex order (sorted by degree inside
+// a class, so a warp mostly sees one degree); the CSR itself (~120 KB for C3) is read
+// through the L1/read-only path.  Two-stage RNG-tail compaction and the fused PT step
+// are shared with the grid kernel (bits_core.cuh).
 //
-// Per (vertex of degree d, word): a_b = ~(s_i ^ s_j ^ J_b) for every neighbour,
-// summed into a 4-bit vertical counter u (bit-sliced adder);
-// dE = -2 s h = 2d - 4u > 0  <=>  2u < d, class q = dE/2 = d - 2u.  The lanes of
-// each class compare their PLANE-contract U64 against the word's threshold
-// planes P[q][j] MSB first, exactly as in k_grid_bits.
-#include "internal.h"
+// Per (vertex of degree d, word): a_b = ~(s_i ^ s_j ^ J_b) for every neighbour, summed
+// into a 4-bit vertical counter u; dE = -2 s h = 2d - 4u > 0 <=> u < ceil(d/2); the
+// lane's threshold row is q = dE/2 = d - 2u, selected per plane by a multiplexer tree
+// over the bits of u (plane rows P[q][j], q = 1..qmax).
+#include "bits_core.cuh"
 
 namespace ising {
 
+using namespace bits;
+
 namespace {
-constexpr int kPlaneStride = 65;  // padded row: classes of one plane land on distinct banks
-constexpr int kMaxCls = 8;        // d <= 15 -> at most 8 classes with dE > 0
-constexpr int kCntLevels = 12;
+
+constexpr int kRow = 68;  // plane-row stride in words (16-byte aligned rows)
+constexpr int kCsrCnt = 14;
+constexpr int kCsrQItem = 12;
+
+struct CsrSite {
+    uint32_t own, D, u0, u1, u2;
+    int d;
+};
+
+// Evaluate vertex v (internal id) of the current class on the words in S.
+__device__ __forceinline__ CsrSite csr_eval(const uint32_t *S, const CsrBitsParams &p, int v)
+{
+    CsrSite r;
+    r.own = S[v];
+    const int e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
+    r.d = e1 - e0;
+    uint32_t u[4] = {0u, 0u, 0u, 0u};
+    for (int e = e0; e < e1; ++e) {
+        const uint32_t nb = __ldg(p.nbr + e);
+        const uint32_t jm = (uint32_t)((int32_t)nb >> 31);
+        vadd(u, ~(r.own ^ S[nb & 0x7FFFFFFFu] ^ jm));
+    }
+    // D = lanes with u < ceil(d/2), by a bit-sliced comparison with the constant
+    const uint32_t cth = (uint32_t)(r.d + 1) >> 1;
+    uint32_t lt = 0u, eq = ~0u;
+#pragma unroll
+    for (int l = 3; l >= 0; --l) {
+        const uint32_t cb = 0u - ((cth >> l) & 1u);
+        lt |= eq & ~u[l] & cb;
+        eq &= ~(u[l] ^ cb);
+    }
+    r.D = lt;
+    r.u0 = u[0];
+    r.u1 = u[1];
+    r.u2 = u[2];
+    return r;
+}
+
+__device__ __forceinline__ uint32_t mux(uint32_t m, uint32_t a, uint32_t b) { return (m & a) | (~m & b); }
+
+// Threshold planes 4*j4 .. 4*j4+3 of each lane: row q-1 with q = d - 2u.
+__device__ __forceinline__ uint4 csr_thr4(const uint32_t *P, const CsrSite &s, uint32_t j4)
+{
+    auto row = [&](int k) {  // plane-row of u = k (clamped; lanes outside D ignore it)
+        const int q = s.d - 2 * k;
+        return *reinterpret_cast<const uint4 *>(P + (q >= 1 ? q - 1 : 0) * kRow + 4 * j4);
+    };
+    const uint4 r0 = row(0);
+    if (s.d <= 2)
+        return r0;
+    const uint4 r1 = row(1);
+    uint4 t;
+    t.x = mux(s.u0, r1.x, r0.x);
+    t.y = mux(s.u0, r1.y, r0.y);
+    t.z = mux(s.u0, r1.z, r0.z);
+    t.w = mux(s.u0, r1.w, r0.w);
+    if (s.d <= 4)
+        return t;
+    const uint4 r2 = row(2), r3 = row(3);
+    uint4 h;
+    h.x = mux(s.u0, r3.x, r2.x);
+    h.y = mux(s.u0, r3.y, r2.y);
+    h.z = mux(s.u0, r3.z, r2.z);
+    h.w = mux(s.u0, r3.w, r2.w);
+    t.x = mux(s.u1, h.x, t.x);
+    t.y = mux(s.u1, h.y, t.y);
+    t.z = mux(s.u1, h.z, t.z);
+    t.w = mux(s.u1, h.w, t.w);
+    if (s.d <= 8)
+        return t;
+    const uint4 r4 = row(4), r5 = row(5), r6 = row(6), r7 = row(7);
+    uint4 a, b;
+    a.x = mux(s.u0, r5.x, r4.x);
+    a.y = mux(s.u0, r5.y, r4.y);
+    a.z = mux(s.u0, r5.z, r4.z);
+    a.w = mux(s.u0, r5.w, r4.w);
+    b.x = mux(s.u0, r7.x, r6.x);
+    b.y = mux(s.u0, r7.y, r6.y);
+    b.z = mux(s.u0, r7.z, r6.z);
+    b.w = mux(s.u0, r7.w, r6.w);
+    a.x = mux(s.u1, b.x, a.x);
+    a.y = mux(s.u1, b.y, a.y);
+    a.z = mux(s.u1, b.z, a.z);
+    a.w = mux(s.u1, b.w, a.w);
+    t.x = mux(s.u2, a.x, t.x);
+    t.y = mux(s.u2, a.y, t.y);
+    t.z = mux(s.u2, a.z, t.z);
+    t.w = mux(s.u2, a.w, t.w);
+    return t;
+}
+
+__device__ __forceinline__ void csr_call(uint32_t sA, uint32_t sB, uint32_t j4, const PlaneUniform &U,
+                                         const RoundKeys &rk, const uint32_t *P, const CsrSite &s,
+                                         uint32_t &D, uint32_t &acc)
+{
+    const uint4 w = philox_plane(sA, sB, j4, U, rk);
+    const uint4 t = csr_thr4(P, s, j4);
+    const uint32_t y0 = D & ~w.x & t.x;
+    D &= ~(w.x ^ t.x);
+    const uint32_t y1 = D & ~w.y & t.y;
+    D &= ~(w.y ^ t.y);
+    acc |= y0 | y1;
+    const uint32_t y2 = D & ~w.z & t.z;
+    D &= ~(w.z ^ t.z);
+    const uint32_t y3 = D & ~w.w & t.w;
+    D &= ~(w.w ^ t.w);
+    acc |= y2 | y3;
+}
+
 }  // namespace
+
+int32_t csr_bits_qcap(int32_t n, int32_t qmax)
+{
+    const size_t base = (size_t)4 * n + (size_t)(qmax > 0 ? qmax : 1) * kRow * 4 + (size_t)8 * ((n + 31) / 32);
+    size_t qcap = (size_t)n < 4096 ? (size_t)n : 4096;
+    const size_t budget = 200 * 1024;
+    if (base + qcap * kCsrQItem > budget)
+        qcap = base < budget ? (budget - base) / kCsrQItem : 0;
+    return (int32_t)qcap;
+}
 
 size_t csr_bits_smem(int32_t n, int32_t qmax, int32_t words_per_copy)
 {
     (void)words_per_copy;
-    return (size_t)n * sizeof(uint32_t) + (size_t)qmax * kPlaneStride * sizeof(uint32_t);
+    return (size_t)4 * n + (size_t)(qmax > 0 ? qmax : 1) * kRow * 4 + (size_t)8 * ((n + 31) / 32) +
+           (size_t)csr_bits_qcap(n, qmax) * kCsrQItem;
 }
 
 __global__ void __launch_bounds__(1024, 1) k_csr_bits(const CsrBitsParams p)
 {
-    extern __shared__ uint32_t sm[];
+    extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t Ucnt[32];
+    __shared__ int32_t wcount[33];
+    __shared__ int32_t wprefix[33];
+    __shared__ PtShared ps;
     const int n = p.n;
+    const int nbw = (n + 31) / 32;
     uint32_t *S = sm;
-    uint32_t *P = sm + n;  // P[(q-1)*65 + j], q = 1..qmax
+    uint32_t *P = sm + ((n + 3) & ~3);  // [qmax][kRow], 16-byte aligned
+    uint32_t *B0 = P + (p.qmax > 0 ? p.qmax : 1) * kRow;
+    uint32_t *B31 = B0 + nbw;
+    uint32_t *Q = B31 + nbw;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = nt >> 5;
+    const int qcap = p.qcap;
+    const int wcap = qcap / nwarps;
+    uint32_t *q_idx = Q, *q_D = Q + qcap, *q_acc = Q + 2 * qcap;
+    const int wq0 = warp * wcap;
+    const int wbase = tid - lane;
+
     const int gl = blockIdx.x;
     const uint32_t g = p.g0 + (uint32_t)gl;
-    const int wt = (int)(g % (uint32_t)p.words_per_copy);
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int KW = p.words_per_copy;
+    const int wt = (int)(g % (uint32_t)KW);
+    const int K = 32 * KW;
+    const bool pt = p.pt != 0;
+    const int c_local = gl / KW;
+    const uint32_t c_global = g / (uint32_t)KW;
 
     const uint32_t *src = p.state_in + (size_t)gl * n;
     for (int i = tid; i < n; i += nt)
         S[i] = src[i];
     for (int x = tid; x < p.qmax * 64; x += nt) {
         const int q = x / 64, j = x % 64;
-        P[q * kPlaneStride + j] = p.planes[((size_t)wt * p.qmax + q) * 64 + j];
+        P[q * kRow + j] = p.planes[((size_t)wt * p.qmax + q) * 64 + j];
     }
-    if (tid < 32)
-        Ucnt[tid] = 0;
+    if (pt)
+        pt_init(ps, p.walker, c_local, K);
     __syncthreads();
 
-    for (int s = 0; s < p.n_sweeps; ++s) {
-        const uint32_t t = p.t0 + (uint32_t)s;
+    for (int round = 0; round < p.n_rounds; ++round) {
+        for (int s = 0; s < p.k_ex; ++s) {
+            const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + s);
+            const PlaneUniform U = plane_uniform(g, t, p.rk);
 #pragma unroll 1
-        for (int c = 0; c < p.ncol; ++c) {
-            const int v0 = __ldg(p.class_off + c), v1 = __ldg(p.class_off + c + 1);
-            for (int v = v0 + tid; v < v1; v += nt) {
-                const uint32_t own = S[v];
-                const int e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
-                const int d = e1 - e0;
-                uint32_t u[4] = {0u, 0u, 0u, 0u};
-                for (int e = e0; e < e1; ++e) {
-                    const uint32_t nb = __ldg(p.nbr + e);
-                    const uint32_t jm = (uint32_t)((int32_t)nb >> 31);
-                    vadd(u, ~(own ^ S[nb & 0x7FFFFFFFu] ^ jm));
-                }
-                // classes v = 0 .. (d-1)/2 : lanes with u == v, q = d - 2v
-                const int ncls = (d + 1) >> 1;
-                uint32_t mk[kMaxCls];
-                uint32_t D = 0u;
-#pragma unroll
-                for (int cv = 0; cv < kMaxCls; ++cv) {
-                    mk[cv] = 0u;
-                    if (cv < ncls) {
-                        const uint32_t e_0 = (cv & 1) ? u[0] : ~u[0];
-                        const uint32_t e_1 = (cv & 2) ? u[1] : ~u[1];
-                        const uint32_t e_2 = (cv & 4) ? u[2] : ~u[2];
-                        const uint32_t e_3 = (cv & 8) ? u[3] : ~u[3];
-                        mk[cv] = e_0 & e_1 & e_2 & e_3;
-                        D |= mk[cv];
+            for (int c = 0; c < p.ncol; ++c) {
+                const int v0 = __ldg(p.class_off + c), v1 = __ldg(p.class_off + c + 1);
+                int wq = 0;  // warp-uniform
+                for (int b = v0 + wbase; b < v1; b += nt) {
+                    const int v = b + lane;
+                    const bool valid = v < v1;
+                    uint32_t D = 0u, acc = 0u, io = 0u, own = 0u;
+                    CsrSite st;
+                    if (valid) {
+                        st = csr_eval(S, p, v);
+                        own = st.own;
+                        D = st.D;
+                        acc = ~D;  // dE <= 0 always flips
+                        if (D) {
+                            io = __ldg(p.orig + v);
+                            uint32_t sA, sB;
+                            plane_site(io, U, p.rk, sA, sB);
+                            csr_call(sA, sB, 0u, U, p.rk, P, st, D, acc);
+                            if (D)
+                                csr_call(sA, sB, 1u, U, p.rk, P, st, D, acc);
+                        }
+                    }
+                    const bool need = D != 0u;
+                    const uint32_t pm = __ballot_sync(0xFFFFFFFFu, need);
+                    const int slot = wq + __popc(pm & lanemask_lt());
+                    wq += __popc(pm);
+                    if (need && slot < wcap) {
+                        const int qs = wq0 + slot;
+                        q_idx[qs] = (uint32_t)v;
+                        q_D[qs] = D;
+                        q_acc[qs] = acc;
+                    } else if (valid) {
+                        if (need) {  // this warp's queue region is full: finish inline
+                            uint32_t sA, sB;
+                            plane_site(io, U, p.rk, sA, sB);
+                            uint32_t j4 = 2;
+                            do {
+                                csr_call(sA, sB, j4, U, p.rk, P, st, D, acc);
+                                ++j4;
+                            } while (D && j4 < 16u);
+                        }
+                        S[v] = own ^ acc;
                     }
                 }
-                const uint32_t always = ~D;  // dE <= 0
-                uint32_t lt = 0u;
-                if (D) {
-                    const uint32_t io = __ldg(p.orig + v);
-                    uint32_t j4 = 0;
+                if (lane == 0)
+                    wcount[warp] = min(wq, wcap);
+                __syncthreads();
+                if (warp == 0) {
+                    const int vv = lane < nwarps ? wcount[lane] : 0;
+                    int incl = vv;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                        if (lane >= o)
+                            incl += u;
+                    }
+                    wprefix[lane] = incl - vv;
+                    if (lane == 31)
+                        wprefix[32] = incl;
+                }
+                __syncthreads();
+                // stage 2: re-evaluate the queued vertices (neighbours are unchanged) and
+                // finish their comparisons from plane 8 on, all lanes busy
+                const int nq = wprefix[32];
+                for (int q = tid; q < nq; q += nt) {
+                    int lo = 0, hi = nwarps;
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (wprefix[mid] <= q)
+                            lo = mid;
+                        else
+                            hi = mid;
+                    }
+                    const int qs = lo * wcap + (q - wprefix[lo]);
+                    const int v = (int)q_idx[qs];
+                    uint32_t D = q_D[qs], acc = q_acc[qs];
+                    const CsrSite st = csr_eval(S, p, v);
+                    uint32_t sA, sB;
+                    plane_site(__ldg(p.orig + v), U, p.rk, sA, sB);
+                    uint32_t j4 = 2;
                     do {
-                        const uint4 w = philox(io, t, g, (ST_PLANE << 24) | j4, p.rk);
-                        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                        for (int a = 0; a < 4; ++a) {
-                            const int j = 4 * (int)j4 + a;
-                            uint32_t tj = 0u;
-#pragma unroll
-                            for (int cv = 0; cv < kMaxCls; ++cv)
-                                if (cv < ncls)
-                                    tj |= mk[cv] & P[(d - 2 * cv - 1) * kPlaneStride + j];
-                            lt |= D & ~ww[a] & tj;
-                            D &= ~(ww[a] ^ tj);
-                        }
+                        csr_call(sA, sB, j4, U, p.rk, P, st, D, acc);
                         ++j4;
                     } while (D && j4 < 16u);
+                    S[v] = st.own ^ acc;
                 }
-                S[v] = own ^ (always | lt);
+                __syncthreads();
             }
+        }
+
+        // energy: each edge once, counted from its endpoint in the higher colour class
+        {
+            if (tid < 32)
+                Ucnt[tid] = 0;
+            uint32_t cnt[kCsrCnt];
+#pragma unroll
+            for (int l = 0; l < kCsrCnt; ++l)
+                cnt[l] = 0u;
+            for (int c = 1; c < p.ncol; ++c) {
+                const int lo_c = __ldg(p.class_off + c), v1 = __ldg(p.class_off + c + 1);
+                for (int v = lo_c + tid; v < v1; v += nt) {
+                    const uint32_t own = S[v];
+                    const int e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
+                    for (int e = e0; e < e1; ++e) {
+                        const uint32_t nb = __ldg(p.nbr + e);
+                        const uint32_t j = nb & 0x7FFFFFFFu;
+                        if ((int)j >= lo_c)
+                            continue;
+                        const uint32_t jm = (uint32_t)((int32_t)nb >> 31);
+                        vadd(cnt, ~(own ^ S[j] ^ jm));
+                    }
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1)
+                vsum_xor(cnt, off);
+            int32_t acc = 0;
+#pragma unroll
+            for (int l = 0; l < kCsrCnt; ++l)
+                acc += (int32_t)((cnt[l] >> lane) & 1u) << l;
+            __syncthreads();
+            atomicAdd(&Ucnt[lane], acc);
             __syncthreads();
         }
+        if (!pt)
+            continue;
+        auto snap = [&](int bit) {
+            int8_t *dst = p.snap + (size_t)c_local * n;
+            for (int v = tid; v < n; v += nt)
+                dst[__ldg(p.orig + v)] = ((S[v] >> bit) & 1u) ? -1 : 1;
+        };
+        pt_step(ps, Ucnt, p.m, S, n, B0, B31, KW, wt, c_global,
+                p.t0 + (uint32_t)((round + 1) * p.k_ex), p.e0 + (uint32_t)round, p.Tx, p.Tx_off,
+                p.Tx_len, p.rk, snap);
     }
 
-    // energy: each undirected edge once (neighbour id > own id); E = 2U - m
-    {
-        uint32_t cnt[kCntLevels];
-#pragma unroll
-        for (int l = 0; l < kCntLevels; ++l)
-            cnt[l] = 0;
-        for (int v = tid; v < n; v += nt) {
-            const uint32_t own = S[v];
-            const int e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
-            for (int e = e0; e < e1; ++e) {
-                const uint32_t nb = __ldg(p.nbr + e);
-                const uint32_t j = nb & 0x7FFFFFFFu;
-                if ((int)j <= v)
-                    continue;
-                const uint32_t jm = (uint32_t)((int32_t)nb >> 31);
-                vadd(cnt, ~(own ^ S[j] ^ jm));
-            }
-        }
-        const int lane = tid & 31;
-        int32_t acc = 0;
-#pragma unroll
-        for (int l = 0; l < kCntLevels; ++l) {
-            if (__syncthreads_or(cnt[l] != 0u) == 0)
-                continue;
-#pragma unroll 4
-            for (int b = 0; b < 32; ++b) {
-                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, (cnt[l] >> b) & 1u);
-                if (lane == b)
-                    acc += __popc(bal) << l;
-            }
-        }
-        atomicAdd(&Ucnt[lane], acc);
-        __syncthreads();
-        if (tid < 32)
-            p.E_out[(size_t)gl * 32 + tid] = 2 * (int64_t)Ucnt[tid] - p.m;
-    }
-
+    pt_finish(ps, pt, p.n_rounds, Ucnt, p.m, p.E_out, p.walker, p.copy_best, gl, wt, c_local, K);
     uint32_t *dst = p.state_out + (size_t)gl * n;
     for (int i = tid; i < n; i += nt)
         dst[i] = S[i];
+    if (pt)
+        cg::this_cluster().sync();
 }
 
 cudaError_t launch_csr_bits(const CsrBitsParams &p, int32_t G, int32_t threads, size_t smem,
                             cudaStream_t st)
 {
-    if (smem > 48 * 1024) {
-        cudaError_t e =
-            cudaFuncSetAttribute(k_csr_bits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess)
-            return e;
-    }
-    k_csr_bits<<<G, threads, smem, st>>>(p);
-    return cudaGetLastError();
+    cudaError_t e = cudaFuncSetAttribute(k_csr_bits, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.pt ? (unsigned)p.words_per_copy : 1u;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_csr_bits, p);
 }
 
 }  // namespace ising

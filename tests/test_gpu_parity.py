@@ -171,8 +171,20 @@ def test_csr_bits_parity(n, m, K, C, signed):
     inst = csr_pm1(n, m, 17 + n, signed)
     betas = synth.beta_ladder(K)
     eng = Engine(inst, K, C, betas, seed=KEY, layout="bits")
-    run_pt(eng, 40, 10)
+    run_pt(eng, 40, 10, fused=False)
     o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=oracle.RNG_PLANE).run(40, 10)
+    compare_copies(eng, o)
+
+
+@pytest.mark.parametrize("n,m,K,C,sweeps,kex,signed", [(300, 299, 64, 2, 50, 10, True),
+                                                       (200, 700, 96, 1, 31, 5, False),
+                                                       (64, 0, 32, 2, 20, 10, False)])
+def test_csr_bits_fused_pt_parity(n, m, K, C, sweeps, kex, signed):
+    inst = csr_pm1(n, m, 5 + n, signed)
+    betas = synth.beta_ladder(K)
+    eng = Engine(inst, K, C, betas, seed=KEY, layout="bits")
+    run_pt(eng, sweeps, kex, fused=True)
+    o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=oracle.RNG_PLANE).run(sweeps, kex)
     compare_copies(eng, o)
 
 
@@ -182,7 +194,7 @@ def test_c3_full_size_sampled_copies():
     betas = synth.beta_ladder(cfg["K"])
     eng = Engine(inst, cfg["K"], cfg["C"], betas, seed=KEY, layout="bits")
     assert 3 <= eng.info.n_colours <= 6
-    run_pt(eng, 20, 10)
+    run_pt(eng, 20, 10, fused=True)
     for c0 in (0, 50):
         o = oracle.Oracle(inst, cfg["K"], betas, KEY, c0, c0 + 1, rng=oracle.RNG_PLANE).run(20, 10)
         compare_copies(eng, o, check_best=False)
