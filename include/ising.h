@@ -189,6 +189,13 @@ ISING_API int ising_check_best(ising_handle *h, const void *dev_recv, int64_t n_
  * ISING_E_STATE.  Before any check: ISING_E_STATE. */
 ISING_API int ising_best(ising_handle *h, void *best_E, int64_t *slot, int64_t *sweep, int8_t *spins_out);
 
+/* Per-copy best-so-far (syncs): for each local copy c (copies are independent PT ladders,
+ * i.e. independent trials in the sense of PAPER.md P:37-45), the lowest energy reached at
+ * any best-so-far check (strict <, ties -> lowest slot), its global slot and sweep.
+ * best_E: int64[C_local] or double[C_local]; slot, sweep: int64[C_local]; slot = -1 before
+ * the first check. */
+ISING_API int ising_copy_best(ising_handle *h, void *best_E, int64_t *slot, int64_t *sweep);
+
 /* Configuration of one LOCAL slot given by its GLOBAL id (syncs): n int8 +-1. */
 ISING_API int ising_get_spins(ising_handle *h, int64_t slot, int8_t *out);
 

@@ -161,6 +161,7 @@ class Oracle:
     t: int = 0
     e: int = 0
     best: Best = field(default_factory=Best)
+    copy_best: list = field(default_factory=list)  # per local copy: Best (trials)
 
     def __post_init__(self):
         inst = self.inst
@@ -223,12 +224,22 @@ class Oracle:
         return int(acc)
 
     def check_best(self):
-        """Best-so-far check (strict <, ascending slot)."""
+        """Best-so-far check (strict <, ascending slot), globally and
+        per copy (each copy is one independent trial)."""
         E = self.energies()
         r = int(np.argmin(E))
         if E[r] < self.best.E:
             self.best = Best(E=E[r].item(), slot=self.slot0 + r, sweep=self.t,
                              walker=int(self.walker[r]), spins=self.s[r].copy())
+        if self.slots is None:
+            if not self.copy_best:
+                self.copy_best = [Best() for _ in range(self.copy_end - self.copy_begin)]
+            for c in range(self.copy_end - self.copy_begin):
+                Ec = E[c * self.K:(c + 1) * self.K]
+                k = int(np.argmin(Ec))
+                if Ec[k] < self.copy_best[c].E:
+                    self.copy_best[c] = Best(E=Ec[k].item(), slot=self.slot0 + c * self.K + k,
+                                             sweep=self.t)
 
     def exchange(self) -> int:
         if self.is_float:

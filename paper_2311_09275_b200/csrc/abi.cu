@@ -102,6 +102,7 @@ struct ising_handle {
     int32_t *d_Tx_len = nullptr;
     BestDev *d_best = nullptr;
     int64_t *d_copy_best = nullptr;  // fused PT launches: per-copy best (E, slot, sweep)
+    int64_t *d_cbest = nullptr;      // persistent per-copy best-so-far (E, slot, sweep)
     int8_t *d_snap = nullptr;        // fused PT launches: per-copy best configuration
     int8_t *d_best_spins = nullptr, *d_tmp = nullptr;
     void *d_scratch = nullptr;
@@ -229,6 +230,17 @@ int build_common_device(ising_handle *h, int64_t sum_abs_w)
     CK(h->alloc(&h->d_walker, h->R));
     CK(h->alloc(&h->d_swapmask, (size_t)h->C_local * h->wpc));
     CK(h->alloc(&h->d_best, 1));
+    CK(h->alloc(&h->d_cbest, (size_t)h->C_local * 3));
+    {
+        std::vector<int64_t> cb((size_t)h->C_local * 3);
+        for (int32_t c = 0; c < h->C_local; ++c) {
+            cb[3 * c] = 0;
+            cb[3 * c + 1] = -1;
+            cb[3 * c + 2] = -1;
+        }
+        CK(cudaMemcpyAsync(h->d_cbest, cb.data(), cb.size() * 8, cudaMemcpyHostToDevice, h->st));
+        CK(cudaStreamSynchronize(h->st));
+    }
     CK(h->alloc(&h->d_best_spins, h->n));
     CK(h->alloc(&h->d_tmp, h->n));
     std::vector<int64_t> walker(h->R);
@@ -589,6 +601,7 @@ ExchangeParams exchange_params(ising_handle *h)
     ExchangeParams p{};
     p.E = h->d_E;
     p.walker = h->d_walker;
+    p.cbest = h->d_cbest;
     p.swapmask = h->d_swapmask;
     p.best = h->d_best;
     p.best_spins = h->d_best_spins;
@@ -930,7 +943,7 @@ int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
             CK(launch_csr_bits(csr_params(h, n_rounds, k_ex, true), h->G, h->threads, h->smem, h->st));
         h->cur ^= 1;
         CK(launch_merge_copy_best(h->d_copy_best, h->d_snap, h->C_local, h->n, h->d_best,
-                                  h->d_best_spins, h->st));
+                                  h->d_best_spins, h->d_cbest, h->st));
         h->t += (uint32_t)(n_rounds * k_ex);
         h->e += (uint32_t)n_rounds;
         return ISING_OK;
@@ -1006,6 +1019,24 @@ int ising_best(ising_handle *h, void *best_E, int64_t *slot, int64_t *sweep, int
             return fail(ISING_E_STATE, "best configuration is held by another shard");
         CK(cudaMemcpyAsync(spins_out, h->d_best_spins, h->n, cudaMemcpyDeviceToHost, h->st));
         CK(cudaStreamSynchronize(h->st));
+    }
+    return ISING_OK;
+}
+
+int ising_copy_best(ising_handle *h, void *best_E, int64_t *slot, int64_t *sweep)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (!best_E || !slot || !sweep)
+        return fail(ISING_E_ARG, "NULL output");
+    std::vector<int64_t> cb((size_t)h->C_local * 3);
+    CK(cudaMemcpyAsync(cb.data(), h->d_cbest, cb.size() * 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    for (int32_t c = 0; c < h->C_local; ++c) {
+        std::memcpy((char *)best_E + 8 * c, &cb[3 * c], 8);
+        slot[c] = cb[3 * c + 1];
+        sweep[c] = cb[3 * c + 2];
     }
     return ISING_OK;
 }

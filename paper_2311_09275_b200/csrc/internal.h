@@ -100,6 +100,7 @@ struct CsrI8Params {
 struct ExchangeParams {
     int64_t *E;                // [R_local] (int64 or double bits)
     int64_t *walker;           // [R_local]
+    int64_t *cbest;            // [C_local][3] persistent per-copy best (E, slot, sweep)
     uint32_t *swapmask;        // [C_local][ceil(K/32)]
     BestDev *best;
     int8_t *best_spins;        // [n] original order
@@ -143,7 +144,8 @@ cudaError_t launch_energy_i8(const int8_t *s, const int32_t *rp, const int32_t *
 size_t energy_i8_scratch(int32_t n, int32_t R);
 cudaError_t launch_exchange(const ExchangeParams &p, cudaStream_t st);
 cudaError_t launch_merge_copy_best(const int64_t *copy_best, const int8_t *snap, int32_t C_local,
-                                   int32_t n, BestDev *best, int8_t *best_spins, cudaStream_t st);
+                                   int32_t n, BestDev *best, int8_t *best_spins, int64_t *cbest,
+                                   cudaStream_t st);
 cudaError_t launch_swap_bits(uint32_t *state, const uint32_t *swapmask, int32_t n, int32_t C_local,
                              int32_t words_per_copy, cudaStream_t st);
 cudaError_t launch_swap_i8(int8_t *s, const uint32_t *swapmask, int32_t n, int32_t R, int32_t K,

@@ -97,6 +97,25 @@ __global__ void __launch_bounds__(1024) k_exchange(const ExchangeParams p)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool is_f = p.is_float != 0;
     if (p.do_best) {
+        // per-copy best-so-far (trials = copies; NEXT-2 harness): strict <, ties -> lowest slot
+        for (int c = tid; c < p.C_local; c += blockDim.x) {
+            int64_t bE = 0, bS = -1;
+            for (int k = 0; k < p.K; ++k) {
+                const int64_t e = p.E[(int64_t)c * p.K + k];
+                if (bS < 0 || key_less(e, p.slot0 + (int64_t)c * p.K + k, bE, bS, is_f)) {
+                    bE = e;
+                    bS = p.slot0 + (int64_t)c * p.K + k;
+                }
+            }
+            int64_t *cb = p.cbest + 3 * c;
+            const bool better = cb[1] < 0 || (is_f ? __longlong_as_double(bE) < __longlong_as_double(cb[0])
+                                                  : bE < cb[0]);
+            if (better) {
+                cb[0] = bE;
+                cb[1] = bS;
+                cb[2] = p.t;
+            }
+        }
         int64_t bE = 0, bS = -1;
         const int64_t ncand = p.recs ? p.n_recs : p.R_local;
         for (int64_t r = tid; r < ncand; r += blockDim.x) {
@@ -195,9 +214,18 @@ cudaError_t launch_exchange(const ExchangeParams &p, cudaStream_t st)
 // lexicographic min over copies of (E, sweep, slot) -- the order in which the sequential
 // schedule would have met them -- then strict improvement over the previous record.
 __global__ void k_merge_copy_best(const int64_t *copy_best, const int8_t *snap, int32_t C_local,
-                                  int32_t n, BestDev *best, int8_t *best_spins)
+                                  int32_t n, BestDev *best, int8_t *best_spins, int64_t *cbest)
 {
     __shared__ int32_t s_win;
+    for (int32_t c = threadIdx.x; c < C_local; c += blockDim.x) {  // persistent per-copy records
+        const int64_t *r = copy_best + 3 * c;
+        int64_t *cb = cbest + 3 * c;
+        if (r[1] >= 0 && (cb[1] < 0 || r[0] < cb[0])) {
+            cb[0] = r[0];
+            cb[1] = r[1];
+            cb[2] = r[2];
+        }
+    }
     if (threadIdx.x == 0) {
         int32_t win = -1;
         for (int32_t c = 0; c < C_local; ++c) {
@@ -231,9 +259,10 @@ __global__ void k_merge_copy_best(const int64_t *copy_best, const int8_t *snap, 
 }
 
 cudaError_t launch_merge_copy_best(const int64_t *copy_best, const int8_t *snap, int32_t C_local,
-                                   int32_t n, BestDev *best, int8_t *best_spins, cudaStream_t st)
+                                   int32_t n, BestDev *best, int8_t *best_spins, int64_t *cbest,
+                                   cudaStream_t st)
 {
-    k_merge_copy_best<<<1, 1024, 0, st>>>(copy_best, snap, C_local, n, best, best_spins);
+    k_merge_copy_best<<<1, 1024, 0, st>>>(copy_best, snap, C_local, n, best, best_spins, cbest);
     return cudaGetLastError();
 }
 

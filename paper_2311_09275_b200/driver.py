@@ -89,6 +89,10 @@ class Engine:
                 return L.ising_best(self.h, spins=False)
             raise
 
+    def copy_best(self):
+        """Per-copy best-so-far (E[C_local], slot[C_local], sweep[C_local])."""
+        return L.ising_copy_best(self.h)
+
     def spins(self, slot: int):
         return L.ising_get_spins(self.h, slot)
 

@@ -24,7 +24,7 @@ LAYOUTS = {"bits": ISING_SPINS_BITS, "i8": ISING_SPINS_I8}
 EXPORTED = [
     "ising_create_grid", "ising_create_csr", "ising_sweep", "ising_run", "ising_energy", "ising_cut",
     "ising_exchange", "ising_exchange_begin", "ising_exchange_end", "ising_check_best",
-    "ising_best", "ising_get_spins", "ising_set_spins", "ising_get_walkers", "ising_info",
+    "ising_best", "ising_copy_best", "ising_get_spins", "ising_set_spins", "ising_get_walkers", "ising_info",
     "ising_sync", "ising_last_error", "ising_destroy", "ising_greedy_colour", "ising_threshold",
     "ising_version", "ising_debug_philox", "ising_debug_exp_bound",
 ]
@@ -84,6 +84,7 @@ def lib(build_if_missing: bool = True):
         "ising_check_best": ([vp, vp, i64], C.c_int),
         "ising_best": ([vp, vp, C.POINTER(i64), C.POINTER(i64), vp], C.c_int),
         "ising_get_spins": ([vp, i64, vp], C.c_int),
+        "ising_copy_best": ([vp, vp, vp, vp], C.c_int),
         "ising_set_spins": ([vp, i64, vp], C.c_int),
         "ising_get_walkers": ([vp, vp], C.c_int),
         "ising_info": ([vp, C.POINTER(Info)], C.c_int),
@@ -219,6 +220,16 @@ def ising_best(h, spins: bool = True):
     _check(lib().ising_best(h, _ptr(e), C.byref(slot), C.byref(sweep),
                             _ptr(sp) if sp is not None else None))
     return dict(E=e[0].item(), slot=slot.value, sweep=sweep.value, spins=sp)
+
+
+def ising_copy_best(h):
+    info = ising_info(h)
+    nc = info.copy_end - info.copy_begin
+    e = np.zeros(nc, np.float64 if info.wtype == ISING_W_F32 else np.int64)
+    slot = np.zeros(nc, np.int64)
+    sweep = np.zeros(nc, np.int64)
+    _check(lib().ising_copy_best(h, _ptr(e), _ptr(slot), _ptr(sweep)))
+    return e, slot, sweep
 
 
 def ising_get_spins(h, slot: int) -> np.ndarray:

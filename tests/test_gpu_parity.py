@@ -319,3 +319,32 @@ def test_set_spins_and_cut_identity():
         s = eng.spins(9)
         eng.set_spins(9, -s)  # global flip invariance
         assert eng.energies()[9] == E[9]
+
+
+@pytest.mark.parametrize("fused,layout", [(True, "bits"), (False, "bits"), (False, "i8")])
+def test_copy_best_parity(fused, layout):
+    """Per-copy best-so-far (copies = trials of the NEXT-2 harness) equals the oracle's."""
+    inst = grid(16, 16, 9)
+    K, C = (64, 4) if layout == "bits" else (8, 5)
+    betas = synth.beta_ladder(K)
+    eng = Engine(inst, K, C, betas, seed=KEY, layout=layout)
+    run_pt(eng, 60, 10, fused=fused)
+    o = oracle.Oracle(inst, K, betas, KEY, 0, C,
+                      rng=oracle.RNG_PLANE if layout == "bits" else oracle.RNG_WORD).run(60, 10)
+    E, slot, sweep = eng.copy_best()
+    assert list(E) == [b.E for b in o.copy_best]
+    assert list(slot) == [b.slot for b in o.copy_best]
+    assert list(sweep) == [b.sweep for b in o.copy_best]
+
+
+def test_trial_harness_reaches_ground_state_4x4():
+    from paper_2311_09275_b200 import ttt
+    inst = grid(4, 4, 405)
+    u, v, w = synth.torus_edges(4, 4, inst["J_right"], inst["J_down"])
+    states = 1 - 2 * ((np.arange(2**16)[:, None] >> np.arange(16)[None, :]) & 1)
+    Emin = int(np.sum(w * states[:, u] * states[:, v], axis=1).min())
+    W = int(w.sum())
+    eng = Engine(inst, 64, 16, synth.beta_ladder(64), seed=KEY)
+    st = ttt.run_trials(eng, 200, 10, target_cut=(W - Emin) / 2, W=W)
+    assert st.trials == 16 and st.p_s == 1.0 and st.r == 1.0 and st.sweeps_to_target == 200
+    assert np.all(st.best_cuts == (W - Emin) / 2)
