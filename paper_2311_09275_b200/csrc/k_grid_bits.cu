@@ -206,32 +206,33 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
                 if (lane == 0)
                     wcount[warp] = min(wq, wcap);
                 __syncthreads();
-                if (warp == 0) {  // exclusive prefix over the warp regions
-                    const int v = lane < nwarps ? wcount[lane] : 0;
-                    int incl = v;
+                // every warp scans the per-warp queue counts itself (no extra barrier):
+                // lane w holds the exclusive prefix of region w
+                const int cnt_l = lane < nwarps ? wcount[lane] : 0;
+                int incl = cnt_l;
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                        if (lane >= o)
-                            incl += u;
-                    }
-                    wprefix[lane] = incl - v;
-                    if (lane == 31)
-                        wprefix[32] = incl;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= o)
+                        incl += u;
                 }
-                __syncthreads();
+                const int excl = incl - cnt_l;
+                const int nq = __shfl_sync(0xFFFFFFFFu, incl, 31);
                 // stage 2: the queued tail, one word per thread, all lanes busy
-                const int nq = wprefix[32];
-                for (int q = tid; q < nq; q += nt) {
-                    int lo = 0, hi = nwarps;  // region w: wprefix[w] <= q < wprefix[w+1]
-                    while (hi - lo > 1) {
-                        const int mid = (lo + hi) >> 1;
-                        if (wprefix[mid] <= q)
-                            lo = mid;
-                        else
-                            hi = mid;
+                for (int qb = tid - lane; qb < nq; qb += nt) {
+                    const int q = qb + lane;
+                    int lo = 0;  // region: last w with excl_w <= q (binary search over lanes)
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const int cand = lo + step;
+                        const int ev = __shfl_sync(0xFFFFFFFFu, excl, cand < 32 ? cand : 31);
+                        if (cand < nwarps && ev <= q)
+                            lo = cand;
                     }
-                    const int qs = lo * wcap + (q - wprefix[lo]);
+                    const int base_lo = __shfl_sync(0xFFFFFFFFu, excl, lo);
+                    if (q >= nq)
+                        continue;
+                    const int qs = lo * wcap + (q - base_lo);
                     const uint32_t idx = q_idx[qs];
                     const int l = (int)(idx & 0xFFFFu);
                     const uint32_t i_orig = idx >> 16;
@@ -255,22 +256,26 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
         {
             if (tid < 32)
                 Ucnt[tid] = 0;
-            uint32_t cnt[kCntLevels];
+            uint32_t c7[7];  // per-thread counts <= 4 * npass <= 124
 #pragma unroll
-            for (int l = 0; l < kCntLevels; ++l)
-                cnt[l] = 0;
+            for (int l = 0; l < 7; ++l)
+                c7[l] = 0;
             const uint32_t *S1 = S + G.half;
             for (int pass = 0; pass < npass; ++pass) {
                 const int y = T.ty + pass * rpp;
                 if (T.active && y < G.Ly) {
                     uint32_t a0, a1, a2, a3, i_orig;
                     site_unsat(S, JB, G, T, 1, y, S1[y * G.hx + T.m], a0, a1, a2, a3, i_orig);
-                    vadd(cnt, a0);
-                    vadd(cnt, a1);
-                    vadd(cnt, a2);
-                    vadd(cnt, a3);
+                    vadd(c7, a0);
+                    vadd(c7, a1);
+                    vadd(c7, a2);
+                    vadd(c7, a3);
                 }
             }
+            uint32_t cnt[kCntLevels];
+#pragma unroll
+            for (int l = 0; l < kCntLevels; ++l)
+                cnt[l] = l < 7 ? c7[l] : 0u;
             // warp total by a butterfly of bit-sliced additions, then lane b reads bit b
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1)
