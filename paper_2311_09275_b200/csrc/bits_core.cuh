@@ -65,8 +65,8 @@ __device__ __forceinline__ uint4 philox_plane(uint32_t sA, uint32_t sB, uint32_t
     for (int r = 2; r < 10; ++r) {
         const uint32_t lo0 = kM0 * c0, hi0 = __umulhi(kM0, c0);
         const uint32_t lo1 = kM1 * c2, hi1 = __umulhi(kM1, c2);
-        const uint32_t n0 = hi1 ^ c1 ^ (k0 + (uint32_t)r * 0x9E3779B9u);
-        const uint32_t n2 = hi0 ^ c3 ^ (k1 + (uint32_t)r * 0xBB67AE85u);
+        const uint32_t n0 = hi1 ^ c1 ^ rk.k[2 * r];
+        const uint32_t n2 = hi0 ^ c3 ^ rk.k[2 * r + 1];
         c0 = n0;
         c1 = lo1;
         c2 = n2;
@@ -188,12 +188,12 @@ __device__ void pt_step(PtShared &ps, const int32_t *Ucnt, int64_t m_edges, uint
     const int K = 32 * KW;
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();  // every CTA's Ucnt complete
-    if (tid < K) {
-        const int32_t *rem = cluster.map_shared_rank(Ucnt, tid >> 5);
-        ps.Ecopy[tid] = 2 * (int64_t)rem[tid & 31] - m_edges;
+    for (int k = tid; k < K; k += nt) {
+        const int32_t *rem = cluster.map_shared_rank(Ucnt, k >> 5);
+        ps.Ecopy[k] = 2 * (int64_t)rem[k & 31] - m_edges;
     }
-    if (tid < KW)
-        ps.Mswap[tid] = 0u;
+    for (int q = tid; q < KW; q += nt)
+        ps.Mswap[q] = 0u;
     __syncthreads();
     if (warp == 0) {  // best-so-far of the copy: argmin, ties -> lowest slot
         int64_t bE = INT64_MAX;
@@ -226,8 +226,8 @@ __device__ void pt_step(PtShared &ps, const int32_t *Ucnt, int64_t m_edges, uint
         snap(ps.kmin & 31);
     const int par = (int)(e_now & 1u);
     const int npairs = (K - par) / 2;
-    if (tid < npairs) {
-        const int k = par + 2 * tid;
+    for (int pi = tid; pi < npairs; pi += nt) {
+        const int k = par + 2 * pi;
         const int64_t d = ps.Ecopy[k + 1] - ps.Ecopy[k];
         bool accept = d >= 0;
         if (!accept) {

@@ -13,6 +13,10 @@ namespace ising {
 
 enum Kernel : int32_t { KER_GRID_BITS = 0, KER_CSR_BITS = 1, KER_CSR_I8 = 2 };
 
+// k_grid_bits CTA size limit: 24 warps leave 85 registers per thread (round keys held in
+// registers); CTA sizes are multiples of 4 warps so the four schedulers get equal work.
+constexpr int32_t kGridMaxThreads = 768;
+
 // Best-so-far record kept in device memory (updated by the exchange kernel).
 struct BestDev {
     int64_t energy;  // int64, or double bits

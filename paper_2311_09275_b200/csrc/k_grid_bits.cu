@@ -89,7 +89,7 @@ size_t grid_bits_smem(int32_t n)
            (size_t)grid_bits_qcap(n) * kQItemBytes + (size_t)8 * ((n + 31) / 32);
 }
 
-__global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
+__global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBitsParams p)
 {
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t Ucnt[32];
@@ -115,6 +115,10 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
     uint32_t *B31 = B0 + nbw;
     const int wq0 = warp * wcap;
 
+    RoundKeys rkr;  // round keys held in registers for the whole launch
+#pragma unroll
+    for (int r = 0; r < 20; ++r)
+        rkr.k[r] = p.rk.k[r];
     const int gl = blockIdx.x;
     const uint32_t g = p.g0 + (uint32_t)gl;
     const int KW = p.words_per_copy;
@@ -152,7 +156,7 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
         // ---- k_ex sweeps
         for (int s = 0; s < p.k_ex; ++s) {
             const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + s);
-            const PlaneUniform U = plane_uniform(g, t, p.rk);
+            const PlaneUniform U = plane_uniform(g, t, rkr);
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
                 uint32_t *Sc = S + c * G.half;
@@ -175,8 +179,8 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
                         acc = ~D;  // dE <= 0 always flips
                         if (D) {  // planes 0..7: both calls issued together (two independent chains)
                             uint32_t sA, sB;
-                            plane_site(i_orig, U, p.rk, sA, sB);
-                            plane_call2(sA, sB, U, p.rk, P, m8, D, acc);
+                            plane_site(i_orig, U, rkr, sA, sB);
+                            plane_call2(sA, sB, U, rkr, P, m8, D, acc);
                         }
                     }
                     const bool need = D != 0u;
@@ -193,10 +197,10 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
                     } else if (valid) {
                         if (need) {  // this warp's queue region is full: finish inline
                             uint32_t sA, sB;
-                            plane_site(i_orig, U, p.rk, sA, sB);
+                            plane_site(i_orig, U, rkr, sA, sB);
                             uint32_t j4 = 2;
                             do {
-                                plane_call(sA, sB, j4, U, p.rk, P, m8, D, acc);
+                                plane_call(sA, sB, j4, U, rkr, P, m8, D, acc);
                                 ++j4;
                             } while (D && j4 < 16u);
                         }
@@ -239,10 +243,10 @@ __global__ void __launch_bounds__(1024, 1) k_grid_bits(const GridBitsParams p)
                     uint32_t D = q_D[qs], acc = q_acc[qs];
                     const uint32_t m8 = q_m8[qs];
                     uint32_t sA, sB;
-                    plane_site(i_orig, U, p.rk, sA, sB);
+                    plane_site(i_orig, U, rkr, sA, sB);
                     uint32_t j4 = 2;
                     do {
-                        plane_call(sA, sB, j4, U, p.rk, P, m8, D, acc);
+                        plane_call(sA, sB, j4, U, rkr, P, m8, D, acc);
                         ++j4;
                     } while (D && j4 < 16u);
                     Sc[l] = q_own[qs] ^ acc;
