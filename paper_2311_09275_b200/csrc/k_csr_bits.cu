@@ -149,7 +149,7 @@ size_t csr_bits_smem(int32_t n, int32_t qmax, int32_t words_per_copy)
            (size_t)csr_bits_qcap(n, qmax) * kCsrQItem;
 }
 
-__global__ void __launch_bounds__(1024, 1) k_csr_bits(const CsrBitsParams p)
+__global__ void __launch_bounds__(kGridMaxThreads, 1) k_csr_bits(const CsrBitsParams p)
 {
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t Ucnt[32];
@@ -171,6 +171,10 @@ __global__ void __launch_bounds__(1024, 1) k_csr_bits(const CsrBitsParams p)
     const int wq0 = warp * wcap;
     const int wbase = tid - lane;
 
+    RoundKeys rkr;  // round keys held in registers for the whole launch
+#pragma unroll
+    for (int r = 0; r < 20; ++r)
+        rkr.k[r] = p.rk.k[r];
     const int gl = blockIdx.x;
     const uint32_t g = p.g0 + (uint32_t)gl;
     const int KW = p.words_per_copy;
@@ -194,7 +198,7 @@ __global__ void __launch_bounds__(1024, 1) k_csr_bits(const CsrBitsParams p)
     for (int round = 0; round < p.n_rounds; ++round) {
         for (int s = 0; s < p.k_ex; ++s) {
             const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + s);
-            const PlaneUniform U = plane_uniform(g, t, p.rk);
+            const PlaneUniform U = plane_uniform(g, t, rkr);
 #pragma unroll 1
             for (int c = 0; c < p.ncol; ++c) {
                 const int v0 = __ldg(p.class_off + c), v1 = __ldg(p.class_off + c + 1);
@@ -212,10 +216,10 @@ __global__ void __launch_bounds__(1024, 1) k_csr_bits(const CsrBitsParams p)
                         if (D) {
                             io = __ldg(p.orig + v);
                             uint32_t sA, sB;
-                            plane_site(io, U, p.rk, sA, sB);
-                            csr_call(sA, sB, 0u, U, p.rk, P, st, D, acc);
+                            plane_site(io, U, rkr, sA, sB);
+                            csr_call(sA, sB, 0u, U, rkr, P, st, D, acc);
                             if (D)
-                                csr_call(sA, sB, 1u, U, p.rk, P, st, D, acc);
+                                csr_call(sA, sB, 1u, U, rkr, P, st, D, acc);
                         }
                     }
                     const bool need = D != 0u;
@@ -230,10 +234,10 @@ __global__ void __launch_bounds__(1024, 1) k_csr_bits(const CsrBitsParams p)
                     } else if (valid) {
                         if (need) {  // this warp's queue region is full: finish inline
                             uint32_t sA, sB;
-                            plane_site(io, U, p.rk, sA, sB);
+                            plane_site(io, U, rkr, sA, sB);
                             uint32_t j4 = 2;
                             do {
-                                csr_call(sA, sB, j4, U, p.rk, P, st, D, acc);
+                                csr_call(sA, sB, j4, U, rkr, P, st, D, acc);
                                 ++j4;
                             } while (D && j4 < 16u);
                         }
@@ -274,10 +278,10 @@ __global__ void __launch_bounds__(1024, 1) k_csr_bits(const CsrBitsParams p)
                     uint32_t D = q_D[qs], acc = q_acc[qs];
                     const CsrSite st = csr_eval(S, p, v);
                     uint32_t sA, sB;
-                    plane_site(__ldg(p.orig + v), U, p.rk, sA, sB);
+                    plane_site(__ldg(p.orig + v), U, rkr, sA, sB);
                     uint32_t j4 = 2;
                     do {
-                        csr_call(sA, sB, j4, U, p.rk, P, st, D, acc);
+                        csr_call(sA, sB, j4, U, rkr, P, st, D, acc);
                         ++j4;
                     } while (D && j4 < 16u);
                     S[v] = st.own ^ acc;
