@@ -72,6 +72,8 @@ def lib():
             L.or_sweeps.restype = C.c_int64
             L.or_exchange.argtypes = [C.POINTER(_Run), vp, vp, vp, C.c_uint32]
             L.or_exchange.restype = C.c_int64
+            L.or_icm.argtypes = [C.POINTER(_Run), vp, vp, C.c_uint32, C.c_int32]
+            L.or_icm.restype = C.c_int64
             _lib = L
     return _lib
 
@@ -160,6 +162,7 @@ class Oracle:
     slots: tuple | None = None  # (lo, hi) global slot subset (no exchange), else whole copies
     t: int = 0
     e: int = 0
+    f: int = 0  # Houdayer/ICM steps done
     best: Best = field(default_factory=Best)
     copy_best: list = field(default_factory=list)  # per local copy: Best (trials)
 
@@ -253,8 +256,17 @@ class Oracle:
         self.e += 1
         return int(acc)
 
-    def run(self, sweeps: int, k_ex: int):
-        """rounds of k_ex sweeps, best check, exchange; final check."""
+    def icm(self, k_min: int) -> int:
+        """Houdayer cluster move f on copy pairs (2p, 2p+1) at temperatures k >= k_min."""
+        n = lib().or_icm(C.byref(self._run), _p(self.s), _p(self.Ei) if not self.is_float else None,
+                         self.f, k_min)
+        if n < 0:
+            raise ValueError("ICM needs a pair-aligned copy range")
+        self.f += 1
+        return int(n)
+
+    def run(self, sweeps: int, k_ex: int, icm_k_min: int | None = None):
+        """rounds of k_ex sweeps, best check, exchange [, ICM]; final check."""
         if k_ex <= 0:
             self.sweeps(sweeps)
             self.check_best()
@@ -265,6 +277,8 @@ class Oracle:
             done += k_ex
             self.check_best()
             self.exchange()
+            if icm_k_min is not None:
+                self.icm(icm_k_min)
         if done < sweeps:
             self.sweeps(sweeps - done)
             self.check_best()

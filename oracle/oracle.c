@@ -64,7 +64,7 @@ void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
 }
 
 /* RNG streams: top byte of counter word 3. */
-enum { ST_INIT = 0, ST_PLANE = 1, ST_WORD_HI = 2, ST_WORD_LO = 3, ST_EXCH = 4 };
+enum { ST_INIT = 0, ST_PLANE = 1, ST_WORD_HI = 2, ST_WORD_LO = 3, ST_EXCH = 4, ST_ICM = 5 };
 enum { RNG_PLANE = 0, RNG_WORD = 1 };
 
 static void philox_at(uint64_t seed, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
@@ -413,4 +413,79 @@ int64_t or_exchange(const or_run *R, int8_t *s, int64_t *Ei, int64_t *walker, ui
     }
     free(tmp);
     return acc;
+}
+
+/* Energy of one configuration (integer weights), each edge once. */
+static int64_t energy_one_int(const or_run *R, const int8_t *sr)
+{
+    int64_t e = 0;
+    for (int32_t i = 0; i < R->n; ++i)
+        for (int64_t k = R->rp[i]; k < R->rp[i + 1]; ++k)
+            if (R->col[k] > i)
+                e += (int64_t)R->wi[k] * sr[i] * sr[R->col[k]];
+    return e;
+}
+
+/* Houdayer / isoenergetic cluster move number f ("two
+ * replicas at the same temperature are compared and a cluster of spins is identified,
+ * after which the sign of the cluster is changed in each replica"; refs [20][21]).
+ * For every copy pair (2p, 2p+1) of this call and every temperature k >= k_min:
+ * X_i = [s_a(i) != s_b(i)] for a = slot (2p, k), b = slot (2p+1, k).  Seed: the first of
+ * 64 candidates i_j = (w_j * n) >> 32, w_j = word (j&3) of Philox(k, f, p, ICM<<24 | j>>2),
+ * with X = 1 (none: no move).  The cluster is the connected component of the seed in the
+ * subgraph induced by {X = 1} (breadth-first search); its spins flip in both replicas, so
+ * E_a + E_b is unchanged (zero field).  Energies are recomputed from scratch.
+ * Returns the number of clusters flipped; -1 if the copy range is not pair-aligned. */
+int64_t or_icm(const or_run *R, int8_t *s, int64_t *Ei, uint32_t f, int32_t k_min)
+{
+    int32_t n = R->n, K = R->K;
+    if ((R->copy_begin & 1) || ((R->copy_end - R->copy_begin) & 1) || R->slot_hi > R->slot_lo)
+        return -1;
+    char *vis = (char *)malloc((size_t)n);
+    int32_t *queue = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    int64_t moves = 0;
+    for (int32_t c = R->copy_begin; c < R->copy_end; c += 2) {
+        uint32_t pair = (uint32_t)(c / 2);
+        for (int32_t k = k_min < 0 ? 0 : k_min; k < K; ++k) {
+            int64_t ra = (int64_t)(c - R->copy_begin) * K + k, rb = ra + K;
+            int8_t *sa = s + ra * n, *sb = s + rb * n;
+            int32_t seed = -1;
+            uint32_t w[4];
+            for (int j = 0; j < 64 && seed < 0; ++j) {
+                if ((j & 3) == 0)
+                    philox_at(R->seed, (uint32_t)k, f, pair, ((uint32_t)ST_ICM << 24) | (uint32_t)(j >> 2), w);
+                int32_t i = (int32_t)(((uint64_t)w[j & 3] * (uint64_t)n) >> 32);
+                if (sa[i] != sb[i])
+                    seed = i;
+            }
+            if (seed < 0)
+                continue;
+            memset(vis, 0, (size_t)n);
+            int32_t head = 0, tail = 0;
+            queue[tail++] = seed;
+            vis[seed] = 1;
+            while (head < tail) {
+                int32_t i = queue[head++];
+                for (int64_t e = R->rp[i]; e < R->rp[i + 1]; ++e) {
+                    int32_t j = R->col[e];
+                    if (!vis[j] && sa[j] != sb[j]) {
+                        vis[j] = 1;
+                        queue[tail++] = j;
+                    }
+                }
+            }
+            for (int32_t q = 0; q < tail; ++q) {
+                sa[queue[q]] = (int8_t)-sa[queue[q]];
+                sb[queue[q]] = (int8_t)-sb[queue[q]];
+            }
+            if (Ei && R->wi) {
+                Ei[ra] = energy_one_int(R, sa);
+                Ei[rb] = energy_one_int(R, sb);
+            }
+            ++moves;
+        }
+    }
+    free(vis);
+    free(queue);
+    return moves;
 }
