@@ -168,6 +168,15 @@ ISING_API int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex);
  * Errors: ISING_E_UNSUPPORTED for float weights (exchange needs exact energies). */
 ISING_API int ising_exchange(ising_handle *h);
 
+/* Houdayer / isoenergetic cluster move number f (async, PAPER.md
+ * P:53, refs [20][21]).  For every copy pair (2p, 2p+1) of the shard and every temperature
+ * k >= k_min: X_i = [s_a(i) != s_b(i)] for the slots a = (2p, k), b = (2p+1, k); the seed is
+ * the first of 64 candidates i_j = (w_j n) >> 32 (w_j = word j&3 of Philox(k, f, p,
+ * ICM<<24 | j>>2)) with X = 1; the connected component of the seed in the {X = 1} subgraph
+ * flips in both replicas (E_a + E_b is conserved).  Energies are refreshed.  Advances f.
+ * Errors: ISING_E_UNSUPPORTED for the I8 layout or a shard that splits a pair. */
+ISING_API int ising_icm(ising_handle *h, int32_t k_min);
+
 /* Multi-process PT step, first half (async): write one ising_record per local
  * slot (n_slots * 16 bytes) into the DEVICE buffer dev_send, to be all-gathered. */
 ISING_API int ising_exchange_begin(ising_handle *h, void *dev_send);

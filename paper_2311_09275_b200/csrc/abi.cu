@@ -92,6 +92,8 @@ struct ising_handle {
     int64_t *d_walker = nullptr;
     uint32_t *d_swapmask = nullptr;
     uint8_t *d_jbyte = nullptr;
+    uint8_t *d_jrd = nullptr;  // grid: original order, bit 0 J_right=-1, bit 1 J_down=-1 (ICM energies)
+    uint32_t f = 0;            // Houdayer/ICM moves done
     uint32_t *d_planes = nullptr;
     int32_t *d_rp = nullptr, *d_col = nullptr, *d_wi = nullptr, *d_class_off = nullptr;
     int32_t *d_ell_col = nullptr, *d_ell_w = nullptr;
@@ -823,6 +825,14 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
     if (rc)
         return rc;
     CK(h->alloc(&h->d_jbyte, n));
+    {
+        std::vector<uint8_t> jrd(n);
+        for (int32_t i = 0; i < n; ++i)
+            jrd[i] = (uint8_t)((J_right[i] < 0 ? 1 : 0) | (J_down[i] < 0 ? 2 : 0));
+        CK(h->alloc(&h->d_jrd, n));
+        CK(cudaMemcpyAsync(h->d_jrd, jrd.data(), (size_t)n, cudaMemcpyHostToDevice, h->st));
+        CK(cudaStreamSynchronize(h->st));
+    }
     CK(h->alloc(&h->d_planes, planes.size()));
     CK(cudaMemcpyAsync(h->d_jbyte, jb.data(), (size_t)n, cudaMemcpyHostToDevice, h->st));
     CK(cudaMemcpyAsync(h->d_planes, planes.data(), planes.size() * 4, cudaMemcpyHostToDevice, h->st));
@@ -976,6 +986,42 @@ int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
         if (rc)
             return rc;
     }
+    return ISING_OK;
+}
+
+int ising_icm(ising_handle *h, int32_t k_min)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (h->layout != ISING_SPINS_BITS)
+        return fail(ISING_E_UNSUPPORTED, "cluster moves are implemented for the BITS layout");
+    if ((h->c0 & 1) || (h->C_local & 1))
+        return fail(ISING_E_UNSUPPORTED, "cluster moves need a copy shard of whole pairs (2p, 2p+1)");
+    if (k_min < 0 || k_min > h->K)
+        return fail(ISING_E_ARG, "k_min out of range");
+    if ((size_t)8 * h->n > 200 * 1024)
+        return fail(ISING_E_UNSUPPORTED, "cluster moves: n too large for shared memory");
+    IcmParams p{};
+    p.state = h->d_state[h->cur];
+    p.E = h->d_E;
+    p.n = h->n;
+    p.kind = h->kernel == KER_GRID_BITS ? 0 : 1;
+    p.Lx = h->Lx;
+    p.Ly = h->Ly;
+    p.jbyte_orig = h->d_jrd;
+    p.rp = h->d_rp;
+    p.nbr = h->d_nbr;
+    p.o2i = h->kernel == KER_GRID_BITS ? nullptr : h->d_o2i;
+    p.KW = h->wpc;
+    p.pair0 = (uint32_t)(h->c0 / 2);
+    p.k_min = k_min;
+    p.f = h->f;
+    p.m_edges = h->m;
+    p.rk = h->rk;
+    if (h->C_local >= 2)
+        CK(launch_icm_bits(p, h->C_local / 2, 1024, h->st));
+    h->f += 1;
     return ISING_OK;
 }
 

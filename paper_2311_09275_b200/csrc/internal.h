@@ -127,7 +127,25 @@ struct ExchangeParams {
     RoundKeys rk;
 };
 
+struct IcmParams {
+    uint32_t *state;           // [G][n] bit-packed (grid: original order, csr: internal order)
+    int64_t *E;                // [R_local]
+    int32_t n, kind;           // kind 0 grid, 1 csr
+    int32_t Lx, Ly;
+    const uint8_t *jbyte_orig; // grid: [n] original order, bit 0 J_right = -1, bit 1 J_down = -1
+    const int32_t *rp;         // csr (internal)
+    const uint32_t *nbr;
+    const uint32_t *o2i;       // csr: original -> internal (null for grids)
+    int32_t KW;
+    uint32_t pair0;            // global pair index of local pair 0
+    int32_t k_min;
+    uint32_t f;                // cluster-move index
+    int64_t m_edges;
+    RoundKeys rk;
+};
+
 // ----------------------------------------------------------------- launchers
+cudaError_t launch_icm_bits(const IcmParams &p, int32_t pairs, int32_t threads, cudaStream_t st);
 cudaError_t launch_init_bits(uint32_t *state, int32_t G, int32_t n, const uint32_t *orig,
                              uint32_t g0, const RoundKeys &rk, cudaStream_t st);
 cudaError_t launch_init_i8(int8_t *s, int32_t n, int32_t R, const uint32_t *orig, int64_t slot0,

@@ -51,6 +51,10 @@ class Engine:
     def exchange(self):
         L.ising_exchange(self.h)
 
+    def icm(self, k_min: int):
+        """Houdayer cluster move on copy pairs at temperatures k >= k_min."""
+        L.ising_icm(self.h, k_min)
+
     def run(self, n_rounds: int, k_ex: int):
         """n_rounds x (k_ex sweeps + exchange); one fused launch on bit-packed tori."""
         L.ising_run(self.h, n_rounds, k_ex)
@@ -141,7 +145,8 @@ def all_gather(recv, send, group=None):
         p.copy_(b)
 
 
-def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True, fused: bool = True):
+def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True, fused: bool = True,
+           icm_k_min: int | None = None):
     """PT schedule: rounds of k_ex sweeps + (best check, exchange); final check.
 
     k_ex <= 0 -> plain Metropolis (no exchange), one best check at the end.
@@ -154,7 +159,7 @@ def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True, fuse
     done = 0
     if multi and gather:
         send, recv = engine.record_buffers(world)
-    if k_ex > 0 and fused and not (multi and gather) and hasattr(engine, "run"):
+    if k_ex > 0 and fused and icm_k_min is None and not (multi and gather) and hasattr(engine, "run"):
         rounds = sweeps // k_ex
         if rounds:
             engine.run(rounds, k_ex)
@@ -169,6 +174,8 @@ def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True, fuse
                 engine.exchange_end(recv)
             else:
                 engine.exchange()
+            if icm_k_min is not None:  # Houdayer/ICM after each exchange
+                engine.icm(icm_k_min)
     if done < sweeps or k_ex <= 0:
         engine.sweep(sweeps - done)
         if multi and gather:

@@ -23,7 +23,7 @@ LAYOUTS = {"bits": ISING_SPINS_BITS, "i8": ISING_SPINS_I8}
 
 EXPORTED = [
     "ising_create_grid", "ising_create_csr", "ising_sweep", "ising_run", "ising_energy", "ising_cut",
-    "ising_exchange", "ising_exchange_begin", "ising_exchange_end", "ising_check_best",
+    "ising_exchange", "ising_icm", "ising_exchange_begin", "ising_exchange_end", "ising_check_best",
     "ising_best", "ising_copy_best", "ising_get_spins", "ising_set_spins", "ising_get_walkers", "ising_info",
     "ising_sync", "ising_last_error", "ising_destroy", "ising_greedy_colour", "ising_threshold",
     "ising_version", "ising_debug_philox", "ising_debug_exp_bound",
@@ -79,6 +79,7 @@ def lib(build_if_missing: bool = True):
         "ising_energy": ([vp, vp], C.c_int),
         "ising_cut": ([vp, vp], C.c_int),
         "ising_exchange": ([vp], C.c_int),
+        "ising_icm": ([vp, i32], C.c_int),
         "ising_exchange_begin": ([vp, vp], C.c_int),
         "ising_exchange_end": ([vp, vp, i64], C.c_int),
         "ising_check_best": ([vp, vp, i64], C.c_int),
@@ -197,6 +198,10 @@ def ising_cut(h) -> np.ndarray:
 
 def ising_exchange(h):
     _check(lib().ising_exchange(h))
+
+
+def ising_icm(h, k_min: int):
+    _check(lib().ising_icm(h, int(k_min)))
 
 
 def ising_exchange_begin(h, dev_send_ptr: int):

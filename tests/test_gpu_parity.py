@@ -348,3 +348,31 @@ def test_trial_harness_reaches_ground_state_4x4():
     st = ttt.run_trials(eng, 200, 10, target_cut=(W - Emin) / 2, W=W)
     assert st.trials == 16 and st.p_s == 1.0 and st.r == 1.0 and st.sweeps_to_target == 200
     assert np.all(st.best_cuts == (W - Emin) / 2)
+
+
+@pytest.mark.parametrize("kind,K,C,kmin", [("grid", 64, 4, 32), ("grid", 96, 2, 0), ("csr", 32, 2, 0),
+                                           ("csr", 64, 4, 40)])
+def test_icm_parity(kind, K, C, kmin):
+    """Houdayer cluster moves (NEXT-1): GPU == oracle bit for bit, every round."""
+    inst = grid(10, 8, 31) if kind == "grid" else csr_pm1(120, 200, 9, signed=True)
+    betas = synth.beta_ladder(K)
+    eng = Engine(inst, K, C, betas, seed=KEY, layout="bits")
+    run_pt(eng, 40, 10, icm_k_min=kmin)
+    o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=oracle.RNG_PLANE).run(40, 10, icm_k_min=kmin)
+    compare_copies(eng, o)
+
+
+def test_icm_c2_sampled_pair_and_errors():
+    cfg = synth.CONFIGS["c2"]
+    inst = synth.make_instance(cfg)
+    betas = synth.beta_ladder(64)
+    eng = Engine(inst, 64, 64, betas, seed=KEY, layout="bits")
+    run_pt(eng, 20, 10, icm_k_min=32)
+    o = oracle.Oracle(inst, 64, betas, KEY, 10, 12, rng=oracle.RNG_PLANE).run(20, 10, icm_k_min=32)
+    compare_copies(eng, o, check_best=False)
+    odd = Engine(grid(8, 8, 1), 32, 3, synth.beta_ladder(32), seed=1, copy_begin=1, copy_end=3)
+    with pytest.raises(L.IsingError):
+        odd.icm(0)
+    i8 = Engine(grid(8, 8, 1), 8, 2, synth.beta_ladder(8), seed=1, layout="i8")
+    with pytest.raises(L.IsingError):
+        i8.icm(0)
