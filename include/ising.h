@@ -168,6 +168,14 @@ ISING_API int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex);
  * Errors: ISING_E_UNSUPPORTED for float weights (exchange needs exact energies). */
 ISING_API int ising_exchange(ising_handle *h);
 
+/* Simulated annealing (async launch, syncs at the end, PAPER.md P:53
+ * "SA-based CMOS annealers"): n_sweeps Metropolis sweeps in which sweep s
+ * uses the inverse temperature sched[s*K + k] for the slots of temperature index k
+ * (schedule: n_sweeps x K doubles > 0, any order; a row equal to the ladder reproduces
+ * ising_sweep).  Same RNG contracts and threshold formula as ising_sweep; advances t; ends
+ * with a best-so-far check.  No exchange. */
+ISING_API int ising_anneal(ising_handle *h, int32_t n_sweeps, const double *sched);
+
 /* Houdayer / isoenergetic cluster move number f (async, PAPER.md
  * P:53, refs [20][21]).  For every copy pair (2p, 2p+1) of the shard and every temperature
  * k >= k_min: X_i = [s_a(i) != s_b(i)] for the slots a = (2p, k), b = (2p+1, k); the seed is

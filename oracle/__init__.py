@@ -256,6 +256,23 @@ class Oracle:
         self.e += 1
         return int(acc)
 
+    def anneal(self, schedule) -> int:
+        """Simulated annealing: sweep s uses schedule[s, k] for temperature index k
+        (SPEC.md S:276-284); then a best-so-far check."""
+        sched = np.ascontiguousarray(schedule, np.float64)
+        acc = 0
+        keep = self.betas
+        try:
+            for s in range(sched.shape[0]):
+                self.betas = np.ascontiguousarray(sched[s])
+                self._run.beta = _p(self.betas).value
+                acc += self.sweeps(1)
+        finally:
+            self.betas = keep
+            self._run.beta = _p(self.betas).value
+        self.check_best()
+        return acc
+
     def icm(self, k_min: int) -> int:
         """Houdayer cluster move f on copy pairs (2p, 2p+1) at temperatures k >= k_min."""
         n = lib().or_icm(C.byref(self._run), _p(self.s), _p(self.Ei) if not self.is_float else None,

@@ -110,6 +110,8 @@ struct ising_handle {
     void *d_scratch = nullptr;
     size_t scratch_bytes = 0;
     std::vector<void *> allocs;
+    void *d_sched = nullptr;  // annealing schedules (planes or thresholds), grown on demand
+    size_t sched_bytes = 0;
     std::vector<uint32_t> orig;  // internal -> original (CSR kernels)
     std::vector<uint32_t> o2i;
 
@@ -128,6 +130,8 @@ struct ising_handle {
     {
         for (void *p : allocs)
             cudaFree(p);
+        if (d_sched)
+            cudaFree(d_sched);
     }
 };
 
@@ -563,6 +567,44 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
     return ISING_OK;
 }
 
+// int8 kernels: per colour phase launches; `sched` (annealing) holds per-sweep threshold
+// tables T[s][R][qmax+1] (integer weights) or betaf[s][R] (float weights), else null.
+int launch_sweeps_i8(ising_handle *h, int32_t ns, const void *sched)
+{
+    CsrI8Params p{};
+    p.s = h->d_s8; p.rp = h->d_rp; p.col = h->d_col; p.wi = h->d_wi; p.wf = h->d_wf;
+    p.orig = h->d_orig; p.T = h->d_T; p.betaf = h->d_betaf; p.R = (int32_t)h->R; p.K = h->K;
+    p.nq = (int32_t)(h->R / 4);
+    p.ell_col = h->d_ell_col;
+    p.ell_w = h->d_ell_w;
+    const int32_t tpv = (int32_t)(h->R % 8 == 0 ? h->R / 8 : h->R / 4);  // threads per vertex
+    p.nq_shift = -1;
+    for (int sh = 0; sh < 31; ++sh)
+        if ((1 << sh) == tpv)
+            p.nq_shift = sh;
+    p.slot0 = h->slot0; p.qmax = h->qmax; p.rk = h->rk;
+    const int32_t thr = h->threads > 256 ? 256 : h->threads;
+    for (int32_t s = 0; s < ns; ++s) {
+        p.t = h->t + (uint32_t)s;
+        if (sched) {
+            if (h->wtype == ISING_W_I32)
+                p.T = (const uint64_t *)sched + (size_t)s * h->R * (h->qmax + 1);
+            else
+                p.betaf = (const float *)sched + (size_t)s * h->R;
+        }
+        for (int32_t c = 0; c < h->ncol; ++c) {
+            p.v_begin = h->class_off[c];
+            p.v_end = h->class_off[c + 1];
+            CK(launch_csr_i8_phase(p, thr, h->st));
+        }
+    }
+    if (ns > 0)
+        CK(launch_energy_i8(h->d_s8, h->d_rp, h->d_col, h->d_wi, h->d_wf, h->n, (int32_t)h->R, h->d_E,
+                            h->d_Ef, h->d_scratch, h->scratch_bytes, h->st));
+    h->t += (uint32_t)ns;
+    return ISING_OK;
+}
+
 int launch_sweeps(ising_handle *h, int32_t ns)
 {
     if (h->kernel == KER_GRID_BITS) {
@@ -572,31 +614,7 @@ int launch_sweeps(ising_handle *h, int32_t ns)
         CK(launch_csr_bits(csr_params(h, 1, ns, false), h->G, h->threads, h->smem, h->st));
         h->cur ^= 1;
     } else {
-        CsrI8Params p{};
-        p.s = h->d_s8; p.rp = h->d_rp; p.col = h->d_col; p.wi = h->d_wi; p.wf = h->d_wf;
-        p.orig = h->d_orig; p.T = h->d_T; p.betaf = h->d_betaf; p.R = (int32_t)h->R; p.K = h->K;
-        p.nq = (int32_t)(h->R / 4);
-        p.ell_col = h->d_ell_col;
-        p.ell_w = h->d_ell_w;
-        const int32_t tpv = (int32_t)(h->R % 8 == 0 ? h->R / 8 : h->R / 4);  // threads per vertex
-        p.nq_shift = -1;
-        for (int sh = 0; sh < 31; ++sh)
-            if ((1 << sh) == tpv)
-                p.nq_shift = sh;
-
-        p.slot0 = h->slot0; p.qmax = h->qmax; p.rk = h->rk;
-        const int32_t thr = h->threads > 256 ? 256 : h->threads;
-        for (int32_t s = 0; s < ns; ++s) {
-            p.t = h->t + (uint32_t)s;
-            for (int32_t c = 0; c < h->ncol; ++c) {
-                p.v_begin = h->class_off[c];
-                p.v_end = h->class_off[c + 1];
-                CK(launch_csr_i8_phase(p, thr, h->st));
-            }
-        }
-        if (ns > 0)
-            CK(launch_energy_i8(h->d_s8, h->d_rp, h->d_col, h->d_wi, h->d_wf, h->n, (int32_t)h->R,
-                                h->d_E, h->d_Ef, h->d_scratch, h->scratch_bytes, h->st));
+        return launch_sweeps_i8(h, ns, nullptr);
     }
     h->t += (uint32_t)ns;
     return ISING_OK;
@@ -987,6 +1005,88 @@ int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
             return rc;
     }
     return ISING_OK;
+}
+
+int ising_anneal(ising_handle *h, int32_t n_sweeps, const double *sched)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (n_sweeps < 0 || (n_sweeps > 0 && !sched))
+        return fail(ISING_E_ARG, "n_sweeps < 0 or schedule is NULL");
+    if ((uint64_t)h->t + (uint64_t)n_sweeps >= ((uint64_t)1 << 32))
+        return fail(ISING_E_ARG, "sweep counter would exceed 2^32");
+    for (int64_t x = 0; x < (int64_t)n_sweeps * h->K; ++x)
+        if (!(sched[x] > 0.0) || !std::isfinite(sched[x]))
+            return fail(ISING_E_ARG, "schedule entry " + std::to_string(x) + " must be finite and > 0");
+    if (n_sweeps == 0)
+        return ISING_OK;
+    // per-sweep tables, same formulas as the fixed ladder
+    std::vector<uint8_t> host;
+    if (h->layout == ISING_SPINS_BITS) {
+        std::vector<int32_t> qs;
+        if (h->kernel == KER_GRID_BITS)
+            qs = {2, 4};
+        else
+            for (int32_t q = 1; q <= h->qmax; ++q)
+                qs.push_back(q);
+        std::vector<uint32_t> all, planes;
+        for (int32_t s = 0; s < n_sweeps; ++s) {
+            std::vector<double> row(sched + (size_t)s * h->K, sched + (size_t)(s + 1) * h->K);
+            plane_table(row, qs, planes);
+            all.insert(all.end(), planes.begin(), planes.end());
+        }
+        host.resize(all.size() * 4);
+        std::memcpy(host.data(), all.data(), host.size());
+    } else if (h->wtype == ISING_W_I32) {
+        const size_t per = (size_t)h->R * (h->qmax + 1);
+        std::vector<uint64_t> all(per * n_sweeps);
+        for (int32_t s = 0; s < n_sweeps; ++s)
+            for (int64_t r = 0; r < h->R; ++r) {
+                const double beta = sched[(size_t)s * h->K + (h->slot0 + r) % h->K];
+                all[s * per + r * (h->qmax + 1)] = std::numeric_limits<uint64_t>::max();
+                for (int32_t q = 1; q <= h->qmax; ++q)
+                    all[s * per + r * (h->qmax + 1) + q] = metropolis_threshold(beta, 2 * (int64_t)q);
+            }
+        host.resize(all.size() * 8);
+        std::memcpy(host.data(), all.data(), host.size());
+    } else {
+        std::vector<float> all((size_t)h->R * n_sweeps);
+        for (int32_t s = 0; s < n_sweeps; ++s)
+            for (int64_t r = 0; r < h->R; ++r)
+                all[(size_t)s * h->R + r] = (float)sched[(size_t)s * h->K + (h->slot0 + r) % h->K];
+        host.resize(all.size() * 4);
+        std::memcpy(host.data(), all.data(), host.size());
+    }
+    CK(cudaStreamSynchronize(h->st));  // the previous schedule buffer may still be in use
+    if (host.size() > h->sched_bytes) {
+        if (h->d_sched)
+            cudaFree(h->d_sched);
+        h->d_sched = nullptr;
+        h->sched_bytes = 0;
+        CK(cudaMalloc(&h->d_sched, host.size()));
+        h->sched_bytes = host.size();
+    }
+    CK(cudaMemcpyAsync(h->d_sched, host.data(), host.size(), cudaMemcpyHostToDevice, h->st));
+    if (h->kernel == KER_GRID_BITS) {
+        GridBitsParams p = grid_params(h, 1, n_sweeps, false);
+        p.planes_sched = (const uint32_t *)h->d_sched;
+        CK(launch_grid_bits(p, h->G, h->threads, h->smem, h->st));
+        h->cur ^= 1;
+        h->t += (uint32_t)n_sweeps;
+    } else if (h->kernel == KER_CSR_BITS) {
+        CsrBitsParams p = csr_params(h, 1, n_sweeps, false);
+        p.planes_sched = (const uint32_t *)h->d_sched;
+        CK(launch_csr_bits(p, h->G, h->threads, h->smem, h->st));
+        h->cur ^= 1;
+        h->t += (uint32_t)n_sweeps;
+    } else {
+        rc = launch_sweeps_i8(h, n_sweeps, h->d_sched);
+        if (rc)
+            return rc;
+    }
+    CK(cudaStreamSynchronize(h->st));  // host table buffer goes out of scope
+    return do_exchange(h, nullptr, 0, false);  // best-so-far check after the anneal
 }
 
 int ising_icm(ising_handle *h, int32_t k_min)

@@ -41,6 +41,7 @@ struct GridBitsParams {
     int32_t n_rounds;          // rounds of k_ex sweeps in this launch
     int32_t k_ex;              // sweeps per round
     int32_t qcap;              // capacity of the shared-memory tail queue
+    const uint32_t *planes_sched;  // annealing: [sweep][K/32][2][64] per-sweep planes, or null
     // fused PT (pt = 1, launched as clusters of words_per_copy CTAs = one copy each)
     int32_t pt;
     uint32_t e0;               // exchange index of the first round
@@ -68,6 +69,7 @@ struct CsrBitsParams {
     uint32_t g0, t0;
     int32_t n_rounds, k_ex;    // n_rounds x k_ex sweeps in this launch
     int32_t qcap;
+    const uint32_t *planes_sched;  // annealing: [sweep][K/32][qmax][64] per-sweep planes, or null
     int32_t pt;                // fused PT (clusters of words_per_copy CTAs)
     uint32_t e0;
     int64_t *walker;

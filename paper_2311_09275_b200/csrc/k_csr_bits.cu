@@ -199,6 +199,16 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_csr_bits(const CsrBitsPa
         for (int s = 0; s < p.k_ex; ++s) {
             const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + s);
             const PlaneUniform U = plane_uniform(g, t, rkr);
+            if (p.planes_sched) {  // annealing: this sweep's threshold planes
+                __syncthreads();
+                const uint32_t *src_p =
+                    p.planes_sched + (size_t)(round * p.k_ex + s) * p.words_per_copy * p.qmax * 64;
+                for (int x = tid; x < p.qmax * 64; x += nt) {
+                    const int q = x / 64, j = x % 64;
+                    P[q * kRow + j] = src_p[((size_t)wt * p.qmax + q) * 64 + j];
+                }
+                __syncthreads();
+            }
 #pragma unroll 1
             for (int c = 0; c < p.ncol; ++c) {
                 const int v0 = __ldg(p.class_off + c), v1 = __ldg(p.class_off + c + 1);

@@ -157,6 +157,13 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
         for (int s = 0; s < p.k_ex; ++s) {
             const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + s);
             const PlaneUniform U = plane_uniform(g, t, rkr);
+            if (p.planes_sched) {  // annealing: this sweep's threshold planes
+                __syncthreads();
+                const uint32_t *src_p = p.planes_sched + (size_t)(round * p.k_ex + s) * p.words_per_copy * 128;
+                for (int j = tid; j < 128; j += nt)
+                    P[j] = src_p[wt * 128 + j];
+                __syncthreads();
+            }
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
                 uint32_t *Sc = S + c * G.half;

@@ -51,6 +51,10 @@ class Engine:
     def exchange(self):
         L.ising_exchange(self.h)
 
+    def anneal(self, schedule):
+        """Simulated annealing: sweep s uses schedule[s, k] for temperature index k."""
+        L.ising_anneal(self.h, schedule)
+
     def icm(self, k_min: int):
         """Houdayer cluster move on copy pairs at temperatures k >= k_min."""
         L.ising_icm(self.h, k_min)
@@ -119,6 +123,18 @@ class Engine:
             self.close()
         except Exception:
             pass
+
+
+def geometric_schedule(betas, sweeps: int, start: float, end: float):
+    """Annealing schedule: every slot's beta_k scaled by a geometric ramp from `start` to
+    `end` over the sweeps ("T multiplied by the geometric factor each
+    sweep")."""
+    betas = np.asarray(betas, np.float64)
+    if sweeps == 1:
+        return (betas * end)[None, :]
+    s = np.arange(sweeps, dtype=np.float64) / (sweeps - 1)
+    ramp = start * np.power(end / start, s)
+    return ramp[:, None] * betas[None, :]
 
 
 def shard(C: int, world: int, rank: int):

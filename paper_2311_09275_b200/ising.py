@@ -22,7 +22,7 @@ ISING_RNG_PLANE, ISING_RNG_WORD = 0, 1
 LAYOUTS = {"bits": ISING_SPINS_BITS, "i8": ISING_SPINS_I8}
 
 EXPORTED = [
-    "ising_create_grid", "ising_create_csr", "ising_sweep", "ising_run", "ising_energy", "ising_cut",
+    "ising_create_grid", "ising_create_csr", "ising_sweep", "ising_run", "ising_anneal", "ising_energy", "ising_cut",
     "ising_exchange", "ising_icm", "ising_exchange_begin", "ising_exchange_end", "ising_check_best",
     "ising_best", "ising_copy_best", "ising_get_spins", "ising_set_spins", "ising_get_walkers", "ising_info",
     "ising_sync", "ising_last_error", "ising_destroy", "ising_greedy_colour", "ising_threshold",
@@ -76,6 +76,7 @@ def lib(build_if_missing: bool = True):
         "ising_create_csr": ([i32, vp, vp, vp, i32, vp, C.POINTER(RunDesc), C.POINTER(vp)], C.c_int),
         "ising_sweep": ([vp, i32], C.c_int),
         "ising_run": ([vp, i32, i32], C.c_int),
+        "ising_anneal": ([vp, i32, vp], C.c_int),
         "ising_energy": ([vp, vp], C.c_int),
         "ising_cut": ([vp, vp], C.c_int),
         "ising_exchange": ([vp], C.c_int),
@@ -180,6 +181,12 @@ def ising_sweep(h, n_sweeps: int):
 
 def ising_run(h, n_rounds: int, k_ex: int):
     _check(lib().ising_run(h, int(n_rounds), int(k_ex)))
+
+
+def ising_anneal(h, schedule):
+    """schedule: (n_sweeps, K) inverse temperatures."""
+    s = np.ascontiguousarray(schedule, np.float64)
+    _check(lib().ising_anneal(h, int(s.shape[0]), _ptr(s)))
 
 
 def ising_energy(h) -> np.ndarray:

@@ -376,3 +376,31 @@ def test_icm_c2_sampled_pair_and_errors():
     i8 = Engine(grid(8, 8, 1), 8, 2, synth.beta_ladder(8), seed=1, layout="i8")
     with pytest.raises(L.IsingError):
         i8.icm(0)
+
+
+@pytest.mark.parametrize("kind,layout,K,C", [("grid", "bits", 64, 2), ("csr", "bits", 32, 2),
+                                             ("grid", "i8", 8, 3), ("float", "i8", 8, 2)])
+def test_anneal_parity(kind, layout, K, C):
+    """Simulated annealing (NEXT-3): GPU == oracle, per-sweep schedules."""
+    from paper_2311_09275_b200.driver import geometric_schedule
+    if kind == "grid":
+        inst = grid(10, 8, 12)
+    elif kind == "csr":
+        inst = csr_pm1(150, 260, 4, signed=True)
+    else:
+        inst = _regular_inst(400, 8)
+    betas = synth.beta_ladder(K)
+    sched = geometric_schedule(betas, 30, 0.2, 2.5)
+    eng = Engine(inst, K, C, betas, seed=KEY, layout=layout)
+    eng.anneal(sched)
+    rng = oracle.RNG_PLANE if layout == "bits" else oracle.RNG_WORD
+    o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=rng)
+    o.anneal(sched)
+    for r in range(K * C):
+        assert np.array_equal(eng.spins(r), o.s[r]), r
+    if kind == "float":
+        assert np.allclose(eng.energies(), o.energies(), rtol=1e-5, atol=0)
+    else:
+        assert np.array_equal(eng.energies(), o.energies())
+        b = eng.best(spins=False)
+        assert (b["E"], b["slot"], b["sweep"]) == (o.best.E, o.best.slot, o.best.sweep)
