@@ -404,3 +404,14 @@ def test_anneal_parity(kind, layout, K, C):
         assert np.array_equal(eng.energies(), o.energies())
         b = eng.best(spins=False)
         assert (b["E"], b["slot"], b["sweep"]) == (o.best.E, o.best.slot, o.best.sweep)
+
+
+def test_certify_cut_on_gpu_matches_definition():
+    from paper_2311_09275_b200 import gset
+    u, v = synth.gnm(500, 1200, 3)
+    w = (synth._below(synth.splitmix64(4, u.size), 5) - 2).astype(np.int32)
+    w[w == 0] = 1
+    bits = gset.decode_hex(gset.encode_hex((synth.splitmix64(5, 500) >> np.uint64(63)).astype(np.uint8)), 500)
+    s = gset.bits_to_spins(bits)
+    rep = gset.certify(500, u, v, w, s, claimed=gset.cut_of(u, v, w, s))
+    assert rep["cut"] == rep["cut_gpu"] and rep["matches_claim"]
