@@ -75,7 +75,13 @@ __device__ __forceinline__ uint4 philox_plane(uint32_t sA, uint32_t sB, uint32_t
     return make_uint4(c0, c1, c2, c3);
 }
 
-__device__ __forceinline__ uint32_t mux(uint32_t m, uint32_t a, uint32_t b) { return (m & a) | (~m & b); }
+// m ? a : b bitwise, as ONE lop3 (the compiler otherwise splits it when ~m is live)
+__device__ __forceinline__ uint32_t mux(uint32_t m, uint32_t a, uint32_t b)
+{
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(r) : "r"(m), "r"(a), "r"(b));
+    return r;
+}
 
 // Planes 4*j4 .. 4*j4+3 of the lazy MSB-first comparison.  Lanes in D have
 // dE = 8 (m8 set) or dE = 4 (m8 clear); P4/P8 are the word type's planes.

@@ -59,7 +59,13 @@ __device__ __forceinline__ CsrSite csr_eval(const uint32_t *S, const CsrBitsPara
     return r;
 }
 
-__device__ __forceinline__ uint32_t mux(uint32_t m, uint32_t a, uint32_t b) { return (m & a) | (~m & b); }
+// m ? a : b bitwise, as ONE lop3 (the compiler otherwise splits it when ~m is live)
+__device__ __forceinline__ uint32_t mux(uint32_t m, uint32_t a, uint32_t b)
+{
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(r) : "r"(m), "r"(a), "r"(b));
+    return r;
+}
 
 // Threshold planes 4*j4 .. 4*j4+3 of each lane: row q-1 with q = d - 2u.
 __device__ __forceinline__ uint4 csr_thr4(const uint32_t *P, const CsrSite &s, uint32_t j4)
