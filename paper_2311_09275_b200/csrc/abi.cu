@@ -533,7 +533,7 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
             CK(cudaMemcpyAsync(h->d_wf, wfv.data(), (size_t)m2 * 4, cudaMemcpyHostToDevice, h->st));
             std::vector<float> bf(h->R);
             for (int64_t r = 0; r < h->R; ++r)
-                bf[r] = (float)h->betas[(h->slot0 + r) % h->K];
+                bf[r] = 2.0f * (float)h->betas[(h->slot0 + r) % h->K];  // exact doubling
             CK(h->alloc(&h->d_betaf, h->R));
             CK(cudaMemcpyAsync(h->d_betaf, bf.data(), h->R * 4, cudaMemcpyHostToDevice, h->st));
         }
@@ -1054,7 +1054,7 @@ int ising_anneal(ising_handle *h, int32_t n_sweeps, const double *sched)
         std::vector<float> all((size_t)h->R * n_sweeps);
         for (int32_t s = 0; s < n_sweeps; ++s)
             for (int64_t r = 0; r < h->R; ++r)
-                all[(size_t)s * h->R + r] = (float)sched[(size_t)s * h->K + (h->slot0 + r) % h->K];
+                all[(size_t)s * h->R + r] = 2.0f * (float)sched[(size_t)s * h->K + (h->slot0 + r) % h->K];
         host.resize(all.size() * 4);
         std::memcpy(host.data(), all.data(), host.size());
     }

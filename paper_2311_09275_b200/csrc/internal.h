@@ -91,7 +91,7 @@ struct CsrI8Params {
     const float *wf;           // float weights or null
     const uint32_t *orig;      // internal -> original id
     const uint64_t *T;         // [R][qmax+1] integer thresholds per LOCAL replica (q = dE/2)
-    const float *betaf;        // [R] float(beta_k) per LOCAL replica, float weights
+    const float *betaf;        // [R] 2 * float(beta_k) per LOCAL replica, float weights
     int32_t R;                 // local replicas (multiple of 4)
     int32_t nq;                // R / 4
     int32_t nq_shift;          // log2(threads per vertex) if a power of two, else -1

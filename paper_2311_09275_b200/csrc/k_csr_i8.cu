@@ -54,25 +54,32 @@ __device__ __forceinline__ uint64_t thr_f32(float betaf, float dE)
 }
 
 // Fast, exact decision of (hi:lo) < floor(cexp32(x) 2^64) for x = -(beta dE) < 0 from the
-// 32-bit word hi alone when it is far from the threshold: e = ex2.approx
-// estimate of cexp32(x) 2^32 with relative error <= 2^-13 (verified exhaustively over all
-// float x in [-64, 0] by tests/test_gpu_parity.py::test_exp_bracket_bound); margin 2^-12.
-// Returns 1 = accept, 0 = reject, -1 = undecided (caller evaluates the exact threshold).
-__device__ __forceinline__ int fast_decide(float x, uint32_t hi)
+// 32-bit word hi alone when it is far from the threshold: e = ex2.approx(
+// fma(x, log2 e, 32)) estimates cexp32(x) 2^32 with relative error <= 2^-13 (verified
+// exhaustively over every float x in [-64, 0] by ising_debug_exp_bound, which evaluates this
+// exact expression); margin 2^-12.  For x < -64 (contract threshold 0) e < 2^-60, so only
+// hi = 0 stays undecided and the exact path rejects it.  Returns 1 = accept, 0 = reject,
+// -1 = undecided (caller evaluates the exact threshold).
+__device__ __forceinline__ float exp_est32(float x)
 {
     float e;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fadd_rn(__fmul_rn(x, 0x1.715476p+0f), 32.0f)));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmaf_rn(x, 0x1.715476p+0f, 32.0f)));
+    return e;
+}
+
+__device__ __forceinline__ int fast_decide(float x, uint32_t hi)
+{
+    const float e = exp_est32(x);
     const float hf = __uint2float_rn(hi);
-    const bool in_range = x >= -64.0f;  // below -64 the contract threshold is exactly 0
-    const bool acc = in_range && __fadd_rn(hf, 2.0f) <= __fmul_rn(e, 1.0f - 0x1p-12f);
-    const bool rej = !in_range || hf >= __fmul_rn(e, 1.0f + 0x1p-12f);
+    const bool acc = hf <= __fmaf_rn(e, 1.0f - 0x1p-12f, -2.0f);
+    const bool rej = hf >= __fmul_rn(e, 1.0f + 0x1p-12f);
     return acc ? 1 : (rej ? 0 : -1);
 }
 
 }  // namespace
 
 // Exhaustive check of the fast-decision bound: max over all float x in [-64, 0] of
-// |ex2.approx(x log2e + 32) / (cexp32(x) 2^32) - 1|, as float bits in *out (atomicMax).
+// |exp_est32(x) / (cexp32(x) 2^32) - 1|, as float bits in *out (atomicMax).
 __global__ void k_debug_exp_bound(uint32_t *out)
 {
     const uint32_t lo = 0x80000000u, hi = 0xC2800000u;  // -0 .. -64
@@ -80,8 +87,7 @@ __global__ void k_debug_exp_bound(uint32_t *out)
     for (uint64_t b = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= hi;
          b += (uint64_t)gridDim.x * blockDim.x) {
         const float x = __uint_as_float((uint32_t)b);
-        float e;
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fadd_rn(__fmul_rn(x, 0x1.715476p+0f), 32.0f)));
+        const float e = exp_est32(x);
         const float c = __fmul_rn(cexp32(x), 0x1p32f);
         const float rel = fabsf(e / c - 1.0f);
         worst = fmaxf(worst, rel);
@@ -192,11 +198,13 @@ __global__ void __launch_bounds__(256, 4) k_csr_i8_phase(const CsrI8Params p)
                 bool need = false;
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    // dE = -2 s h: flip h's sign by the own spin's sign bit, times -2 (exact)
+                    // s h (the own spin's sign bit xor-ed into h); dE = -2 s h is exact, so
+                    // dE <= 0 <=> s h >= 0 and x = -(beta dE) = RN((2 beta) * (s h)) exactly
                     const uint32_t sbit = (own[w] << (24 - 8 * b)) & 0x80000000u;
-                    dEv[b] = __fmul_rn(-2.0f, __uint_as_float(__float_as_uint(hf[4 * w + b]) ^ sbit));
-                    flip[b] = dEv[b] <= 0.0f;
-                    x[b] = -__fmul_rn(__ldg(p.betaf + r0 + b), dEv[b]);
+                    const float sh = __uint_as_float(__float_as_uint(hf[4 * w + b]) ^ sbit);
+                    dEv[b] = -2.0f * sh;
+                    flip[b] = sh >= 0.0f;
+                    x[b] = __fmul_rn(__ldg(p.betaf + r0 + b), sh);  // betaf holds 2 beta_k
                     need |= !flip[b];
                 }
                 if (need) {
@@ -216,7 +224,7 @@ __global__ void __launch_bounds__(256, 4) k_csr_i8_phase(const CsrI8Params p)
                         for (int b = 0; b < 4; ++b) {
                             T[b] = 0;
                             if (dec[b] < 0) {
-                                T[b] = thr_f32(__ldg(p.betaf + r0 + b), dEv[b]);
+                                T[b] = thr_f32(0.5f * __ldg(p.betaf + r0 + b), dEv[b]);
                                 const uint32_t th = (uint32_t)(T[b] >> 32);
                                 dec[b] = hw[b] < th ? 1 : (hw[b] > th ? 0 : -1);
                                 tie |= dec[b] < 0;
