@@ -807,19 +807,21 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
     if (desc->block_threads == 0) {
         h->threads = 0;
         for (int32_t np = 1; np <= Ly && !h->threads; ++np) {
-            const int32_t rows = (Ly + np - 1) / np;
+            int32_t rows = (Ly + np - 1) / np;
+            if (rows >= 2)
+                rows += rows & 1;  // grid_rows_per_pass keeps rows per pass even
             const int32_t nt = ((hx * rows + 127) / 128) * 128;
             if (nt <= kGridMaxThreads)
                 h->threads = nt;
         }
         if (!h->threads)
-            return fail(ISING_E_UNSUPPORTED, "BITS grid: Lx/2 exceeds the CTA size limit");
+            return fail(ISING_E_UNSUPPORTED, "BITS grid: Lx exceeds the CTA size limit");
     }
     if (h->threads > kGridMaxThreads)
         return fail(ISING_E_ARG, "BITS grid: block_threads must be <= " + std::to_string(kGridMaxThreads));
-    if (hx > h->threads)
-        return fail(ISING_E_UNSUPPORTED, "BITS grid needs block_threads >= Lx/2");
-    const int32_t rpp = h->threads / hx, npass = (Ly + rpp - 1) / rpp;
+    if (2 * hx > h->threads)  // two class rows per pass at least (even rows per pass)
+        return fail(ISING_E_UNSUPPORTED, "BITS grid needs block_threads >= Lx");
+    const int32_t rpp = grid_rows_per_pass(h->threads, hx), npass = (Ly + rpp - 1) / rpp;
     if (npass > 31)
         return fail(ISING_E_UNSUPPORTED, "BITS grid: too many rows per thread (Ly/(threads/(Lx/2)) > 31)");
     // J bytes in colour-separated order: bit 0..3 = (right, left, down, up) bond has J = -1

@@ -134,6 +134,28 @@ __device__ __forceinline__ void plane_call2(uint32_t sA, uint32_t sB, const Plan
     }
 }
 
+// Shared-memory word / byte access at an explicit 32-bit shared address.  volatile keeps
+// them ordered among themselves and against barriers; plain C++ accesses of the same
+// arrays elsewhere are separated from them by __syncthreads.
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v)
+{
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt()
 {
     uint32_t r;

@@ -17,6 +17,16 @@ enum Kernel : int32_t { KER_GRID_BITS = 0, KER_CSR_BITS = 1, KER_CSR_I8 = 2 };
 // registers); CTA sizes are multiples of 4 warps so the four schedulers get equal work.
 constexpr int32_t kGridMaxThreads = 768;
 
+// Rows of a colour class per pass of the 2-D thread mapping: threads / (Lx/2), rounded
+// down to an even number when >= 2 so that the parity (c + y) & 1 of a thread's sites is
+// the same in every pass.  The host uses the same rule (abi.cu) to validate the shape.
+__host__ __device__ inline int grid_rows_per_pass(int threads, int hx)
+{
+    const int r = threads / hx;
+    return r >= 2 ? (r & ~1) : r;
+}
+
+
 // Best-so-far record kept in device memory (updated by the exchange kernel).
 struct BestDev {
     int64_t energy;  // int64, or double bits

@@ -38,6 +38,18 @@ using namespace bits;
 
 namespace {
 
+__device__ __forceinline__ int T_m_plus1_off(int tid, int hx)
+{
+    const int m = tid % hx;
+    return m + 1 == hx ? 1 - hx : 1;
+}
+
+__device__ __forceinline__ int T_m_minus1_off(int tid, int hx)
+{
+    const int m = tid % hx;
+    return m == 0 ? hx - 1 : -1;
+}
+
 // Site geometry of one thread in the 2-D mapping (column m of a colour class,
 // rows ty, ty + rpp, ...).
 struct ThreadGeom {
@@ -70,15 +82,18 @@ __device__ __forceinline__ void site_unsat(const uint32_t *S, const uint8_t *JB,
 
 }  // namespace
 
+// tail-queue item: {l | i_orig << 16, D, acc, m8} (the own word is re-read from S)
+constexpr int kGridQItem = 16;
+
 int32_t grid_bits_qcap(int32_t n)
 {
     const size_t base = (size_t)4 * n + (((size_t)n + 15) & ~(size_t)15) + 512 +
                         (size_t)8 * ((n + 31) / 32);
     const size_t half = (size_t)n / 2;
-    size_t qcap = half < 4096 ? half : 4096;
+    size_t qcap = half;
     const size_t budget = 200 * 1024;
-    if (base + qcap * kQItemBytes > budget)
-        qcap = base < budget ? (budget - base) / kQItemBytes : 0;
+    if (base + qcap * kGridQItem > budget)
+        qcap = base < budget ? (budget - base) / kGridQItem : 0;
     return (int32_t)qcap;
 }
 
@@ -86,7 +101,7 @@ size_t grid_bits_smem(int32_t n)
 {
     // S (4n) + JB (n, padded to 16) + planes (512) + queue + 2 boundary bit planes
     return (size_t)4 * n + (((size_t)n + 15) & ~(size_t)15) + 512 +
-           (size_t)grid_bits_qcap(n) * kQItemBytes + (size_t)8 * ((n + 31) / 32);
+           (size_t)grid_bits_qcap(n) * kGridQItem + (size_t)8 * ((n + 31) / 32);
 }
 
 __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBitsParams p)
@@ -103,15 +118,13 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
     uint32_t *S = sm;
     uint8_t *JB = reinterpret_cast<uint8_t *>(sm + n);
     uint32_t *P = reinterpret_cast<uint32_t *>(JB + ((n + 15) & ~15));  // P[0..63] dE=4, P[64..127] dE=8
-    uint32_t *Q = P + 128;
+    uint4 *Q4 = reinterpret_cast<uint4 *>(P + 128);  // tail queue (16-byte items)
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = nt >> 5;
     const int qcap = p.qcap;
     const int wcap = qcap / nwarps;  // per-warp queue region
-    uint32_t *q_idx = Q, *q_own = Q + qcap, *q_D = Q + 2 * qcap, *q_acc = Q + 3 * qcap,
-             *q_m8 = Q + 4 * qcap;
     const int nbw = (n + 31) / 32;
-    uint32_t *B0 = Q + 5 * qcap;  // boundary bit planes for cross-word swaps (PT mode)
+    uint32_t *B0 = reinterpret_cast<uint32_t *>(Q4 + qcap);  // boundary bit planes (PT mode)
     uint32_t *B31 = B0 + nbw;
     const int wq0 = warp * wcap;
 
@@ -129,8 +142,14 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
     const uint32_t c_global = g / (uint32_t)KW;
 
     // 2-D thread mapping: column m = tid % hx of a class row, rows ty + k*rpp
-    const int rpp = nt / G.hx;  // rows per pass (host guarantees >= 1)
+    const int rpp = grid_rows_per_pass(nt, G.hx);  // even when possible (host guarantees >= 1)
     const int npass = (G.Ly + rpp - 1) / rpp;
+    // neighbour offsets of a class column: m+1 and m-1 wrapped, rows below/above wrapped
+    const int offR1 = T_m_plus1_off(tid, G.hx), offL0 = T_m_minus1_off(tid, G.hx);
+    const uint32_t hx4 = 4u * (uint32_t)G.hx;
+    const uint32_t wrapDb = 4u * (uint32_t)((1 - G.Ly) * G.hx), wrapUb = 4u * (uint32_t)((G.Ly - 1) * G.hx);
+    const uint32_t sS = (uint32_t)__cvta_generic_to_shared(S);
+    const uint32_t sJB = (uint32_t)__cvta_generic_to_shared(JB);
     ThreadGeom T;
     T.ty = tid / G.hx;
     T.m = tid - T.ty * G.hx;
@@ -167,17 +186,38 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
                 uint32_t *Sc = S + c * G.half;
-                // stage 1: planes 0..7 for every site; undecided words go to this warp's queue
+                // stage 1: planes 0..7 for every site; undecided words go to this warp's queue.
+                // rpp is even, so a thread's sites all have parity par = (c + ty) & 1 and fixed
+                // horizontal neighbour offsets; rows advance by rpp per pass.  Shared-memory
+                // addresses are explicit 32-bit byte addresses advanced per pass.
+                const int par = (c + T.ty) & 1;
+                const int hx = G.hx;
+                const uint32_t l0 = (uint32_t)(T.ty * hx + T.m);
+                uint32_t aC = sS + 4u * ((uint32_t)(c * G.half) + l0);        // own word
+                uint32_t aO = sS + 4u * ((uint32_t)((1 - c) * G.half) + l0);  // same cell, other class
+                uint32_t aJ = sJB + (uint32_t)(c * G.half) + l0;
+                const uint32_t offRb = 4u * (uint32_t)(par ? offR1 : 0);
+                const uint32_t offLb = 4u * (uint32_t)(par ? 0 : offL0);
+                const uint32_t rstep = (uint32_t)(rpp * hx), istep = (uint32_t)(G.Lx * rpp);
+                uint32_t i_orig = (uint32_t)(2 * T.m + par + G.Lx * T.ty);
                 int wq = 0;  // warp-uniform
-                for (int pass = 0; pass < npass; ++pass) {
-                    const int y = T.ty + pass * rpp;
+                int y = T.ty;
+#pragma unroll 1
+                for (int pass = 0; pass < npass;
+                     ++pass, y += rpp, aC += 4u * rstep, aO += 4u * rstep, aJ += rstep, i_orig += istep) {
                     const bool valid = T.active && y < G.Ly;
-                    const int l = y * G.hx + T.m;
-                    uint32_t own = 0, D = 0, acc = 0, m8 = 0, i_orig = 0;
+                    uint32_t own = 0, D = 0, acc = 0, m8 = 0;
                     if (valid) {
-                        own = Sc[l];
-                        uint32_t a0, a1, a2, a3;
-                        site_unsat(S, JB, G, T, c, y, own, a0, a1, a2, a3, i_orig);
+                        own = lds_u32(aC);
+                        const uint32_t xr = lds_u32(aO + offRb);
+                        const uint32_t xl = lds_u32(aO + offLb);
+                        const uint32_t xd = lds_u32(aO + (y + 1 == G.Ly ? wrapDb : hx4));
+                        const uint32_t xu = lds_u32(aO + (y == 0 ? wrapUb : 0u - hx4));
+                        const uint32_t jw = lds_u8(aJ) * 0x10204080u;
+                        const uint32_t a0 = ~(own ^ xr ^ byte_sign_mask<0>(jw));
+                        const uint32_t a1 = ~(own ^ xl ^ byte_sign_mask<1>(jw));
+                        const uint32_t a2 = ~(own ^ xd ^ byte_sign_mask<2>(jw));
+                        const uint32_t a3 = ~(own ^ xu ^ byte_sign_mask<3>(jw));
                         const uint32_t s01 = a0 ^ a1, c01 = a0 & a1;
                         const uint32_t s23 = a2 ^ a3, c23 = a2 & a3;
                         m8 = ~(s01 | c01 | s23 | c23);                   // u = 0 -> dE = 8
@@ -195,12 +235,8 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
                     const int slot = wq + __popc(pm & lanemask_lt());
                     wq += __popc(pm);
                     if (need && slot < wcap) {
-                        const int qs = wq0 + slot;
-                        q_idx[qs] = (uint32_t)l | (i_orig << 16);
-                        q_own[qs] = own;
-                        q_D[qs] = D;
-                        q_acc[qs] = acc;
-                        q_m8[qs] = m8;
+                        const uint32_t l = (aC - sS) / 4u - (uint32_t)(c * G.half);
+                        Q4[wq0 + slot] = make_uint4(l | (i_orig << 16), D, acc, m8);
                     } else if (valid) {
                         if (need) {  // this warp's queue region is full: finish inline
                             uint32_t sA, sB;
@@ -211,7 +247,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
                                 ++j4;
                             } while (D && j4 < 16u);
                         }
-                        Sc[l] = own ^ acc;
+                        sts_u32(aC, own ^ acc);
                     }
                 }
                 if (lane == 0)
@@ -243,12 +279,11 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
                     const int base_lo = __shfl_sync(0xFFFFFFFFu, excl, lo);
                     if (q >= nq)
                         continue;
-                    const int qs = lo * wcap + (q - base_lo);
-                    const uint32_t idx = q_idx[qs];
-                    const int l = (int)(idx & 0xFFFFu);
-                    const uint32_t i_orig = idx >> 16;
-                    uint32_t D = q_D[qs], acc = q_acc[qs];
-                    const uint32_t m8 = q_m8[qs];
+                    const uint4 item = Q4[lo * wcap + (q - base_lo)];
+                    const int l = (int)(item.x & 0xFFFFu);
+                    const uint32_t i_orig = item.x >> 16;
+                    uint32_t D = item.y, acc = item.z;
+                    const uint32_t m8 = item.w;
                     uint32_t sA, sB;
                     plane_site(i_orig, U, rkr, sA, sB);
                     uint32_t j4 = 2;
@@ -256,7 +291,8 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
                         plane_call(sA, sB, j4, U, rkr, P, m8, D, acc);
                         ++j4;
                     } while (D && j4 < 16u);
-                    Sc[l] = q_own[qs] ^ acc;
+                    const uint32_t a = sS + 4u * ((uint32_t)(c * G.half) + (uint32_t)l);
+                    sts_u32(a, lds_u32(a) ^ acc);  // queued words were not written in stage 1
                 }
                 __syncthreads();
             }
