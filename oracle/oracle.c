@@ -288,14 +288,20 @@ static uint64_t plane_u64(const uint32_t planes[64], int64_t r)
     return u;
 }
 
-/* U64 of the WORD contract: hi = word (r&3) of Philox(i,t,r>>2,WORD_HI<<24),
- * lo = word (r&3) of Philox(i,t,r>>2,WORD_LO<<24). */
+/* U64 of the WORD contract: U = hi16 * 2^48 + lo48 with
+ * hi16 = 16-bit half (r & 1) (half 0 = the low 16 bits) of word ((r >> 1) & 3) of
+ * Philox(i, t, r >> 3, WORD_HI<<24), and lo48 = w0 * 2^16 + (w1 >> 16) of
+ * Philox(i, t, r, WORD_LO<<24).  Written out in full (the library draws lo48 only when
+ * hi16 == T >> 48, which cannot change U < T). */
 static uint64_t word_u64(uint64_t seed, uint32_t i, uint32_t t, int64_t r)
 {
     uint32_t hi[4], lo[4];
-    philox_at(seed, i, t, (uint32_t)(r >> 2), (uint32_t)ST_WORD_HI << 24, hi);
-    philox_at(seed, i, t, (uint32_t)(r >> 2), (uint32_t)ST_WORD_LO << 24, lo);
-    return ((uint64_t)hi[r & 3] << 32) | (uint64_t)lo[r & 3];
+    philox_at(seed, i, t, (uint32_t)(r >> 3), (uint32_t)ST_WORD_HI << 24, hi);
+    philox_at(seed, i, t, (uint32_t)r, (uint32_t)ST_WORD_LO << 24, lo);
+    uint32_t w = hi[(r >> 1) & 3];
+    uint64_t hi16 = (r & 1) ? (w >> 16) : (w & 0xFFFFu);
+    uint64_t lo48 = ((uint64_t)lo[0] << 16) | (uint64_t)(lo[1] >> 16);
+    return (hi16 << 48) | lo48;
 }
 
 /* Metropolis sweeps t0 .. t0+nsweeps-1.  One sweep visits the colour classes

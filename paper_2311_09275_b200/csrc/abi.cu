@@ -82,6 +82,7 @@ struct ising_handle {
     uint32_t ymagic = 0;
     int32_t cnt_levels = 8;
     int32_t qmax = 0;
+    int32_t ell_deg = 0;  // I8: width of the padded neighbour table (0 = CSR path)
     std::vector<int32_t> class_off;
     // device buffers
     uint32_t *d_state[2] = {nullptr, nullptr};
@@ -165,8 +166,8 @@ int validate_desc(const ising_run_desc *d)
         return fail(ISING_E_ARG, "I8 layout requires the WORD RNG contract");
     if (d->layout == ISING_SPINS_BITS && (d->n_temps % 32 != 0 || d->n_temps > 256))
         return fail(ISING_E_ARG, "BITS layout requires n_temps % 32 == 0 and <= 256");
-    if (d->layout == ISING_SPINS_I8 && d->n_temps % 4 != 0)
-        return fail(ISING_E_ARG, "I8 layout requires n_temps % 4 == 0");
+    if (d->layout == ISING_SPINS_I8 && d->n_temps % 8 != 0)  // one WORD Philox call = 8 replicas
+        return fail(ISING_E_ARG, "I8 layout requires n_temps % 8 == 0");
     if ((int64_t)d->n_copies * d->n_temps >= (int64_t)1 << 33)
         return fail(ISING_E_ARG, "too many replicas");
     if (d->block_threads != 0 && (d->block_threads < 32 || d->block_threads > 1024 ||
@@ -538,6 +539,7 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
             CK(cudaMemcpyAsync(h->d_betaf, bf.data(), h->R * 4, cudaMemcpyHostToDevice, h->st));
         }
         if (maxdeg <= 4) {
+            h->ell_deg = maxdeg;
             // padded 4-wide neighbour table (row order kept, pad col = -1, w = 0)
             std::vector<int32_t> ec((size_t)n * 4, -1), ew((size_t)n * 4, 0);
             for (int32_t v = 0; v < n; ++v)
@@ -577,13 +579,14 @@ int launch_sweeps_i8(ising_handle *h, int32_t ns, const void *sched)
     p.nq = (int32_t)(h->R / 4);
     p.ell_col = h->d_ell_col;
     p.ell_w = h->d_ell_w;
-    const int32_t tpv = (int32_t)(h->R % 8 == 0 ? h->R / 8 : h->R / 4);  // threads per vertex
+    p.ell_deg = h->ell_deg;
+    const int32_t tpv = (int32_t)(h->R / 8);  // threads per vertex
     p.nq_shift = -1;
     for (int sh = 0; sh < 31; ++sh)
         if ((1 << sh) == tpv)
             p.nq_shift = sh;
     p.slot0 = h->slot0; p.qmax = h->qmax; p.rk = h->rk;
-    const int32_t thr = h->threads > 256 ? 256 : h->threads;
+    const int32_t thr = h->threads > kI8Threads ? kI8Threads : h->threads;
     for (int32_t s = 0; s < ns; ++s) {
         p.t = h->t + (uint32_t)s;
         if (sched) {

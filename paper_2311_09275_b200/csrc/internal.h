@@ -17,6 +17,9 @@ enum Kernel : int32_t { KER_GRID_BITS = 0, KER_CSR_BITS = 1, KER_CSR_I8 = 2 };
 // registers); CTA sizes are multiples of 4 warps so the four schedulers get equal work.
 constexpr int32_t kGridMaxThreads = 768;
 
+// k_csr_i8_phase CTA size and the resident CTAs per SM its register budget is sized for
+constexpr int32_t kI8Threads = 256, kI8MinBlocks = 3;
+
 // Rows of a colour class per pass of the 2-D thread mapping: threads / (Lx/2), rounded
 // down to an even number when >= 2 so that the parity (c + y) & 1 of a thread's sites is
 // the same in every pass.  The host uses the same rule (abi.cu) to validate the shape.
@@ -97,6 +100,7 @@ struct CsrI8Params {
     const int32_t *col;        // internal ids
     const int32_t *ell_col;    // [n][4] padded neighbour table (pad -1) or null (CSR path)
     const int32_t *ell_w;      // [n][4] weights (int32 or float bits), pad 0
+    int32_t ell_deg;           // used width of the ELL table (max degree, <= 4)
     const int32_t *wi;         // int weights or null
     const float *wf;           // float weights or null
     const uint32_t *orig;      // internal -> original id

@@ -3,19 +3,23 @@
 // Rows a3-a4 (field + decision + flip) for the I8 layout: any int32 or float32
 // couplings (C5: random 3-regular with N(0,1) float32 weights; C1 torus in
 // int8).  Spins are stored s[v][r] (internal vertex v, local replica r,
-// replica-minor), so a warp that owns 128 consecutive replicas of one vertex
-// reads every neighbour row as one coalesced 128-byte segment.
+// replica-minor), so the 32 threads that own the R = 256 replicas of one vertex
+// read every neighbour row as one coalesced 256-byte segment.
 //
-// One thread = (vertex of the current colour class, 4 consecutive replicas as
-// char4).  Field h = sum_j w_ij s_j: exact int32 for integer weights; for float
-// weights a left fold in the CSR row order with round-to-nearest adds and no
-// contraction (h = ((0 + t0) + t1) + t2, t = +-w) -- the order is part of the
-// contract.  dE = -2 s h.  dE <= 0 accepts
-// without drawing randomness; otherwise the WORD contract draws
-// hi = word (r&3) of Philox(i, t, r>>2, WORD_HI<<24) and, only if
-// hi == T >> 32, lo from the WORD_LO stream: accept iff (hi<<32 | lo) < T,
-// T = floor(exp(-beta_k dE) 2^64) (integer: host table; float: the float32
-// contract exponential cexp32 below).
+// One thread = (vertex of the current colour class, 8 consecutive replicas as
+// two 32-bit words).  The field is evaluated in relative signs: sigma_j =
+// s_i s_j is bit 7 of each byte of own ^ nb_j, and s_i h = sum_j w_ij sigma_j
+// (exact int32; float: a left fold in CSR row order with round-to-nearest adds
+// and no contraction, ((0 + t0) + t1) + t2 -- multiplying every term by s_i
+// commutes exactly with RN addition, up to the sign of a zero, which cannot
+// change the decision s_i h >= 0).  dE = -2 s_i h: s_i h >= 0
+// flips without randomness; otherwise the WORD contract
+// decides U < T with U = hi16 * 2^48 + lo48:
+//   hi16 = 16-bit half (r & 1) of word ((r >> 1) & 3) of Philox(i, t, r >> 3, WORD_HI<<24)
+//   lo48 = w0 * 2^16 + (w1 >> 16) of Philox(i, t, r, WORD_LO<<24)   (only if hi16 == T >> 48)
+// so one Philox call serves the thread's 8 attempts.  T = floor(exp(-beta dE) 2^64):
+// integer weights from the host table; float weights from the float32 contract
+// exponential cexp32, which is only evaluated when a fast estimate cannot decide.
 #include "internal.h"
 
 namespace ising {
@@ -44,42 +48,54 @@ __device__ __forceinline__ float cexp32(float x)
     return __fmul_rn(p, __int_as_float(((int)k + 127) << 23));
 }
 
-__device__ __forceinline__ uint64_t thr_f32(float betaf, float dE)
+// Contract threshold floor(cexp32(x) 2^64), saturated, for x = -(beta dE) <= 0.
+__device__ __forceinline__ uint64_t thr_x(float x)
 {
-    const float x = -__fmul_rn(betaf, dE);
     const float v = __fmul_rn(cexp32(x), 0x1p64f);
     if (v >= 0x1p64f)
         return ~0ull;
     return __float2ull_rz(v);
 }
 
-// Fast, exact decision of (hi:lo) < floor(cexp32(x) 2^64) for x = -(beta dE) < 0 from the
-// 32-bit word hi alone when it is far from the threshold: e = ex2.approx(
-// fma(x, log2 e, 32)) estimates cexp32(x) 2^32 with relative error <= 2^-13 (verified
-// exhaustively over every float x in [-64, 0] by ising_debug_exp_bound, which evaluates this
-// exact expression); margin 2^-12.  For x < -64 (contract threshold 0) e < 2^-60, so only
-// hi = 0 stays undecided and the exact path rejects it.  Returns 1 = accept, 0 = reject,
-// -1 = undecided (caller evaluates the exact threshold).
-__device__ __forceinline__ float exp_est32(float x)
+// e = ex2.approx(fma(x, log2 e, 16)) estimates cexp32(x) 2^16 = T / 2^48 with relative
+// error below 2^-17 (measured 3.6e-6 = 2^-18.1, checked exhaustively over every float x in
+// [-64, 0] by ising_debug_exp_bound, which evaluates this exact expression).  With the
+// 2^-16 margin (> twice the error bound):
+//   2^23 + hi16 <= RN(e (1 - 2^-16) + 2^23 - 2)  =>  hi16 + 1 <= T / 2^48  =>  accept
+//   2^23 + hi16 >= RN(e (1 + 2^-16) + 2^23 + 1)  =>  hi16 > T / 2^48      =>  reject
+// (the RN of a value near 2^23 is within 1/2, covered by the -2 / +1 slack)
+// and anything else is decided exactly.  For x < -64 (T = 0) e < 2^-76,
+// so only hi16 = 0 stays undecided and the exact path rejects it.
+__device__ __forceinline__ float exp_est16(float x)
 {
     float e;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmaf_rn(x, 0x1.715476p+0f, 32.0f)));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmaf_rn(x, 0x1.715476p+0f, 16.0f)));
     return e;
 }
 
-__device__ __forceinline__ int fast_decide(float x, uint32_t hi)
+constexpr float kLoMargin = 1.0f - 0x1p-16f, kHiMargin = 1.0f + 0x1p-16f;
+
+// lo48 of replica r: Philox(i, t, r, WORD_LO<<24) words 0 and 1
+__device__ __forceinline__ uint64_t lo48_of(uint32_t io, uint32_t t, uint32_t r, const RoundKeys &rk)
 {
-    const float e = exp_est32(x);
-    const float hf = __uint2float_rn(hi);
-    const bool acc = hf <= __fmaf_rn(e, 1.0f - 0x1p-12f, -2.0f);
-    const bool rej = hf >= __fmul_rn(e, 1.0f + 0x1p-12f);
-    return acc ? 1 : (rej ? 0 : -1);
+    const uint4 l = philox(io, t, r, ST_WORD_LO << 24, rk);
+    return ((uint64_t)l.x << 16) | (uint64_t)(l.y >> 16);
+}
+
+// exact U < T for hi16 on the tie path
+__device__ __forceinline__ bool exact_less(uint32_t hi16, uint64_t T, uint32_t io, uint32_t t, uint32_t r,
+                                           const RoundKeys &rk)
+{
+    const uint32_t th = (uint32_t)(T >> 48);
+    if (hi16 != th)
+        return hi16 < th;
+    return lo48_of(io, t, r, rk) < (T & 0xFFFFFFFFFFFFull);
 }
 
 }  // namespace
 
 // Exhaustive check of the fast-decision bound: max over all float x in [-64, 0] of
-// |exp_est32(x) / (cexp32(x) 2^32) - 1|, as float bits in *out (atomicMax).
+// |exp_est16(x) / (cexp32(x) 2^16) - 1|, as float bits in *out (atomicMax).
 __global__ void k_debug_exp_bound(uint32_t *out)
 {
     const uint32_t lo = 0x80000000u, hi = 0xC2800000u;  // -0 .. -64
@@ -87,8 +103,8 @@ __global__ void k_debug_exp_bound(uint32_t *out)
     for (uint64_t b = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= hi;
          b += (uint64_t)gridDim.x * blockDim.x) {
         const float x = __uint_as_float((uint32_t)b);
-        const float e = exp_est32(x);
-        const float c = __fmul_rn(cexp32(x), 0x1p32f);
+        const float e = exp_est16(x);
+        const float c = __fmul_rn(cexp32(x), 0x1p16f);
         const float rel = fabsf(e / c - 1.0f);
         worst = fmaxf(worst, rel);
     }
@@ -101,216 +117,231 @@ cudaError_t launch_debug_exp_bound(uint32_t *out, cudaStream_t st)
     return cudaGetLastError();
 }
 
-// One thread = (vertex of the current colour class, W words = 4W consecutive replicas).
+// Philox4x32-10 with each round's products as one 64-bit multiply (IMAD.WIDE.U32).
+__device__ __forceinline__ uint4 philox_w(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                          const RoundKeys &rk)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ rk.k[2 * r];
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ rk.k[2 * r + 1];
+        c1 = (uint32_t)p1;
+        c3 = (uint32_t)p0;
+        c0 = n0;
+        c2 = n2;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+// 2^23 + hi16 as a float (exact), from half (b & 1) of word w: one PRMT
+template <int b>
+__device__ __forceinline__ float hi16_f(uint32_t w)
+{
+    uint32_t r;
+    // bytes (lo..hi): hi16 low byte, hi16 high byte, 0x00, 0x4B  (0x4B000000 = 2^23)
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(0x4B000000u), "n"((b & 1) ? 0x7432 : 0x7410));
+    return __uint_as_float(r);
+}
+
+// One thread = (vertex v of the current colour class, local replicas 8o .. 8o+7), with
+// o = blockIdx.y * blockDim.x + threadIdx.x fixed for the thread's lifetime and vertices strided over (blockIdx.x, threadIdx.y).
 // ELL: neighbours from the padded 4-wide table (one 16-byte load per vertex, pad = -1)
 // instead of row_ptr -> col -> spins, so a neighbour-row load depends on one load only.
-template <bool FLOAT, bool ELL, int W>
-__global__ void __launch_bounds__(256, 4) k_csr_i8_phase(const CsrI8Params p)
+template <bool FLOAT, bool ELL>
+__global__ void __launch_bounds__(kI8Threads, kI8MinBlocks) k_csr_i8_phase(const CsrI8Params p)
 {
     const uint32_t rw = (uint32_t)p.R >> 2;  // 32-bit words per vertex row
-    const uint32_t ntv = rw / W;             // threads per vertex
-    const uint32_t total = (uint32_t)(p.v_end - p.v_begin) * ntv;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    const uint32_t *s32 = reinterpret_cast<const uint32_t *>(p.s);
-    for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
-        const uint32_t vv = p.nq_shift >= 0 ? idx >> p.nq_shift : idx / ntv;
-        const uint32_t o = idx - vv * ntv;
-        const int32_t v = p.v_begin + (int32_t)vv;
-        const uint32_t wbase = (uint32_t)v * rw + o * W;  // first own word
-        uint32_t own[W];
-        if (W == 2) {
-            const uint2 t2 = *reinterpret_cast<const uint2 *>(s32 + wbase);
-            own[0] = t2.x;
-            own[W - 1] = t2.y;
-        } else {
-            own[0] = s32[wbase];
-        }
-        float hf[4 * W];
-        int32_t hi[4 * W];
-#pragma unroll
-        for (int a = 0; a < 4 * W; ++a) {
-            hf[a] = 0.f;
-            hi[a] = 0;
-        }
-        auto accumulate = [&](const uint32_t (&nb)[W], uint32_t wb) {
-#pragma unroll
-            for (int w = 0; w < W; ++w)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    if (FLOAT) {
-                        // term = s_j > 0 ? w : -w == w with its sign bit xor-ed by s_j's sign bit
-                        const uint32_t sb = (nb[w] << (24 - 8 * b)) & 0x80000000u;
-                        hf[4 * w + b] = __fadd_rn(hf[4 * w + b], __uint_as_float(wb ^ sb));
-                    } else {
-                        hi[4 * w + b] += (int32_t)wb * (int32_t)(int8_t)(nb[w] >> (8 * b));
-                    }
-                }
-        };
-        auto load_nb = [&](int32_t j, uint32_t (&nb)[W]) {
-            const uint32_t a = (uint32_t)j * rw + o * W;
-            if (W == 2) {
-                const uint2 t2 = __ldg(reinterpret_cast<const uint2 *>(s32 + a));
-                nb[0] = t2.x;
-                nb[W - 1] = t2.y;
-            } else {
-                nb[0] = __ldg(s32 + a);
-            }
-        };
+    const uint32_t ntv = rw >> 1;            // threads per vertex (8 replicas each)
+    const uint32_t o = blockIdx.y * blockDim.x + threadIdx.x;
+    if (o >= ntv)
+        return;
+    const uint32_t nv = (uint32_t)(p.v_end - p.v_begin);
+    const uint32_t vstride = gridDim.x * blockDim.y;
+    uint32_t *tb = reinterpret_cast<uint32_t *>(p.s) + 2u * o;  // this thread's column of words
+    const uint32_t g0 = (uint32_t)(p.slot0 >> 3) + o;            // Philox counter word 2
+    const float4 *bp = reinterpret_cast<const float4 *>(p.betaf) + 2u * o;  // 2 beta_k (float)
+    // software pipeline: the next vertex's neighbour table row and original id are loaded
+    // one iteration ahead, so a vertex's spin-row loads issue as soon as it starts
+    uint32_t vv = blockIdx.x * blockDim.y + threadIdx.y;
+    int4 c_nx = make_int4(-1, -1, -1, -1), w_nx = make_int4(0, 0, 0, 0);
+    uint32_t io_nx = 0u;
+    if (vv < nv) {
+        io_nx = __ldg(p.orig + p.v_begin + (int32_t)vv);
         if (ELL) {
-            const int4 c = __ldg(reinterpret_cast<const int4 *>(p.ell_col) + v);
-            const int4 wv = __ldg(reinterpret_cast<const int4 *>(p.ell_w) + v);
-            const int32_t cs[4] = {c.x, c.y, c.z, c.w};
-            const uint32_t ws[4] = {(uint32_t)wv.x, (uint32_t)wv.y, (uint32_t)wv.z, (uint32_t)wv.w};
-            uint32_t nbv[4][W];
+            c_nx = __ldg(reinterpret_cast<const int4 *>(p.ell_col) + p.v_begin + (int32_t)vv);
+            w_nx = __ldg(reinterpret_cast<const int4 *>(p.ell_w) + p.v_begin + (int32_t)vv);
+        }
+    }
+    for (; vv < nv; vv += vstride) {
+        const int32_t v = p.v_begin + (int32_t)vv;
+        uint2 *own_p = reinterpret_cast<uint2 *>(tb + (uint32_t)v * rw);
+        const uint32_t io = io_nx;
+        const uint2 own = *own_p;
+        // x[u] = own ^ nb_u: bit 8b+7 of word w set iff s_i != s_j for replica 4w+b
+        uint2 x[4];
+        uint32_t wv[4];
+        if (ELL) {
+            const int32_t cs[4] = {c_nx.x, c_nx.y, c_nx.z, c_nx.w};
+            wv[0] = (uint32_t)w_nx.x; wv[1] = (uint32_t)w_nx.y; wv[2] = (uint32_t)w_nx.z; wv[3] = (uint32_t)w_nx.w;
+            uint2 nb[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                nb[u] = own;  // a pad (col -1, w 0) adds an exact zero term
+                if (u < p.ell_deg && cs[u] >= 0)
+                    nb[u] = __ldg(reinterpret_cast<const uint2 *>(tb + (uint32_t)cs[u] * rw));
+            }
+            const uint32_t vn = vv + vstride;
+            if (vn < nv) {
+                io_nx = __ldg(p.orig + p.v_begin + (int32_t)vn);
+                c_nx = __ldg(reinterpret_cast<const int4 *>(p.ell_col) + p.v_begin + (int32_t)vn);
+                w_nx = __ldg(reinterpret_cast<const int4 *>(p.ell_w) + p.v_begin + (int32_t)vn);
+            }
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (cs[u] >= 0)
-                    load_nb(cs[u], nbv[u]);
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (cs[u] >= 0)  // row order: ELL slots keep the CSR order, pads at the end
-                    accumulate(nbv[u], ws[u]);
+                x[u] = make_uint2(own.x ^ nb[u].x, own.y ^ nb[u].y);
         } else {
-            const int32_t e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
-            for (int32_t eb = e0; eb < e1; eb += 4) {
-                const int32_t cnt = e1 - eb < 4 ? e1 - eb : 4;
-                uint32_t nbv[4][W];
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (u < cnt)
-                        load_nb(__ldg(p.col + eb + u), nbv[u]);
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (u < cnt)
-                        accumulate(nbv[u], FLOAT ? __float_as_uint(__ldg(p.wf + eb + u))
-                                                 : (uint32_t)__ldg(p.wi + eb + u));
-            }
+            const uint32_t vn = vv + vstride;
+            if (vn < nv)
+                io_nx = __ldg(p.orig + p.v_begin + (int32_t)vn);
         }
-        uint32_t fm[W];
-        const uint32_t io = __ldg(p.orig + v);
+        // one Philox call for the 8 replicas (issued early: independent of the loads)
+        const uint4 h = philox_w(io, p.t, g0, ST_WORD_HI << 24, p.rk);
+        const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+        uint32_t fm0 = 0u, fm1 = 0u;  // flip masks (0xFE per flipped byte)
+        if (FLOAT) {
+            float sh[8];
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-            const uint32_t r0 = 4u * (o * W + w);  // local replica of byte 0 of this word
-            const uint32_t quad = (uint32_t)(p.slot0 >> 2) + o * W + w;
-            bool flip[4];
-            if (FLOAT) {
-                float dEv[4], x[4];
-                bool need = false;
+            for (int b = 0; b < 8; ++b)
+                sh[b] = 0.0f;
+            auto fold = [&](const uint2 &xx, uint32_t w) {
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    // s h (the own spin's sign bit xor-ed into h); dE = -2 s h is exact, so
-                    // dE <= 0 <=> s h >= 0 and x = -(beta dE) = RN((2 beta) * (s h)) exactly
-                    const uint32_t sbit = (own[w] << (24 - 8 * b)) & 0x80000000u;
-                    const float sh = __uint_as_float(__float_as_uint(hf[4 * w + b]) ^ sbit);
-                    dEv[b] = -2.0f * sh;
-                    flip[b] = sh >= 0.0f;
-                    x[b] = __fmul_rn(__ldg(p.betaf + r0 + b), sh);  // betaf holds 2 beta_k
-                    need |= !flip[b];
+                for (int b = 0; b < 8; ++b) {
+                    const uint32_t word = b < 4 ? xx.x : xx.y;
+                    const uint32_t sg = (word << (24 - 8 * (b & 3))) & 0x80000000u;
+                    sh[b] = __fadd_rn(sh[b], __uint_as_float(w ^ sg));
                 }
-                if (need) {
-                    const uint4 h4 = philox(io, p.t, quad, ST_WORD_HI << 24, p.rk);
-                    const uint32_t hw[4] = {h4.x, h4.y, h4.z, h4.w};
-                    int dec[4];
-                    bool undecided = false;
+            };
+            if (ELL) {
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        dec[b] = flip[b] ? 1 : fast_decide(x[b], hw[b]);
-                        undecided |= dec[b] < 0;
-                    }
-                    if (undecided) {  // rare: exact contract threshold; lo word only on a hi tie
-                        uint64_t T[4];
-                        bool tie = false;
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) {
-                            T[b] = 0;
-                            if (dec[b] < 0) {
-                                T[b] = thr_f32(0.5f * __ldg(p.betaf + r0 + b), dEv[b]);
-                                const uint32_t th = (uint32_t)(T[b] >> 32);
-                                dec[b] = hw[b] < th ? 1 : (hw[b] > th ? 0 : -1);
-                                tie |= dec[b] < 0;
-                            }
-                        }
-                        if (tie) {
-                            const uint4 l4 = philox(io, p.t, quad, ST_WORD_LO << 24, p.rk);
-                            const uint32_t lw[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-                            for (int b = 0; b < 4; ++b)
-                                if (dec[b] < 0)
-                                    dec[b] = lw[b] < (uint32_t)T[b] ? 1 : 0;
-                        }
-                    }
-#pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        flip[b] = dec[b] == 1;
-                }
+                for (int u = 0; u < 4; ++u)
+                    if (u < p.ell_deg)  // kernel-uniform: the table's used width
+                        fold(x[u], wv[u]);
             } else {
-                uint64_t T[4];
-                bool need = false;
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int32_t sv = (int32_t)(int8_t)(own[w] >> (8 * b));
-                    const int32_t dE = -2 * sv * hi[4 * w + b];  // |h| < 2^30
-                    flip[b] = dE <= 0;
-                    T[b] = 0;
-                    if (!flip[b]) {
-                        T[b] = __ldg(p.T + (size_t)(r0 + b) * (p.qmax + 1) + (dE >> 1));
-                        need = true;
-                    }
+                const int32_t e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
+                for (int32_t e = e0; e < e1; ++e) {
+                    const uint2 nb = __ldg(reinterpret_cast<const uint2 *>(tb + (uint32_t)__ldg(p.col + e) * rw));
+                    fold(make_uint2(own.x ^ nb.x, own.y ^ nb.y), __float_as_uint(__ldg(p.wf + e)));
                 }
-                if (need) {
-                    const uint4 h4 = philox(io, p.t, quad, ST_WORD_HI << 24, p.rk);
-                    const uint32_t hw[4] = {h4.x, h4.y, h4.z, h4.w};
-                    bool tie = false;
+            }
+            uint32_t und = 0u;  // replicas the fast estimate cannot decide
+            const float4 bA = __ldg(bp), bB = __ldg(bp + 1);  // L1-resident: reloaded, not held
+            const float b2[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
+            float xs[8];
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        if (!flip[b]) {
-                            const uint32_t th = (uint32_t)(T[b] >> 32);
-                            flip[b] = hw[b] < th;
-                            tie |= hw[b] == th;
+            for (int b = 0; b < 8; ++b) {
+                // x = -(beta dE) = (2 beta)(s h) exactly; s h >= 0 flips
+                xs[b] = __fmul_rn(b2[b], sh[b]);
+                const float e = exp_est16(xs[b]);
+                const float hf = (b & 1) ? hi16_f<1>(hw[b >> 1]) : hi16_f<0>(hw[b >> 1]);  // 2^23 + hi16
+                const bool acc = sh[b] >= 0.0f || hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f);
+                const bool rej = sh[b] < 0.0f && hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f);
+                const uint32_t bit = 0xFEu << (8 * (b & 3));
+                if (b < 4)
+                    fm0 |= acc ? bit : 0u;
+                else
+                    fm1 |= acc ? bit : 0u;
+                und |= (!acc && !rej) ? (1u << b) : 0u;
+            }
+            if (__builtin_expect(und != 0u, 0)) {  // rare: exact contract threshold
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    if (und & (1u << b)) {
+                        const uint32_t hb = (b & 1) ? (hw[b >> 1] >> 16) : (hw[b >> 1] & 0xFFFFu);
+                        if (exact_less(hb, thr_x(xs[b]), io, p.t, 8u * g0 + (uint32_t)b, p.rk)) {
+                            if (b < 4)
+                                fm0 |= 0xFEu << (8 * (b & 3));
+                            else
+                                fm1 |= 0xFEu << (8 * (b & 3));
                         }
-                    }
-                    if (tie) {
-                        const uint4 l4 = philox(io, p.t, quad, ST_WORD_LO << 24, p.rk);
-                        const uint32_t lw[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-                        for (int b = 0; b < 4; ++b)
-                            if (!flip[b] && hw[b] == (uint32_t)(T[b] >> 32))
-                                flip[b] = lw[b] < (uint32_t)T[b];
                     }
                 }
             }
-            // +1 (0x01) <-> -1 (0xFF): xor the byte with 0xFE
-            fm[w] = (flip[0] ? 0x000000FEu : 0u) | (flip[1] ? 0x0000FE00u : 0u) |
-                    (flip[2] ? 0x00FE0000u : 0u) | (flip[3] ? 0xFE000000u : 0u);
+        } else {
+            int32_t sh[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+                sh[b] = 0;
+            auto fold = [&](const uint2 &xx, int32_t w) {
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const uint32_t word = b < 4 ? xx.x : xx.y;
+                    const int32_t m = (int32_t)(word << (24 - 8 * (b & 3))) >> 31;  // -1 iff s_i != s_j
+                    sh[b] += (w ^ m) - m;
+                }
+            };
+            if (ELL) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (u < p.ell_deg)
+                        fold(x[u], (int32_t)wv[u]);
+            } else {
+                const int32_t e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
+                for (int32_t e = e0; e < e1; ++e) {
+                    const uint2 nb = __ldg(reinterpret_cast<const uint2 *>(tb + (uint32_t)__ldg(p.col + e) * rw));
+                    fold(make_uint2(own.x ^ nb.x, own.y ^ nb.y), __ldg(p.wi + e));
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                bool acc = sh[b] >= 0;  // dE = -2 s h <= 0
+                if (!acc) {
+                    const uint32_t hb = (b & 1) ? (hw[b >> 1] >> 16) : (hw[b >> 1] & 0xFFFFu);
+                    const uint32_t rl = 8u * o + (uint32_t)b;  // local replica
+                    const uint64_t T = __ldg(p.T + (size_t)rl * (p.qmax + 1) + (uint32_t)(-sh[b]));
+                    acc = exact_less(hb, T, io, p.t, 8u * g0 + (uint32_t)b, p.rk);
+                }
+                if (acc) {
+                    if (b < 4)
+                        fm0 |= 0xFEu << (8 * (b & 3));
+                    else
+                        fm1 |= 0xFEu << (8 * (b & 3));
+                }
+            }
         }
-        uint32_t *dst = const_cast<uint32_t *>(s32) + wbase;
-        if (W == 2)
-            *reinterpret_cast<uint2 *>(dst) = make_uint2(own[0] ^ fm[0], own[W - 1] ^ fm[W - 1]);
-        else
-            dst[0] = own[0] ^ fm[0];
+        // +1 (0x01) <-> -1 (0xFF): xor the byte with 0xFE
+        *own_p = make_uint2(own.x ^ fm0, own.y ^ fm1);
     }
 }
 
 cudaError_t launch_csr_i8_phase(const CsrI8Params &p, int32_t threads, cudaStream_t st)
 {
-    const int32_t W = (p.R % 8 == 0) ? 2 : 1;
-    const int64_t total = (int64_t)(p.v_end - p.v_begin) * (p.R / (4 * W));
-    if (total <= 0)
-        return cudaSuccess;
-    if (total >= ((int64_t)1 << 32))
+    if (p.R % 8 != 0 || p.slot0 % 8 != 0)
         return cudaErrorInvalidValue;
-    const int64_t want = (total + threads - 1) / threads;
-    const unsigned blocks = (unsigned)(want < 148 * 32 ? want : 148 * 32);
+    const int64_t nv = (int64_t)(p.v_end - p.v_begin);
+    if (nv <= 0)
+        return cudaSuccess;
+    const int32_t ntv = p.R / 8;  // threads per vertex
+    if (threads < 32 || threads > kI8Threads)
+        threads = kI8Threads;
+    const int32_t bx = ntv < threads ? ntv : threads;
+    const int32_t by = threads / bx;
+    const int64_t gy = (ntv + bx - 1) / bx;
+    if (gy > 65535)
+        return cudaErrorInvalidValue;
+    const int64_t want = (nv + by - 1) / by;
+    const int64_t cap = (int64_t)148 * 64 / (gy < 64 ? gy : 64);  // a few waves of resident CTAs
+    const dim3 grid((unsigned)(want < cap ? want : cap), (unsigned)gy);
+    const dim3 block((unsigned)bx, (unsigned)by);
     const bool ell = p.ell_col != nullptr;
-#define LAUNCH(F, E, WW) k_csr_i8_phase<F, E, WW><<<blocks, threads, 0, st>>>(p)
     if (p.wf) {
-        if (ell) { if (W == 2) LAUNCH(true, true, 2); else LAUNCH(true, true, 1); }
-        else { if (W == 2) LAUNCH(true, false, 2); else LAUNCH(true, false, 1); }
+        if (ell) k_csr_i8_phase<true, true><<<grid, block, 0, st>>>(p);
+        else k_csr_i8_phase<true, false><<<grid, block, 0, st>>>(p);
     } else {
-        if (ell) { if (W == 2) LAUNCH(false, true, 2); else LAUNCH(false, true, 1); }
-        else { if (W == 2) LAUNCH(false, false, 2); else LAUNCH(false, false, 1); }
+        if (ell) k_csr_i8_phase<false, true><<<grid, block, 0, st>>>(p);
+        else k_csr_i8_phase<false, false><<<grid, block, 0, st>>>(p);
     }
-#undef LAUNCH
     return cudaGetLastError();
 }
 

@@ -74,8 +74,8 @@ def certify(n, u, v, w, spins, claimed=None, device: int = 0):
     from . import ising as L
     rp, col, ww = edges_to_csr(n, u, v, w)
     host = cut_of(u, v, w, spins)
-    betas = np.linspace(0.1, 3.0, 4)
-    h = L.ising_create_csr(n, rp, col, ww.astype(np.int32), seed=1, n_temps=4, n_copies=1,
+    betas = np.linspace(0.1, 3.0, 8)
+    h = L.ising_create_csr(n, rp, col, ww.astype(np.int32), seed=1, n_temps=8, n_copies=1,
                            betas=betas, layout="i8", device=device)
     try:
         L.ising_set_spins(h, 0, spins)

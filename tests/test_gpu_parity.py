@@ -231,11 +231,12 @@ def _regular_inst(n, seed):
 
 
 def test_exp_bracket_bound():
-    """The I8 kernel decides float-weight attempts from the 32-bit hi word with a 2^-12
+    """The I8 kernel decides float-weight attempts from the 16-bit hi word with a 2^-16
     relative margin around an ex2.approx estimate; exact-decision safety needs the estimate
-    within 2^-13 of the contract exponential for EVERY float x in [-64, 0] (exhaustive)."""
+    within half the margin of the contract exponential for EVERY float x in [-64, 0]
+    (exhaustive; measured 3.6e-6 = 2^-18.1 on a B200)."""
     worst = L.ising_debug_exp_bound()
-    assert worst < 2.0 ** -14, worst
+    assert worst < 2.0 ** -17, worst
 
 
 def test_float_int8_parity_small():
