@@ -18,7 +18,7 @@ enum Kernel : int32_t { KER_GRID_BITS = 0, KER_CSR_BITS = 1, KER_CSR_I8 = 2 };
 constexpr int32_t kGridMaxThreads = 768;
 
 // k_csr_i8_phase CTA size and the resident CTAs per SM its register budget is sized for
-constexpr int32_t kI8Threads = 256, kI8MinBlocks = 3;
+constexpr int32_t kI8Threads = 256, kI8MinBlocks = 4;
 
 // Rows of a colour class per pass of the 2-D thread mapping: threads / (Lx/2), rounded
 // down to an even number when >= 2 so that the parity (c + y) & 1 of a thread's sites is

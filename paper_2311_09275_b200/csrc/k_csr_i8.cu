@@ -150,7 +150,7 @@ __device__ __forceinline__ float hi16_f(uint32_t w)
 // ELL: neighbours from the padded 4-wide table (one 16-byte load per vertex, pad = -1)
 // instead of row_ptr -> col -> spins, so a neighbour-row load depends on one load only.
 template <bool FLOAT, bool ELL>
-__global__ void __launch_bounds__(kI8Threads, kI8MinBlocks) k_csr_i8_phase(const CsrI8Params p)
+__global__ void __launch_bounds__(kI8Threads, FLOAT ? kI8MinBlocks : 3) k_csr_i8_phase(const CsrI8Params p)
 {
     const uint32_t rw = (uint32_t)p.R >> 2;  // 32-bit words per vertex row
     const uint32_t ntv = rw >> 1;            // threads per vertex (8 replicas each)
@@ -211,60 +211,90 @@ __global__ void __launch_bounds__(kI8Threads, kI8MinBlocks) k_csr_i8_phase(const
         const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
         uint32_t fm0 = 0u, fm1 = 0u;  // flip masks (0xFE per flipped byte)
         if (FLOAT) {
-            float sh[8];
-#pragma unroll
-            for (int b = 0; b < 8; ++b)
-                sh[b] = 0.0f;
-            auto fold = [&](const uint2 &xx, uint32_t w) {
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    const uint32_t word = b < 4 ? xx.x : xx.y;
-                    const uint32_t sg = (word << (24 - 8 * (b & 3))) & 0x80000000u;
-                    sh[b] = __fadd_rn(sh[b], __uint_as_float(w ^ sg));
-                }
-            };
-            if (ELL) {
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (u < p.ell_deg)  // kernel-uniform: the table's used width
-                        fold(x[u], wv[u]);
-            } else {
-                const int32_t e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
-                for (int32_t e = e0; e < e1; ++e) {
-                    const uint2 nb = __ldg(reinterpret_cast<const uint2 *>(tb + (uint32_t)__ldg(p.col + e) * rw));
-                    fold(make_uint2(own.x ^ nb.x, own.y ^ nb.y), __float_as_uint(__ldg(p.wf + e)));
-                }
-            }
+            // two halves of 4 replicas (one spin word each) to keep the live set small
+            const float4 *bph = bp;
             uint32_t und = 0u;  // replicas the fast estimate cannot decide
-            const float4 bA = __ldg(bp), bB = __ldg(bp + 1);  // L1-resident: reloaded, not held
-            const float b2[8] = {bA.x, bA.y, bA.z, bA.w, bB.x, bB.y, bB.z, bB.w};
-            float xs[8];
 #pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                // x = -(beta dE) = (2 beta)(s h) exactly; s h >= 0 flips
-                xs[b] = __fmul_rn(b2[b], sh[b]);
-                const float e = exp_est16(xs[b]);
-                const float hf = (b & 1) ? hi16_f<1>(hw[b >> 1]) : hi16_f<0>(hw[b >> 1]);  // 2^23 + hi16
-                const bool acc = sh[b] >= 0.0f || hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f);
-                const bool rej = sh[b] < 0.0f && hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f);
-                const uint32_t bit = 0xFEu << (8 * (b & 3));
-                if (b < 4)
-                    fm0 |= acc ? bit : 0u;
-                else
-                    fm1 |= acc ? bit : 0u;
-                und |= (!acc && !rej) ? (1u << b) : 0u;
-            }
-            if (__builtin_expect(und != 0u, 0)) {  // rare: exact contract threshold
+            for (int half = 0; half < 2; ++half) {
+                float sh[4];
+                if (ELL) {
 #pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    if (und & (1u << b)) {
-                        const uint32_t hb = (b & 1) ? (hw[b >> 1] >> 16) : (hw[b >> 1] & 0xFFFFu);
-                        if (exact_less(hb, thr_x(xs[b]), io, p.t, 8u * g0 + (uint32_t)b, p.rk)) {
-                            if (b < 4)
-                                fm0 |= 0xFEu << (8 * (b & 3));
-                            else
-                                fm1 |= 0xFEu << (8 * (b & 3));
+                    for (int b = 0; b < 4; ++b)
+                        sh[b] = 0.0f;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (u < p.ell_deg) {  // kernel-uniform: the table's used width
+                            const uint32_t word = half ? x[u].y : x[u].x;
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) {
+                                const uint32_t sg = (word << (24 - 8 * b)) & 0x80000000u;
+                                sh[b] = __fadd_rn(sh[b], __uint_as_float(wv[u] ^ sg));
+                            }
                         }
+                } else {
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        sh[b] = 0.0f;
+                    const int32_t e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
+                    for (int32_t e = e0; e < e1; ++e) {
+                        const uint32_t nbw = __ldg(tb + (uint32_t)__ldg(p.col + e) * rw + (uint32_t)half);
+                        const uint32_t word = (half ? own.y : own.x) ^ nbw;
+                        const uint32_t w = __float_as_uint(__ldg(p.wf + e));
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const uint32_t sg = (word << (24 - 8 * b)) & 0x80000000u;
+                            sh[b] = __fadd_rn(sh[b], __uint_as_float(w ^ sg));
+                        }
+                    }
+                }
+                const float4 bq = __ldg(bph + half);  // 2 beta_k, L1-resident
+                const float b2[4] = {bq.x, bq.y, bq.z, bq.w};
+                uint32_t fm = 0u;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    // x = -(beta dE) = (2 beta)(s h) exactly; s h >= 0 flips
+                    const float xv = __fmul_rn(b2[b], sh[b]);
+                    const float e = exp_est16(xv);
+                    const uint32_t hword = hw[2 * half + (b >> 1)];
+                    const float hf = (b & 1) ? hi16_f<1>(hword) : hi16_f<0>(hword);  // 2^23 + hi16
+                    const bool acc = sh[b] >= 0.0f || hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f);
+                    const bool rej = sh[b] < 0.0f && hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f);
+                    fm |= acc ? (0xFEu << (8 * b)) : 0u;
+                    und |= (!acc && !rej) ? (1u << (4 * half + b)) : 0u;
+                }
+                if (half)
+                    fm1 = fm;
+                else
+                    fm0 = fm;
+            }
+            if (__builtin_expect(und != 0u, 0)) {  // rare: recompute the field, exact threshold
+#pragma unroll 1
+                for (int b = 0; b < 8; ++b) {
+                    if (!(und & (1u << b)))
+                        continue;
+                    float shb = 0.0f;
+                    if (ELL) {
+                        for (int u = 0; u < p.ell_deg; ++u) {
+                            const uint32_t word = b < 4 ? x[u].x : x[u].y;
+                            shb = __fadd_rn(shb, __uint_as_float(wv[u] ^ ((word << (24 - 8 * (b & 3))) & 0x80000000u)));
+                        }
+                    } else {
+                        const int32_t e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
+                        for (int32_t e = e0; e < e1; ++e) {
+                            const uint32_t nbw = __ldg(tb + (uint32_t)__ldg(p.col + e) * rw + (uint32_t)(b >> 2));
+                            const uint32_t word = (b < 4 ? own.x : own.y) ^ nbw;
+                            shb = __fadd_rn(shb, __uint_as_float(__float_as_uint(__ldg(p.wf + e)) ^
+                                                                 ((word << (24 - 8 * (b & 3))) & 0x80000000u)));
+                        }
+                    }
+                    const float xv = __fmul_rn(__ldg(p.betaf + 8u * o + (uint32_t)b), shb);
+                    const uint32_t hword = hw[b >> 1];
+                    const uint32_t hb = (b & 1) ? (hword >> 16) : (hword & 0xFFFFu);
+                    if (exact_less(hb, thr_x(xv), io, p.t, 8u * g0 + (uint32_t)b, p.rk)) {
+                        if (b < 4)
+                            fm0 |= 0xFEu << (8 * (b & 3));
+                        else
+                            fm1 |= 0xFEu << (8 * (b & 3));
                     }
                 }
             }
