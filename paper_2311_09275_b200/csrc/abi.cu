@@ -540,8 +540,13 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
         }
         if (maxdeg <= 4) {
             h->ell_deg = maxdeg;
-            // padded 4-wide neighbour table (row order kept, pad col = -1, w = 0)
+            // padded 4-wide neighbour table (row order kept, pad col = self, w = 0)
+            // pads point at the vertex itself with weight 0: the kernel loads them
+            // unconditionally, own ^ own = 0 and the term is an exact zero
             std::vector<int32_t> ec((size_t)n * 4, -1), ew((size_t)n * 4, 0);
+            for (int32_t v = 0; v < n; ++v)
+                for (int32_t u = 0; u < 4; ++u)
+                    ec[(size_t)v * 4 + u] = v;
             for (int32_t v = 0; v < n; ++v)
                 for (int32_t u = 0; u < rp[v + 1] - rp[v]; ++u) {
                     ec[(size_t)v * 4 + u] = ci[rp[v] + u];

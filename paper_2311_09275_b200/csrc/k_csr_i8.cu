@@ -160,6 +160,8 @@ __global__ void __launch_bounds__(kI8Threads, FLOAT ? kI8MinBlocks : 3) k_csr_i8
     const uint32_t nv = (uint32_t)(p.v_end - p.v_begin);
     const uint32_t vstride = gridDim.x * blockDim.y;
     uint32_t *tb = reinterpret_cast<uint32_t *>(p.s) + 2u * o;  // this thread's column of words
+    char *tbb = reinterpret_cast<char *>(tb);                    // ... as bytes: one IMAD.WIDE per row
+    const uint32_t rwb = 4u * rw;                                // row bytes
     const uint32_t g0 = (uint32_t)(p.slot0 >> 3) + o;            // Philox counter word 2
     const float4 *bp = reinterpret_cast<const float4 *>(p.betaf) + 2u * o;  // 2 beta_k (float)
     // software pipeline: the next vertex's neighbour table row and original id are loaded
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(kI8Threads, FLOAT ? kI8MinBlocks : 3) k_csr_i8
     }
     for (; vv < nv; vv += vstride) {
         const int32_t v = p.v_begin + (int32_t)vv;
-        uint2 *own_p = reinterpret_cast<uint2 *>(tb + (uint32_t)v * rw);
+        uint2 *own_p = reinterpret_cast<uint2 *>(tbb + (uint32_t)v * rwb);
         const uint32_t io = io_nx;
         const uint2 own = *own_p;
         // x[u] = own ^ nb_u: bit 8b+7 of word w set iff s_i != s_j for replica 4w+b
@@ -188,9 +190,9 @@ __global__ void __launch_bounds__(kI8Threads, FLOAT ? kI8MinBlocks : 3) k_csr_i8
             uint2 nb[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                nb[u] = own;  // a pad (col -1, w 0) adds an exact zero term
-                if (u < p.ell_deg && cs[u] >= 0)
-                    nb[u] = __ldg(reinterpret_cast<const uint2 *>(tb + (uint32_t)cs[u] * rw));
+                nb[u] = own;  // a pad (col = self, w 0) adds an exact zero term
+                if (u < p.ell_deg)  // kernel-uniform
+                    nb[u] = __ldg(reinterpret_cast<const uint2 *>(tbb + (uint32_t)cs[u] * rwb));
             }
             const uint32_t vn = vv + vstride;
             if (vn < nv) {
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(kI8Threads, FLOAT ? kI8MinBlocks : 3) k_csr_i8
         if (FLOAT) {
             // two halves of 4 replicas (one spin word each) to keep the live set small
             const float4 *bph = bp;
-            uint32_t und = 0u;  // replicas the fast estimate cannot decide
+            bool und = false;  // some replica the fast estimate cannot decide
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 float sh[4];
@@ -258,20 +260,18 @@ __global__ void __launch_bounds__(kI8Threads, FLOAT ? kI8MinBlocks : 3) k_csr_i8
                     const uint32_t hword = hw[2 * half + (b >> 1)];
                     const float hf = (b & 1) ? hi16_f<1>(hword) : hi16_f<0>(hword);  // 2^23 + hi16
                     const bool acc = sh[b] >= 0.0f || hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f);
-                    const bool rej = sh[b] < 0.0f && hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f);
+                    const bool dec = acc || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f);
                     fm |= acc ? (0xFEu << (8 * b)) : 0u;
-                    und |= (!acc && !rej) ? (1u << (4 * half + b)) : 0u;
+                    und |= !dec;
                 }
                 if (half)
                     fm1 = fm;
                 else
                     fm0 = fm;
             }
-            if (__builtin_expect(und != 0u, 0)) {  // rare: recompute the field, exact threshold
+            if (__builtin_expect(und != 0u, 0)) {  // rare: recompute field and estimate; exact threshold
 #pragma unroll 1
                 for (int b = 0; b < 8; ++b) {
-                    if (!(und & (1u << b)))
-                        continue;
                     float shb = 0.0f;
                     if (ELL) {
                         for (int u = 0; u < p.ell_deg; ++u) {
@@ -290,6 +290,12 @@ __global__ void __launch_bounds__(kI8Threads, FLOAT ? kI8MinBlocks : 3) k_csr_i8
                     const float xv = __fmul_rn(__ldg(p.betaf + 8u * o + (uint32_t)b), shb);
                     const uint32_t hword = hw[b >> 1];
                     const uint32_t hb = (b & 1) ? (hword >> 16) : (hword & 0xFFFFu);
+                    if (shb >= 0.0f)
+                        continue;
+                    const float e = exp_est16(xv);
+                    const float hf = __uint_as_float(0x4B000000u | hb);
+                    if (hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f) || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f))
+                        continue;  // decided by the fast path (same expressions)
                     if (exact_less(hb, thr_x(xv), io, p.t, 8u * g0 + (uint32_t)b, p.rk)) {
                         if (b < 4)
                             fm0 |= 0xFEu << (8 * (b & 3));
