@@ -145,6 +145,111 @@ __device__ __forceinline__ float hi16_f(uint32_t w)
     return __uint_as_float(r);
 }
 
+// Float-weight decisions of one thread's 8 replicas: field s_i h in two
+// halves of 4 replicas, fast estimate, exact contract threshold for the rare undecided.
+template <bool ELL>
+__device__ __forceinline__ void float_decide(const CsrI8Params &p, int32_t v, const uint2 own,
+                                             const uint2 (&x)[4], const uint32_t (&wv)[4],
+                                             const uint32_t *tb, uint32_t rw, uint32_t io, uint32_t g0,
+                                             uint32_t o, const float4 *bp, const uint32_t (&hw)[4],
+                                             uint32_t &fm0, uint32_t &fm1)
+{
+        // two halves of 4 replicas (one spin word each) to keep the live set small
+        const float4 *bph = bp;
+        bool und = false;  // some replica the fast estimate cannot decide
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            float sh[4];
+            if (ELL) {
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    sh[b] = 0.0f;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (u < p.ell_deg) {  // kernel-uniform: the table's used width
+                        const uint32_t word = half ? x[u].y : x[u].x;
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const uint32_t sg = (word << (24 - 8 * b)) & 0x80000000u;
+                            sh[b] = __fadd_rn(sh[b], __uint_as_float(wv[u] ^ sg));
+                        }
+                    }
+            } else {
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    sh[b] = 0.0f;
+                const int32_t e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
+                for (int32_t e = e0; e < e1; ++e) {
+                    const uint32_t nbw = __ldg(tb + (uint32_t)__ldg(p.col + e) * rw + (uint32_t)half);
+                    const uint32_t word = (half ? own.y : own.x) ^ nbw;
+                    const uint32_t w = __float_as_uint(__ldg(p.wf + e));
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const uint32_t sg = (word << (24 - 8 * b)) & 0x80000000u;
+                        sh[b] = __fadd_rn(sh[b], __uint_as_float(w ^ sg));
+                    }
+                }
+            }
+            const float4 bq = __ldg(bph + half);  // 2 beta_k, L1-resident
+            const float b2[4] = {bq.x, bq.y, bq.z, bq.w};
+            uint32_t fm = 0u;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                // x = -(beta dE) = (2 beta)(s h) exactly; s h >= 0 flips
+                const float xv = __fmul_rn(b2[b], sh[b]);
+                const float e = exp_est16(xv);
+                const uint32_t hword = hw[2 * half + (b >> 1)];
+                const float hf = (b & 1) ? hi16_f<1>(hword) : hi16_f<0>(hword);  // 2^23 + hi16
+                const bool acc = sh[b] >= 0.0f || hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f);
+                const bool dec = acc || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f);
+                fm |= acc ? (0xFEu << (8 * b)) : 0u;
+                und |= !dec;
+            }
+            if (half)
+                fm1 = fm;
+            else
+                fm0 = fm;
+        }
+        if (__builtin_expect(und != 0u, 0)) {  // rare: recompute field and estimate; exact threshold
+#pragma unroll 1
+            for (int b = 0; b < 8; ++b) {  // no dynamic indexing: x[] and hw[] stay in registers
+                float shb = 0.0f;
+                if (ELL) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (u >= p.ell_deg)
+                            break;
+                        const uint32_t word = b < 4 ? x[u].x : x[u].y;  // select, u static
+                        shb = __fadd_rn(shb, __uint_as_float(wv[u] ^ ((word << (24 - 8 * (b & 3))) & 0x80000000u)));
+                    }
+                } else {
+                    const int32_t e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
+                    for (int32_t e = e0; e < e1; ++e) {
+                        const uint32_t nbw = __ldg(tb + (uint32_t)__ldg(p.col + e) * rw + (uint32_t)(b >> 2));
+                        const uint32_t word = (b < 4 ? own.x : own.y) ^ nbw;
+                        shb = __fadd_rn(shb, __uint_as_float(__float_as_uint(__ldg(p.wf + e)) ^
+                                                             ((word << (24 - 8 * (b & 3))) & 0x80000000u)));
+                    }
+                }
+                const float xv = __fmul_rn(__ldg(p.betaf + 8u * o + (uint32_t)b), shb);
+                const uint32_t hword = (b >> 1) == 0 ? hw[0] : (b >> 1) == 1 ? hw[1] : (b >> 1) == 2 ? hw[2] : hw[3];
+                const uint32_t hb = (b & 1) ? (hword >> 16) : (hword & 0xFFFFu);
+                if (shb >= 0.0f)
+                    continue;
+                const float e = exp_est16(xv);
+                const float hf = __uint_as_float(0x4B000000u | hb);
+                if (hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f) || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f))
+                    continue;  // decided by the fast path (same expressions)
+                if (exact_less(hb, thr_x(xv), io, p.t, 8u * g0 + (uint32_t)b, p.rk)) {
+                    if (b < 4)
+                        fm0 |= 0xFEu << (8 * (b & 3));
+                    else
+                        fm1 |= 0xFEu << (8 * (b & 3));
+                }
+            }
+        }
+}
+
 // One thread = (vertex v of the current colour class, local replicas 8o .. 8o+7), with
 // o = blockIdx.y * blockDim.x + threadIdx.x fixed for the thread's lifetime and vertices strided over (blockIdx.x, threadIdx.y).
 // ELL: neighbours from the padded 4-wide table (one 16-byte load per vertex, pad = -1)
@@ -213,97 +318,7 @@ __global__ void __launch_bounds__(kI8Threads, FLOAT ? kI8MinBlocks : 3) k_csr_i8
         const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
         uint32_t fm0 = 0u, fm1 = 0u;  // flip masks (0xFE per flipped byte)
         if (FLOAT) {
-            // two halves of 4 replicas (one spin word each) to keep the live set small
-            const float4 *bph = bp;
-            bool und = false;  // some replica the fast estimate cannot decide
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                float sh[4];
-                if (ELL) {
-#pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        sh[b] = 0.0f;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (u < p.ell_deg) {  // kernel-uniform: the table's used width
-                            const uint32_t word = half ? x[u].y : x[u].x;
-#pragma unroll
-                            for (int b = 0; b < 4; ++b) {
-                                const uint32_t sg = (word << (24 - 8 * b)) & 0x80000000u;
-                                sh[b] = __fadd_rn(sh[b], __uint_as_float(wv[u] ^ sg));
-                            }
-                        }
-                } else {
-#pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        sh[b] = 0.0f;
-                    const int32_t e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
-                    for (int32_t e = e0; e < e1; ++e) {
-                        const uint32_t nbw = __ldg(tb + (uint32_t)__ldg(p.col + e) * rw + (uint32_t)half);
-                        const uint32_t word = (half ? own.y : own.x) ^ nbw;
-                        const uint32_t w = __float_as_uint(__ldg(p.wf + e));
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) {
-                            const uint32_t sg = (word << (24 - 8 * b)) & 0x80000000u;
-                            sh[b] = __fadd_rn(sh[b], __uint_as_float(w ^ sg));
-                        }
-                    }
-                }
-                const float4 bq = __ldg(bph + half);  // 2 beta_k, L1-resident
-                const float b2[4] = {bq.x, bq.y, bq.z, bq.w};
-                uint32_t fm = 0u;
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    // x = -(beta dE) = (2 beta)(s h) exactly; s h >= 0 flips
-                    const float xv = __fmul_rn(b2[b], sh[b]);
-                    const float e = exp_est16(xv);
-                    const uint32_t hword = hw[2 * half + (b >> 1)];
-                    const float hf = (b & 1) ? hi16_f<1>(hword) : hi16_f<0>(hword);  // 2^23 + hi16
-                    const bool acc = sh[b] >= 0.0f || hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f);
-                    const bool dec = acc || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f);
-                    fm |= acc ? (0xFEu << (8 * b)) : 0u;
-                    und |= !dec;
-                }
-                if (half)
-                    fm1 = fm;
-                else
-                    fm0 = fm;
-            }
-            if (__builtin_expect(und != 0u, 0)) {  // rare: recompute field and estimate; exact threshold
-#pragma unroll 1
-                for (int b = 0; b < 8; ++b) {
-                    float shb = 0.0f;
-                    if (ELL) {
-                        for (int u = 0; u < p.ell_deg; ++u) {
-                            const uint32_t word = b < 4 ? x[u].x : x[u].y;
-                            shb = __fadd_rn(shb, __uint_as_float(wv[u] ^ ((word << (24 - 8 * (b & 3))) & 0x80000000u)));
-                        }
-                    } else {
-                        const int32_t e0 = __ldg(p.rp + v), e1 = __ldg(p.rp + v + 1);
-                        for (int32_t e = e0; e < e1; ++e) {
-                            const uint32_t nbw = __ldg(tb + (uint32_t)__ldg(p.col + e) * rw + (uint32_t)(b >> 2));
-                            const uint32_t word = (b < 4 ? own.x : own.y) ^ nbw;
-                            shb = __fadd_rn(shb, __uint_as_float(__float_as_uint(__ldg(p.wf + e)) ^
-                                                                 ((word << (24 - 8 * (b & 3))) & 0x80000000u)));
-                        }
-                    }
-                    const float xv = __fmul_rn(__ldg(p.betaf + 8u * o + (uint32_t)b), shb);
-                    const uint32_t hword = hw[b >> 1];
-                    const uint32_t hb = (b & 1) ? (hword >> 16) : (hword & 0xFFFFu);
-                    if (shb >= 0.0f)
-                        continue;
-                    const float e = exp_est16(xv);
-                    const float hf = __uint_as_float(0x4B000000u | hb);
-                    if (hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f) || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f))
-                        continue;  // decided by the fast path (same expressions)
-                    if (exact_less(hb, thr_x(xv), io, p.t, 8u * g0 + (uint32_t)b, p.rk)) {
-                        if (b < 4)
-                            fm0 |= 0xFEu << (8 * (b & 3));
-                        else
-                            fm1 |= 0xFEu << (8 * (b & 3));
-                    }
-                }
-            }
+            float_decide<ELL>(p, v, own, x, wv, tb, rw, io, g0, o, bp, hw, fm0, fm1);
         } else {
             int32_t sh[8];
 #pragma unroll
