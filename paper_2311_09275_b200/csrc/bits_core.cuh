@@ -108,18 +108,18 @@ __device__ __forceinline__ void plane_call(uint32_t sA, uint32_t sB, uint32_t j4
     acc |= y2 | y3;
 }
 
-// Planes 0..7 (calls j4 = 0 and 1) with both Philox evaluations interleaved.
+// Planes 4 j4 .. 4 j4 + 7 (calls j4 and j4 + 1) with both Philox evaluations interleaved.
 __device__ __forceinline__ void plane_call2(uint32_t sA, uint32_t sB, const PlaneUniform &u,
                                             const RoundKeys &rk, const uint32_t *P, uint32_t m8,
-                                            uint32_t &D, uint32_t &acc)
+                                            uint32_t &D, uint32_t &acc, uint32_t j4 = 0u)
 {
-    const uint4 w0 = philox_plane(sA, sB, 0u, u, rk);
-    const uint4 w1 = philox_plane(sA, sB, 1u, u, rk);
+    const uint4 w0 = philox_plane(sA, sB, j4, u, rk);
+    const uint4 w1 = philox_plane(sA, sB, j4 + 1u, u, rk);
     const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-    const uint4 a4 = *reinterpret_cast<const uint4 *>(P);
-    const uint4 b4 = *reinterpret_cast<const uint4 *>(P + 4);
-    const uint4 a8 = *reinterpret_cast<const uint4 *>(P + 64);
-    const uint4 b8 = *reinterpret_cast<const uint4 *>(P + 68);
+    const uint4 a4 = *reinterpret_cast<const uint4 *>(P + 4 * j4);
+    const uint4 b4 = *reinterpret_cast<const uint4 *>(P + 4 * j4 + 4);
+    const uint4 a8 = *reinterpret_cast<const uint4 *>(P + 64 + 4 * j4);
+    const uint4 b8 = *reinterpret_cast<const uint4 *>(P + 68 + 4 * j4);
     const uint32_t t4[8] = {a4.x, a4.y, a4.z, a4.w, b4.x, b4.y, b4.z, b4.w};
     const uint32_t t8[8] = {a8.x, a8.y, a8.z, a8.w, b8.x, b8.y, b8.z, b8.w};
 #pragma unroll

@@ -186,6 +186,9 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
                 uint32_t *Sc = S + c * G.half;
+#ifdef ISING_GRID_TIMING
+                long long tA = clock64();
+#endif
                 // stage 1: planes 0..7 for every site; undecided words go to this warp's queue.
                 // rpp is even, so a thread's sites all have parity par = (c + ty) & 1 and fixed
                 // horizontal neighbour offsets; rows advance by rpp per pass.  Shared-memory
@@ -250,9 +253,15 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
                         sts_u32(aC, own ^ acc);
                     }
                 }
+#ifdef ISING_GRID_TIMING
+                long long tB = clock64();
+#endif
                 if (lane == 0)
                     wcount[warp] = min(wq, wcap);
                 __syncthreads();
+#ifdef ISING_GRID_TIMING
+                long long tC = clock64();
+#endif
                 // every warp scans the per-warp queue counts itself (no extra barrier):
                 // lane w holds the exclusive prefix of region w
                 const int cnt_l = lane < nwarps ? wcount[lane] : 0;
@@ -265,7 +274,8 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
                 }
                 const int excl = incl - cnt_l;
                 const int nq = __shfl_sync(0xFFFFFFFFu, incl, 31);
-                // stage 2: the queued tail, one word per thread, all lanes busy
+                // stage 2: the queued tail, one word per thread, all lanes busy; the first two
+                // further Philox calls are issued together (the tail is latency bound)
                 for (int qb = tid - lane; qb < nq; qb += nt) {
                     const int q = qb + lane;
                     int lo = 0;  // region: last w with excl_w <= q (binary search over lanes)
@@ -286,15 +296,25 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
                     const uint32_t m8 = item.w;
                     uint32_t sA, sB;
                     plane_site(i_orig, U, rkr, sA, sB);
-                    uint32_t j4 = 2;
-                    do {
+                    plane_call2(sA, sB, U, rkr, P, m8, D, acc, 2u);  // planes 8..15, calls interleaved
+                    uint32_t j4 = 4;
+                    while (D && j4 < 16u) {
                         plane_call(sA, sB, j4, U, rkr, P, m8, D, acc);
                         ++j4;
-                    } while (D && j4 < 16u);
+                    }
                     const uint32_t a = sS + 4u * ((uint32_t)(c * G.half) + (uint32_t)l);
                     sts_u32(a, lds_u32(a) ^ acc);  // queued words were not written in stage 1
                 }
+#ifdef ISING_GRID_TIMING
+                long long tD = clock64();
+#endif
                 __syncthreads();
+#ifdef ISING_GRID_TIMING
+                long long tE = clock64();
+                if (blockIdx.x == 0 && lane == 0 && round == 2 && s == 0)
+                    printf("T c=%d w=%2d s1=%lld b1=%lld s2=%lld b2=%lld nq=%d wq=%d\n", c, warp, tB - tA, tC - tB,
+                           tD - tC, tE - tD, nq, wq);
+#endif
             }
         }
 
