@@ -19,6 +19,9 @@ constexpr int32_t kGridMaxThreads = 768;
 
 // k_csr_i8_phase CTA size and the resident CTAs per SM its register budget is sized for
 constexpr int32_t kI8Threads = 256, kI8MinBlocks = 4;
+// float + padded-table graphs: two-deep pipelined kernel and its resident CTAs per SM
+constexpr bool kI8Pipe = true;
+constexpr int32_t kI8PipeMinBlocks = 3;
 
 // Rows of a colour class per pass of the 2-D thread mapping: threads / (Lx/2), rounded
 // down to an even number when >= 2 so that the parity (c + y) & 1 of a thread's sites is

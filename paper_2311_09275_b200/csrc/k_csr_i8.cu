@@ -366,6 +366,88 @@ __global__ void __launch_bounds__(kI8Threads, FLOAT ? kI8MinBlocks : 3) k_csr_i8
     }
 }
 
+// Float weights + padded neighbour table, two-deep software pipeline: while vertex k is
+// decided, the spin rows of vertex k+1 are already in flight (issued at the top of iteration
+// k) and the table row of vertex k+2 is being loaded, so each warp keeps two vertices' gathers
+// outstanding.
+__global__ void __launch_bounds__(kI8Threads, kI8PipeMinBlocks) k_csr_i8_pipe(const CsrI8Params p)
+{
+    const uint32_t rw = (uint32_t)p.R >> 2;
+    const uint32_t ntv = rw >> 1;
+    const uint32_t o = blockIdx.y * blockDim.x + threadIdx.x;
+    if (o >= ntv)
+        return;
+    const uint32_t nv = (uint32_t)(p.v_end - p.v_begin);
+    const uint32_t vstride = gridDim.x * blockDim.y;
+    uint32_t *tb = reinterpret_cast<uint32_t *>(p.s) + 2u * o;
+    const char *tbb = reinterpret_cast<const char *>(tb);
+    const uint32_t rwb = 4u * rw;
+    const uint32_t g0 = (uint32_t)(p.slot0 >> 3) + o;
+    const float4 *bp = reinterpret_cast<const float4 *>(p.betaf) + 2u * o;
+    const int deg = p.ell_deg;
+    const int4 *ec = reinterpret_cast<const int4 *>(p.ell_col) + p.v_begin;
+    const int4 *ew = reinterpret_cast<const int4 *>(p.ell_w) + p.v_begin;
+    const uint32_t *eo = p.orig + p.v_begin;
+    uint32_t vv = blockIdx.x * blockDim.y + threadIdx.y;
+    if (vv >= nv)
+        return;
+    auto rows = [&](uint32_t vq, const int4 &c, uint2 &own, uint2 (&nb)[4]) {
+        own = *reinterpret_cast<const uint2 *>(tbb + (p.v_begin + vq) * rwb);
+        const int32_t cs[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (u < deg)
+                nb[u] = __ldg(reinterpret_cast<const uint2 *>(tbb + (uint32_t)cs[u] * rwb));
+    };
+    // prologue: table rows of vertices 0 and 1, spin rows of vertex 0
+    int4 c1 = __ldg(ec + vv), w1 = __ldg(ew + vv);
+    uint32_t io1 = __ldg(eo + vv);
+    uint2 own1, nb1[4];
+    rows(vv, c1, own1, nb1);
+    uint32_t vq2 = vv + vstride;
+    int4 c2 = make_int4(0, 0, 0, 0), w2 = make_int4(0, 0, 0, 0);
+    uint32_t io2 = 0;
+    if (vq2 < nv) {
+        c2 = __ldg(ec + vq2);
+        w2 = __ldg(ew + vq2);
+        io2 = __ldg(eo + vq2);
+    }
+    for (; vv < nv; vv += vstride) {
+        // current vertex: rows and meta from the previous iteration
+        const uint2 own = own1;
+        uint2 nb[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            nb[u] = nb1[u];
+        const int4 wq = w1;
+        const uint32_t io = io1;
+        // next vertex: issue its spin-row gathers now; the one after: its table row
+        const uint32_t vn = vv + vstride;
+        if (vn < nv) {
+            rows(vn, c2, own1, nb1);
+            w1 = w2;
+            io1 = io2;
+            const uint32_t vn2 = vn + vstride;
+            if (vn2 < nv) {
+                c2 = __ldg(ec + vn2);
+                w2 = __ldg(ew + vn2);
+                io2 = __ldg(eo + vn2);
+            }
+        }
+        uint2 x[4];
+        const uint32_t wv[4] = {(uint32_t)wq.x, (uint32_t)wq.y, (uint32_t)wq.z, (uint32_t)wq.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            x[u] = u < deg ? make_uint2(own.x ^ nb[u].x, own.y ^ nb[u].y) : make_uint2(0u, 0u);
+        const uint4 h = philox_w(io, p.t, g0, ST_WORD_HI << 24, p.rk);
+        const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+        uint32_t fm0 = 0u, fm1 = 0u;
+        const int32_t v = p.v_begin + (int32_t)vv;
+        float_decide<true>(p, v, own, x, wv, tb, rw, io, g0, o, bp, hw, fm0, fm1);
+        *reinterpret_cast<uint2 *>(tb + (size_t)(uint32_t)v * rw) = make_uint2(own.x ^ fm0, own.y ^ fm1);
+    }
+}
+
 cudaError_t launch_csr_i8_phase(const CsrI8Params &p, int32_t threads, cudaStream_t st)
 {
     if (p.R % 8 != 0 || p.slot0 % 8 != 0)
@@ -387,7 +469,8 @@ cudaError_t launch_csr_i8_phase(const CsrI8Params &p, int32_t threads, cudaStrea
     const dim3 block((unsigned)bx, (unsigned)by);
     const bool ell = p.ell_col != nullptr;
     if (p.wf) {
-        if (ell) k_csr_i8_phase<true, true><<<grid, block, 0, st>>>(p);
+        if (ell && kI8Pipe) k_csr_i8_pipe<<<grid, block, 0, st>>>(p);
+        else if (ell) k_csr_i8_phase<true, true><<<grid, block, 0, st>>>(p);
         else k_csr_i8_phase<true, false><<<grid, block, 0, st>>>(p);
     } else {
         if (ell) k_csr_i8_phase<false, true><<<grid, block, 0, st>>>(p);
