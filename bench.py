@@ -142,14 +142,17 @@ def cpu_oracle_sample(cfg, target_s=12.0):
     n = inst["n"]
     kex = cfg["k_ex"] if cfg["k_ex"] > 0 else 0
     rng = oracle.RNG_PLANE if cfg["layout"] == "bits" else oracle.RNG_WORD
+    colour = None  # the workload's colouring, computed by the oracle's own implementation
+    if cfg.get("colouring") == "sl":
+        colour, _ = oracle.greedy_colour_sl(n, inst["row_ptr"], inst["col"])
     # calibrate on one copy x 2 sweeps
     t0 = time.perf_counter()
     if cfg["C"] == 1 and cfg["K"] > 64:
-        o = oracle.Oracle(inst, K, betas, synth.PHILOX_KEY, 0, 1, rng=rng, slots=(0, 4))
+        o = oracle.Oracle(inst, K, betas, synth.PHILOX_KEY, 0, 1, rng=rng, colour=colour, slots=(0, 4))
         o.sweeps(1)
         per = (time.perf_counter() - t0) / (4 * n)
     else:
-        o = oracle.Oracle(inst, K, betas, synth.PHILOX_KEY, 0, 1, rng=rng)
+        o = oracle.Oracle(inst, K, betas, synth.PHILOX_KEY, 0, 1, rng=rng, colour=colour)
         o.sweeps(2)
         per = (time.perf_counter() - t0) / (2 * K * n)
     if cfg["C"] == 1 and cfg["K"] > 64:
@@ -160,7 +163,8 @@ def cpu_oracle_sample(cfg, target_s=12.0):
         res = []
 
         def work(q):
-            oo = oracle.Oracle(inst, K, betas, synth.PHILOX_KEY, 0, 1, rng=rng, slots=(2 * q, 2 * q + 2))
+            oo = oracle.Oracle(inst, K, betas, synth.PHILOX_KEY, 0, 1, rng=rng, colour=colour,
+                               slots=(2 * q, 2 * q + 2))
             oo.sweeps(sweeps)
             res.append(oo)
         t0 = time.perf_counter()
@@ -176,7 +180,7 @@ def cpu_oracle_sample(cfg, target_s=12.0):
             sweeps = max(kex, (sweeps // kex) * kex)
         t0 = time.perf_counter()
         oracle.run_sharded(inst, K, betas, synth.PHILOX_KEY, 0, threads, sweeps, kex, rng=rng,
-                           threads=threads)
+                           threads=threads, colour=colour)
         dt = time.perf_counter() - t0
         attempts = n * K * threads * sweeps
         sample = f"{threads} copies x {K} temps x {sweeps} sweeps (exchange every {kex})"
@@ -261,7 +265,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     eng = Engine(inst, K, Cg, betas, seed=synth.PHILOX_KEY, copy_begin=rank * C,
                  copy_end=(rank + 1) * C, layout=cfg["layout"], device=local,
-                 block_threads=args.threads, stream=stream.cuda_stream)
+                 block_threads=args.threads, stream=stream.cuda_stream, colour=cfg.get("colouring"))
     n, R = inst["n"], eng.R
     sweeps, kex = cfg["sweeps"], cfg["k_ex"]
     rounds = sweeps // kex if kex > 0 else 0
@@ -351,7 +355,8 @@ def run_ours(args):
             a.record(stream)
             e = Engine(inst, K, Cg, betas, seed=synth.PHILOX_KEY + s, copy_begin=rank * C,
                        copy_end=(rank + 1) * C, layout=cfg["layout"], device=local,
-                       block_threads=args.threads, stream=stream.cuda_stream)
+                       block_threads=args.threads, stream=stream.cuda_stream,
+                       colour=cfg.get("colouring"))
             if fused:
                 e.run(rounds, kex)
             else:

@@ -241,6 +241,16 @@ ISING_API void ising_destroy(ising_handle *h);
 ISING_API int ising_greedy_colour(int32_t n, const int64_t *row_ptr, const int32_t *col,
                         int32_t *colour_out);
 
+/* Smallest-last greedy colouring (R12b; a "greedy colouring" in the sense of
+ * BASELINE configs[2], with at most degeneracy + 1 colours -- 3 on the sparse random
+ * graphs of C3): repeatedly remove a vertex of minimum remaining degree (ties: lowest id),
+ * then colour vertices in reverse removal order, each with the smallest colour unused by
+ * its already-coloured neighbours.  Pass the result as `colour` to ising_create_csr.
+ * row_ptr: n+1 int64, col: row_ptr[n] int32 (symmetric, as for create_csr); colour_out: n
+ * int32 (caller-owned).  Returns the number of colours, or ISING_E_ARG on NULL / n < 1. */
+ISING_API int ising_greedy_colour_sl(int32_t n, const int64_t *row_ptr, const int32_t *col,
+                        int32_t *colour_out);
+
 /* Metropolis threshold floor(exp(-(beta*dE)) * 2^64) saturated to 2^64-1, as the
  * library's host tables compute it (integer dE > 0). */
 ISING_API uint64_t ising_threshold(double beta, int64_t dE);

@@ -66,6 +66,8 @@ def lib():
             L.or_grid_to_csr.argtypes = [C.c_int32, C.c_int32, vp, vp, vp, vp, vp, vp]
             L.or_greedy_colour.argtypes = [C.c_int32, vp, vp, vp]
             L.or_greedy_colour.restype = C.c_int32
+            L.or_greedy_colour_sl.argtypes = [C.c_int32, vp, vp, vp]
+            L.or_greedy_colour_sl.restype = C.c_int32
             L.or_init.argtypes = [C.POINTER(_Run), vp]
             L.or_energy.argtypes = [C.POINTER(_Run), vp, vp, vp]
             L.or_sweeps.argtypes = [C.POINTER(_Run), vp, vp, C.c_uint32, C.c_int32]
@@ -128,6 +130,15 @@ def greedy_colour(n, row_ptr, col):
     cc = np.ascontiguousarray(col, np.int32)
     out = np.zeros(n, np.int32)
     ncol = lib().or_greedy_colour(n, _p(rp), _p(cc), _p(out))
+    return out, int(ncol)
+
+
+def greedy_colour_sl(n, row_ptr, col):
+    """Smallest-last greedy colouring (R12b), the oracle's own implementation."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cc = np.ascontiguousarray(col, np.int32)
+    out = np.zeros(n, np.int32)
+    ncol = lib().or_greedy_colour_sl(n, _p(rp), _p(cc), _p(out))
     return out, int(ncol)
 
 

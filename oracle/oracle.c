@@ -191,6 +191,103 @@ int32_t or_greedy_colour(int32_t n, const int64_t *rp, const int32_t *col, int32
     return ncol;
 }
 
+/* Smallest-last greedy colouring (R12b): repeatedly remove a vertex of
+ * minimum remaining degree, ties by lowest id; then colour the vertices in reverse
+ * removal order, each with the smallest colour not used by an already-coloured
+ * neighbour.  The minimum is kept in a binary min-heap of keys (degree << 32 | id);
+ * a degree change pushes a new key and stale keys are skipped when popped.
+ * Returns the number of colours. */
+static void heap_push(uint64_t *h, int64_t *len, uint64_t key)
+{
+    int64_t k = (*len)++;
+    h[k] = key;
+    while (k > 0 && h[(k - 1) / 2] > h[k]) {
+        uint64_t t = h[k];
+        h[k] = h[(k - 1) / 2];
+        h[(k - 1) / 2] = t;
+        k = (k - 1) / 2;
+    }
+}
+
+static uint64_t heap_pop(uint64_t *h, int64_t *len)
+{
+    uint64_t top = h[0];
+    h[0] = h[--(*len)];
+    int64_t k = 0;
+    for (;;) {
+        int64_t l = 2 * k + 1, r = l + 1, m = k;
+        if (l < *len && h[l] < h[m])
+            m = l;
+        if (r < *len && h[r] < h[m])
+            m = r;
+        if (m == k)
+            break;
+        uint64_t t = h[k];
+        h[k] = h[m];
+        h[m] = t;
+        k = m;
+    }
+    return top;
+}
+
+int32_t or_greedy_colour_sl(int32_t n, const int64_t *rp, const int32_t *col, int32_t *colour)
+{
+    int32_t maxdeg = 0;
+    for (int32_t i = 0; i < n; ++i)
+        if (rp[i + 1] - rp[i] > maxdeg)
+            maxdeg = (int32_t)(rp[i + 1] - rp[i]);
+    size_t nn = (size_t)(uint32_t)n;
+    int32_t *deg = (int32_t *)malloc(sizeof(int32_t) * nn);
+    char *gone = (char *)calloc(nn, 1);
+    int32_t *order = (int32_t *)malloc(sizeof(int32_t) * nn);
+    uint64_t *heap = (uint64_t *)malloc(sizeof(uint64_t) * (nn + (size_t)rp[n] + 1));
+    int64_t len = 0, nord = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        deg[i] = (int32_t)(rp[i + 1] - rp[i]);
+        heap_push(heap, &len, ((uint64_t)(uint32_t)deg[i] << 32) | (uint32_t)i);
+    }
+    while (len > 0) {
+        uint64_t key = heap_pop(heap, &len);
+        int32_t i = (int32_t)(key & 0xFFFFFFFFu);
+        if (gone[i] || (int32_t)(key >> 32) != deg[i])
+            continue; /* stale */
+        gone[i] = 1;
+        order[nord++] = i;
+        for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+            int32_t j = col[e];
+            if (gone[j])
+                continue;
+            deg[j]--;
+            heap_push(heap, &len, ((uint64_t)(uint32_t)deg[j] << 32) | (uint32_t)j);
+        }
+    }
+    char *used = (char *)calloc((size_t)maxdeg + 2, 1);
+    for (int32_t i = 0; i < n; ++i)
+        colour[i] = -1;
+    int32_t ncol = 0;
+    for (int64_t q = nord - 1; q >= 0; --q) {
+        int32_t i = order[q];
+        memset(used, 0, (size_t)maxdeg + 2);
+        for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+            int32_t c = colour[col[e]];
+            if (c >= 0 && c <= maxdeg + 1)
+                used[c] = 1;
+        }
+        int32_t c = 0;
+        while (used[c])
+            ++c;
+        colour[i] = c;
+        if (c + 1 > ncol)
+            ncol = c + 1;
+    }
+    free(used);
+    free(deg);
+    free(gone);
+    free(order);
+    free(heap);
+    return ncol;
+}
+
 /* ------------------------------------------------------------------- run */
 typedef struct {
     int32_t n;

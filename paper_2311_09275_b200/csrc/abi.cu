@@ -15,6 +15,8 @@
 #include <numeric>
 #include <string>
 #include <vector>
+#include <queue>
+#include <functional>
 
 #include "internal.h"
 
@@ -724,6 +726,60 @@ int ising_greedy_colour(int32_t n, const int64_t *row_ptr, const int32_t *col, i
     for (int32_t i = 0; i < n; ++i)
         colour_out[i] = -1;
     for (int32_t i = 0; i < n; ++i) {
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+            const int32_t c = colour_out[col[e]];
+            if (c >= 0 && c <= maxdeg + 1)
+                stamp[c] = i;
+        }
+        int32_t c = 0;
+        while (stamp[c] == i)
+            ++c;
+        colour_out[i] = c;
+        ncol = std::max(ncol, c + 1);
+    }
+    return ncol;
+}
+
+int ising_greedy_colour_sl(int32_t n, const int64_t *row_ptr, const int32_t *col, int32_t *colour_out)
+{
+    if (n < 1 || !row_ptr || !col || !colour_out)
+        return fail(ISING_E_ARG, "greedy_colour_sl: bad arguments");
+    // smallest-last order: repeatedly remove a vertex of minimum remaining degree (ties:
+    // lowest id) -- a min-heap of (degree << 32 | id) with lazy deletion
+    std::vector<int32_t> deg(n), order;
+    order.reserve(n);
+    std::vector<char> gone(n, 0);
+    std::priority_queue<uint64_t, std::vector<uint64_t>, std::greater<uint64_t>> heap;
+    for (int32_t i = 0; i < n; ++i) {
+        deg[i] = (int32_t)(row_ptr[i + 1] - row_ptr[i]);
+        heap.push(((uint64_t)(uint32_t)deg[i] << 32) | (uint32_t)i);
+    }
+    while (!heap.empty()) {
+        const uint64_t top = heap.top();
+        heap.pop();
+        const int32_t i = (int32_t)(top & 0xFFFFFFFFu);
+        if (gone[i] || (int32_t)(top >> 32) != deg[i])
+            continue;  // stale entry
+        gone[i] = 1;
+        order.push_back(i);
+        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+            const int32_t j = col[e];
+            if (!gone[j]) {
+                --deg[j];
+                heap.push(((uint64_t)(uint32_t)deg[j] << 32) | (uint32_t)j);
+            }
+        }
+    }
+    // greedy in reverse removal order, smallest colour unused by coloured neighbours
+    int32_t maxdeg = 0;
+    for (int32_t i = 0; i < n; ++i)
+        maxdeg = std::max<int32_t>(maxdeg, (int32_t)(row_ptr[i + 1] - row_ptr[i]));
+    std::vector<int32_t> stamp(maxdeg + 2, -1);
+    for (int32_t i = 0; i < n; ++i)
+        colour_out[i] = -1;
+    int32_t ncol = 0;
+    for (int32_t q = n - 1; q >= 0; --q) {
+        const int32_t i = order[q];
         for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
             const int32_t c = colour_out[col[e]];
             if (c >= 0 && c <= maxdeg + 1)

@@ -24,7 +24,9 @@ from . import ising as L
 
 
 class Engine:
-    """One libising handle.  inst: dict from synth.make_instance (grid or csr)."""
+    """One libising handle.  inst: dict from synth.make_instance (grid or csr).  colour (csr):
+    None = the library's ascending-id greedy colouring, "sl" = smallest-last greedy
+    (ising_greedy_colour_sl), or an explicit int32 array (validated by the library)."""
 
     def __init__(self, inst: dict, K: int, C: int, betas, seed: int, copy_begin: int = 0,
                  copy_end: int | None = None, layout: str = "bits", device: int = 0,
@@ -35,6 +37,10 @@ class Engine:
         if inst["kind"] == "grid":
             self.h = L.ising_create_grid(inst["Lx"], inst["Ly"], inst["J_right"], inst["J_down"], **kw)
         else:
+            if isinstance(colour, str):  # "sl": the library's smallest-last greedy colouring
+                if colour != "sl":
+                    raise ValueError(f"unknown colouring {colour!r}")
+                colour, _ = L.ising_greedy_colour_sl(inst["n"], inst["row_ptr"], inst["col"])
             self.h = L.ising_create_csr(inst["n"], inst["row_ptr"], inst["col"], inst["w"],
                                         colour=colour, **kw)
         self.info = L.ising_info(self.h)

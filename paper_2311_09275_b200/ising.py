@@ -25,7 +25,7 @@ EXPORTED = [
     "ising_create_grid", "ising_create_csr", "ising_sweep", "ising_run", "ising_anneal", "ising_energy", "ising_cut",
     "ising_exchange", "ising_icm", "ising_exchange_begin", "ising_exchange_end", "ising_check_best",
     "ising_best", "ising_copy_best", "ising_get_spins", "ising_set_spins", "ising_get_walkers", "ising_info",
-    "ising_sync", "ising_last_error", "ising_destroy", "ising_greedy_colour", "ising_threshold",
+    "ising_sync", "ising_last_error", "ising_destroy", "ising_greedy_colour", "ising_greedy_colour_sl", "ising_threshold",
     "ising_version", "ising_debug_philox", "ising_debug_exp_bound",
 ]
 
@@ -94,6 +94,7 @@ def lib(build_if_missing: bool = True):
         "ising_last_error": ([], C.c_char_p),
         "ising_destroy": ([vp], None),
         "ising_greedy_colour": ([i32, vp, vp, vp], C.c_int),
+        "ising_greedy_colour_sl": ([i32, vp, vp, vp], C.c_int),
         "ising_threshold": ([C.c_double, i64], C.c_uint64),
         "ising_version": ([], C.c_char_p),
         "ising_debug_philox": ([i32, vp, i32, vp, vp], C.c_int),
@@ -285,6 +286,17 @@ def ising_greedy_colour(n, row_ptr, col):
     cc = np.ascontiguousarray(col, np.int32)
     out = np.zeros(n, np.int32)
     rc = lib().ising_greedy_colour(int(n), _ptr(rp), _ptr(cc), _ptr(out))
+    if rc < 0:
+        _check(rc)
+    return out, rc
+
+
+def ising_greedy_colour_sl(n, row_ptr, col):
+    """Smallest-last greedy colouring (include/ising.h); returns (colour, n_colours)."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cc = np.ascontiguousarray(col, np.int32)
+    out = np.zeros(n, np.int32)
+    rc = lib().ising_greedy_colour_sl(int(n), _ptr(rp), _ptr(cc), _ptr(out))
     if rc < 0:
         _check(rc)
     return out, rc

@@ -188,7 +188,7 @@ CONFIGS = {
                layout="bits"),
     # configs[2]: G(1e4, 9999), J=+1, greedy colouring, 4096 replicas, 10000 sweeps
     "c3": dict(kind="gnm", n=10000, m=9999, seed=70, K=64, C=64, sweeps=10000, k_ex=10,
-               layout="bits"),
+               layout="bits", colouring="sl"),
     # configs[3]: 100x140 / 100x200 tori, 128 temps x 128 copies, 50000 sweeps
     "c4a": dict(kind="grid", Lx=100, Ly=140, seed=77, K=128, C=128, sweeps=50000, k_ex=10,
                 layout="bits"),
@@ -196,7 +196,7 @@ CONFIGS = {
                 layout="bits"),
     # configs[4]: random 3-regular 4e6 vertices, N(0,1) f32, 256 replicas/GPU, 1000 sweeps
     "c5": dict(kind="regular", n=4_000_000, d=3, seed=3, K=256, C=1, sweeps=1000, k_ex=0,
-               layout="i8"),
+               layout="i8", colouring="sl"),
 }
 
 

@@ -192,11 +192,12 @@ def test_c3_full_size_sampled_copies():
     cfg = synth.CONFIGS["c3"]
     inst = synth.make_instance(cfg)
     betas = synth.beta_ladder(cfg["K"])
-    eng = Engine(inst, cfg["K"], cfg["C"], betas, seed=KEY, layout="bits")
-    assert 3 <= eng.info.n_colours <= 6
+    eng = Engine(inst, cfg["K"], cfg["C"], betas, seed=KEY, layout="bits", colour=cfg["colouring"])
+    assert eng.info.n_colours == 3  # smallest-last greedy on G(1e4, 9999)
     run_pt(eng, 20, 10, fused=True)
+    col, _ = oracle.greedy_colour_sl(inst["n"], inst["row_ptr"], inst["col"])
     for c0 in (0, 50):
-        o = oracle.Oracle(inst, cfg["K"], betas, KEY, c0, c0 + 1, rng=oracle.RNG_PLANE).run(20, 10)
+        o = oracle.Oracle(inst, cfg["K"], betas, KEY, c0, c0 + 1, rng=oracle.RNG_PLANE, colour=col).run(20, 10)
         compare_copies(eng, o, check_best=False)
 
 
@@ -257,13 +258,15 @@ def test_c5_full_size_sampled_replicas():
     cfg = synth.CONFIGS["c5"]
     inst = synth.make_instance(cfg)
     betas = synth.beta_ladder(cfg["K"])
-    eng = Engine(inst, cfg["K"], cfg["C"], betas, seed=KEY, layout="i8")
+    eng = Engine(inst, cfg["K"], cfg["C"], betas, seed=KEY, layout="i8", colour=cfg["colouring"])
     assert eng.info.n_colours >= 3
     sweeps = 4
     eng.sweep(sweeps)
     E = eng.energies()
+    col, _ = oracle.greedy_colour_sl(inst["n"], inst["row_ptr"], inst["col"])
     for lo in (0, 255):
-        o = oracle.Oracle(inst, cfg["K"], betas, KEY, 0, 1, rng=oracle.RNG_WORD, slots=(lo, lo + 1))
+        o = oracle.Oracle(inst, cfg["K"], betas, KEY, 0, 1, rng=oracle.RNG_WORD, colour=col,
+                          slots=(lo, lo + 1))
         o.sweeps(sweeps)
         assert np.array_equal(eng.spins(lo), o.s[0])
         assert abs(E[lo] - o.energies()[0]) <= 1e-5 * abs(o.energies()[0])

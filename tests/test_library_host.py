@@ -43,6 +43,20 @@ def test_greedy_colouring_matches_oracle():
     assert na == nb and np.array_equal(a, b)
 
 
+def test_smallest_last_colouring_matches_oracle():
+    for n, m, seed in ((3000, 2999, 70), (2000, 3000, 3)):
+        u, v = synth.gnm(n, m, seed)
+        rp, col, _ = synth.edges_to_csr(n, u, v, np.ones(u.size, np.int32))
+        a, na = L.ising_greedy_colour_sl(n, rp, col)
+        b, nb = oracle.greedy_colour_sl(n, rp, col)
+        assert na == nb and np.array_equal(a, b)
+    u, v = synth.random_regular(3000, 3, 9)
+    rp, col, _ = synth.edges_to_csr(3000, u, v, np.ones(u.size, np.int32))
+    a, na = L.ising_greedy_colour_sl(3000, rp, col)
+    b, nb = oracle.greedy_colour_sl(3000, rp, col)
+    assert na == nb and np.array_equal(a, b)
+
+
 def _desc(**kw):
     d = dict(seed=1, n_temps=32, n_copies=1, betas=synth.beta_ladder(32), layout="bits", device=0)
     d.update(kw)

@@ -151,6 +151,60 @@ def test_greedy_colouring():
         assert all(c in lower for c in range(colour[i]))
 
 
+def _smallest_last_order_bruteforce(n, rp, col):
+    """Definition of the smallest-last removal order, written out with a linear scan:
+    repeatedly the live vertex of minimum remaining degree, ties to the lowest id."""
+    live = np.ones(n, bool)
+    deg = np.diff(rp).astype(np.int64)
+    order = []
+    for _ in range(n):
+        cand = np.where(live)[0]
+        i = int(cand[np.argmin(deg[cand])])  # argmin returns the first (lowest id) minimum
+        order.append(i)
+        live[i] = False
+        for j in col[rp[i]:rp[i + 1]]:
+            if live[j]:
+                deg[j] -= 1
+    return order
+
+
+@pytest.mark.parametrize("n,m,seed", [(60, 90, 1), (200, 199, 2), (300, 600, 3), (40, 0, 4)])
+def test_smallest_last_colouring_definition(n, m, seed):
+    u, v = synth.gnm(n, m, seed)
+    rp, col, _ = synth.edges_to_csr(n, u, v, np.ones(u.size, np.int32))
+    colour, ncol = oracle.greedy_colour_sl(n, rp, col)
+    order = _smallest_last_order_bruteforce(n, rp, col)
+    # greedy in reverse removal order: each vertex takes the smallest colour not used by a
+    # neighbour that comes before it in that order
+    pos = np.empty(n, np.int64)
+    pos[np.array(order[::-1])] = np.arange(n)
+    for i in range(n):
+        nb = col[rp[i]:rp[i + 1]]
+        before = set(colour[nb[pos[nb] < pos[i]]].tolist())
+        c = 0
+        while c in before:
+            c += 1
+        assert colour[i] == c
+    assert ncol == colour.max() + 1 if n else True
+    # at most degeneracy + 1 colours: degeneracy = max over the order of the remaining degree
+    live = np.ones(n, bool)
+    degen = 0
+    for i in order:
+        nb = col[rp[i]:rp[i + 1]]
+        degen = max(degen, int(live[nb].sum()))
+        live[i] = False
+    assert ncol <= degen + 1
+
+
+def test_smallest_last_colouring_c3_three_colours():
+    """G(1e4, 9999) (average degree 2) has degeneracy <= 2, so smallest-last needs <= 3."""
+    inst = synth.make_instance(synth.CONFIGS["c3"])
+    colour, ncol = oracle.greedy_colour_sl(inst["n"], inst["row_ptr"], inst["col"])
+    src = np.repeat(np.arange(inst["n"]), np.diff(inst["row_ptr"]))
+    assert np.all(colour[src] != colour[inst["col"]])
+    assert ncol == 3
+
+
 def test_grid_to_csr_matches_edge_list():
     Jr, Jd = synth.torus_pm1(6, 8, 9)
     rp, col, w, chk = oracle.grid_to_csr(6, 8, Jr, Jd)
