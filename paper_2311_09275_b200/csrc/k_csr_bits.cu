@@ -160,7 +160,6 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_csr_bits(const CsrBitsPa
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t Ucnt[32];
     __shared__ int32_t wcount[33];
-    __shared__ int32_t wprefix[33];
     __shared__ PtShared ps;
     const int n = p.n;
     const int nbw = (n + 31) / 32;
@@ -217,9 +216,9 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_csr_bits(const CsrBitsPa
             }
 #pragma unroll 1
             for (int c = 0; c < p.ncol; ++c) {
-                const int v0 = __ldg(p.class_off + c), v1 = __ldg(p.class_off + c + 1);
+                const int v1 = __ldg(p.class_off + c + 1);
                 int wq = 0;  // warp-uniform
-                for (int b = v0 + wbase; b < v1; b += nt) {
+                for (int b = __ldg(p.class_off + c) + wbase; b < v1; b += nt) {
                     const int v = b + lane;
                     const bool valid = v < v1;
                     uint32_t D = 0u, acc = 0u, io = 0u, own = 0u;
@@ -263,33 +262,34 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_csr_bits(const CsrBitsPa
                 if (lane == 0)
                     wcount[warp] = min(wq, wcap);
                 __syncthreads();
-                if (warp == 0) {
-                    const int vv = lane < nwarps ? wcount[lane] : 0;
-                    int incl = vv;
+                // every warp scans the per-warp queue counts itself (no extra barrier):
+                // lane w holds the exclusive prefix of region w
+                const int cnt_l = lane < nwarps ? wcount[lane] : 0;
+                int incl = cnt_l;
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                        if (lane >= o)
-                            incl += u;
-                    }
-                    wprefix[lane] = incl - vv;
-                    if (lane == 31)
-                        wprefix[32] = incl;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= o)
+                        incl += u;
                 }
-                __syncthreads();
+                const int excl = incl - cnt_l;
+                const int nq = __shfl_sync(0xFFFFFFFFu, incl, 31);
                 // stage 2: re-evaluate the queued vertices (neighbours are unchanged) and
                 // finish their comparisons from plane 8 on, all lanes busy
-                const int nq = wprefix[32];
-                for (int q = tid; q < nq; q += nt) {
-                    int lo = 0, hi = nwarps;
-                    while (hi - lo > 1) {
-                        const int mid = (lo + hi) >> 1;
-                        if (wprefix[mid] <= q)
-                            lo = mid;
-                        else
-                            hi = mid;
+                for (int qb = wbase; qb < nq; qb += nt) {
+                    const int q = qb + lane;
+                    int lo = 0;  // region: last w with excl_w <= q (binary search over lanes)
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1) {
+                        const int cand = lo + step;
+                        const int ev = __shfl_sync(0xFFFFFFFFu, excl, cand < 32 ? cand : 31);
+                        if (cand < nwarps && ev <= q)
+                            lo = cand;
                     }
-                    const int qs = lo * wcap + (q - wprefix[lo]);
+                    const int base_lo = __shfl_sync(0xFFFFFFFFu, excl, lo);
+                    if (q >= nq)
+                        continue;
+                    const int qs = lo * wcap + (q - base_lo);
                     const int v = (int)q_idx[qs];
                     uint32_t D = q_D[qs], acc = q_acc[qs];
                     const CsrSite st = csr_eval(S, p, v);
