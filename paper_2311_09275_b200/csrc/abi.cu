@@ -396,9 +396,9 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
     sum_abs /= 2;
     if (desc->layout == ISING_SPINS_BITS) {
         if (!desc->block_threads)
-            h->threads = kGridMaxThreads;
-        if (h->threads > kGridMaxThreads)
-            return fail(ISING_E_ARG, "BITS: block_threads must be <= " + std::to_string(kGridMaxThreads));
+            h->threads = kCsrMaxThreads;
+        if (h->threads > kCsrMaxThreads)
+            return fail(ISING_E_ARG, "BITS: block_threads must be <= " + std::to_string(kCsrMaxThreads));
         if (!wi || !pm1)
             return fail(ISING_E_UNSUPPORTED, "BITS layout needs integer weights in {-1,+1}");
         if (maxdeg > 15)

@@ -13,9 +13,11 @@ namespace ising {
 
 enum Kernel : int32_t { KER_GRID_BITS = 0, KER_CSR_BITS = 1, KER_CSR_I8 = 2 };
 
-// k_grid_bits CTA size limit: 24 warps leave 85 registers per thread (round keys held in
-// registers); CTA sizes are multiples of 4 warps so the four schedulers get equal work.
-constexpr int32_t kGridMaxThreads = 768;
+// CTA size limits (and launch bounds) of the bit-packed kernels, multiples of 4 warps so the
+// four schedulers get equal work.  Measured on C2/C4b/C3: the torus kernel
+// runs fastest with 16 warps and up to 128 registers per thread, the CSR kernel with 24.
+constexpr int32_t kGridMaxThreads = 512;
+constexpr int32_t kCsrMaxThreads = 768;
 
 // k_csr_i8_phase CTA size and the resident CTAs per SM its register budget is sized for
 constexpr int32_t kI8Threads = 256, kI8MinBlocks = 4;

@@ -155,7 +155,7 @@ size_t csr_bits_smem(int32_t n, int32_t qmax, int32_t words_per_copy)
            (size_t)csr_bits_qcap(n, qmax) * kCsrQItem;
 }
 
-__global__ void __launch_bounds__(kGridMaxThreads, 1) k_csr_bits(const CsrBitsParams p)
+__global__ void __launch_bounds__(kCsrMaxThreads, 1) k_csr_bits(const CsrBitsParams p)
 {
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t Ucnt[32];

@@ -112,7 +112,7 @@ def test_grid_bits_block_size_invariance():
     inst = grid(16, 12, 5)
     betas = synth.beta_ladder(32)
     outs = []
-    for thr in (32, 128, 768):
+    for thr in (32, 128, 512):
         eng = Engine(inst, 32, 4, betas, seed=7, layout="bits", block_threads=thr)
         run_pt(eng, 25, 5)
         outs.append((eng.energies(), [eng.spins(r) for r in range(0, 128, 13)]))

@@ -6,7 +6,7 @@ inst = dict(kind="grid", Lx=16, Ly=12, J_right=Jr, J_down=Jd, n=192)
 betas = synth.beta_ladder(32)
 o = oracle.Oracle(inst, 32, betas, 7, 0, 4, rng=oracle.RNG_PLANE).run(25, 5)
 for fused in (False, True):
-    for thr in (32, 64, 96, 128, 256, 768):
+    for thr in (32, 64, 96, 128, 256, 512):
         eng = Engine(inst, 32, 4, betas, seed=7, layout="bits", block_threads=thr)
         run_pt(eng, 25, 5, fused=fused)
         print("fused", fused, "thr", thr, np.array_equal(eng.energies(), o.Ei), flush=True)
