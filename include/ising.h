@@ -225,6 +225,28 @@ ISING_API int ising_get_walkers(ising_handle *h, int64_t *out);
 
 ISING_API int ising_info(const ising_handle *h, ising_info_t *out);
 
+/* ---- checkpoint / resume (SURVEY.md §5 "Checkpoint / resume"; SPEC S:326 seeds) -----
+ * Every random number is keyed by (seed, vertex, sweep t, group/slot, exchange e,
+ * cluster-move f), so the complete dynamic state of a handle is: the
+ * configurations, the energies, the walker ids, the counters t/e/f and the best-so-far
+ * records.  A handle created from the SAME instance, colouring, ladder, seed and shard
+ * (copy_begin/copy_end) that loads a checkpoint continues bit for bit as the saving
+ * handle would have (test_checkpoint_resume_parity).
+ *
+ * ising_state_size: bytes of this handle's checkpoint blob (host-only, no sync).
+ * ising_state_save: writes the blob into the caller's HOST buffer buf of `bytes` >=
+ *   the size (syncs).  Layout (little-endian, opaque to callers): a 128-byte header
+ *   (magic "ISNGCKP1", shape, counters, fingerprints of the instance/ladder/colouring),
+ *   then the state buffer in the handle's internal layout, E, walkers, per-copy best,
+ *   the best record and the best configuration.
+ * ising_state_load: restores a blob written by a compatible handle (syncs).
+ *   ISING_E_ARG: NULL buf or bytes too small; ISING_E_STATE: bad magic/version or a
+ *   header that does not match this handle (different n, m, weights sum, shard,
+ *   layout, RNG contract, seed, ladder or colouring) -- the handle is left unchanged. */
+ISING_API int ising_state_size(const ising_handle *h, int64_t *bytes);
+ISING_API int ising_state_save(ising_handle *h, void *buf, int64_t bytes);
+ISING_API int ising_state_load(ising_handle *h, const void *buf, int64_t bytes);
+
 /* Block until all work enqueued by the handle has finished. */
 ISING_API int ising_sync(ising_handle *h);
 

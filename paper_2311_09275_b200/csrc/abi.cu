@@ -56,6 +56,18 @@ uint64_t p64(double x)
 
 uint64_t metropolis_threshold(double beta, int64_t dE) { return p64(-(beta * (double)dE)); }
 
+// FNV-1a over raw bytes: checkpoint fingerprint of what a resumed handle must share.
+uint64_t fnv1a(uint64_t hsh, const void *p, size_t bytes)
+{
+    const unsigned char *b = (const unsigned char *)p;
+    for (size_t i = 0; i < bytes; ++i) {
+        hsh ^= b[i];
+        hsh *= 0x100000001b3ull;
+    }
+    return hsh;
+}
+constexpr uint64_t kFnvBasis = 0xcbf29ce484222325ull;
+
 uint64_t exchange_threshold(double beta_lo, double beta_hi, int64_t d)
 {
     return p64((beta_hi - beta_lo) * (double)d);
@@ -117,6 +129,7 @@ struct ising_handle {
     size_t sched_bytes = 0;
     std::vector<uint32_t> orig;  // internal -> original (CSR kernels)
     std::vector<uint32_t> o2i;
+    uint64_t fingerprint = 0;  // FNV-1a of the instance, colouring and ladder (checkpoints)
 
     template <class T>
     cudaError_t alloc(T **p, size_t count)
@@ -572,6 +585,11 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
     if (rc)
         return rc;
     CK(cudaStreamSynchronize(h->st));
+    h->fingerprint = fnv1a(kFnvBasis, row_ptr, ((size_t)n + 1) * 8);
+    h->fingerprint = fnv1a(h->fingerprint, col, (size_t)m2 * 4);
+    h->fingerprint = fnv1a(h->fingerprint, w, (size_t)m2 * 4);
+    h->fingerprint = fnv1a(h->fingerprint, h->orig.data(), h->orig.size() * 4);
+    h->fingerprint = fnv1a(h->fingerprint, h->betas.data(), h->betas.size() * 8);
     *out = h.release();
     return ISING_OK;
 }
@@ -929,6 +947,9 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
     if (rc)
         return rc;
     CK(cudaStreamSynchronize(h->st));
+    h->fingerprint = fnv1a(kFnvBasis, J_right, (size_t)n);
+    h->fingerprint = fnv1a(h->fingerprint, J_down, (size_t)n);
+    h->fingerprint = fnv1a(h->fingerprint, h->betas.data(), h->betas.size() * 8);
     *out = h.release();
     return ISING_OK;
 }
@@ -1364,6 +1385,124 @@ int ising_info(const ising_handle *h, ising_info_t *out)
     out->exchanges_done = h->e;
     out->W_int = h->W_int;
     out->W_f64 = h->W_f;
+    return ISING_OK;
+}
+
+// ---------------------------------------------------------------- checkpoint / resume
+}  // extern "C"
+namespace {
+
+struct CkptHeader {             // 128 bytes
+    char magic[8];              // "ISNGCKP1"
+    int32_t kernel, layout, wtype, rng;
+    int32_t n, K, C, c0, c1, pad0;
+    int64_t m, W_int;
+    double W_f;
+    uint64_t seed, fingerprint;
+    uint32_t t, e, f, pad1;
+    int64_t payload;            // bytes after the header
+    uint8_t reserved[16];
+};
+static_assert(sizeof(CkptHeader) == 128, "checkpoint header must stay 128 bytes");
+
+// (device pointer, bytes) of every dynamic state buffer, in blob order.
+std::vector<std::pair<void *, size_t>> ckpt_parts(const ising_handle *h)
+{
+    std::vector<std::pair<void *, size_t>> v;
+    if (h->layout == ISING_SPINS_BITS)
+        v.push_back({h->d_state[h->cur], (size_t)h->G * h->n * 4});
+    else
+        v.push_back({h->d_s8, (size_t)h->n * h->R});
+    v.push_back({h->d_E, (size_t)h->R * 8});
+    if (h->d_Ef)
+        v.push_back({h->d_Ef, (size_t)h->R * 8});
+    v.push_back({h->d_walker, (size_t)h->R * 8});
+    v.push_back({h->d_cbest, (size_t)h->C_local * 3 * 8});
+    v.push_back({h->d_best, sizeof(BestDev)});
+    v.push_back({h->d_best_spins, (size_t)h->n});
+    return v;
+}
+
+CkptHeader ckpt_header(const ising_handle *h)
+{
+    CkptHeader c{};
+    std::memcpy(c.magic, "ISNGCKP1", 8);
+    c.kernel = h->kernel; c.layout = h->layout; c.wtype = h->wtype; c.rng = h->rng;
+    c.n = h->n; c.K = h->K; c.C = h->C; c.c0 = h->c0; c.c1 = h->c1;
+    c.m = h->m; c.W_int = h->W_int; c.W_f = h->W_f;
+    c.seed = h->seed; c.fingerprint = h->fingerprint;
+    c.t = h->t; c.e = h->e; c.f = h->f;
+    for (const auto &p : ckpt_parts(h))
+        c.payload += (int64_t)p.second;
+    return c;
+}
+
+}  // namespace
+extern "C" {
+
+int ising_state_size(const ising_handle *h, int64_t *bytes)
+{
+    if (!h || !bytes)
+        return fail(ISING_E_ARG, "NULL argument");
+    *bytes = (int64_t)sizeof(CkptHeader) + ckpt_header(h).payload;
+    return ISING_OK;
+}
+
+int ising_state_save(ising_handle *h, void *buf, int64_t bytes)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    const CkptHeader c = ckpt_header(h);
+    if (!buf || bytes < (int64_t)sizeof(c) + c.payload)
+        return fail(ISING_E_ARG, "buffer is NULL or smaller than ising_state_size");
+    std::memcpy(buf, &c, sizeof(c));
+    char *dst = (char *)buf + sizeof(c);
+    for (const auto &p : ckpt_parts(h)) {
+        CK(cudaMemcpyAsync(dst, p.first, p.second, cudaMemcpyDeviceToHost, h->st));
+        dst += p.second;
+    }
+    CK(cudaStreamSynchronize(h->st));
+    return ISING_OK;
+}
+
+int ising_state_load(ising_handle *h, const void *buf, int64_t bytes)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (!buf || bytes < (int64_t)sizeof(CkptHeader))
+        return fail(ISING_E_ARG, "buffer is NULL or shorter than a checkpoint header");
+    CkptHeader in;
+    std::memcpy(&in, buf, sizeof(in));
+    if (std::memcmp(in.magic, "ISNGCKP1", 8) != 0)
+        return fail(ISING_E_STATE, "not a libising checkpoint (bad magic/version)");
+    const CkptHeader me = ckpt_header(h);
+    auto mismatch = [&](const char *what) {
+        return fail(ISING_E_STATE, std::string("checkpoint does not match this handle: ") + what);
+    };
+    if (in.kernel != me.kernel || in.layout != me.layout || in.wtype != me.wtype || in.rng != me.rng)
+        return mismatch("kernel/layout/weight type/RNG contract");
+    if (in.n != me.n || in.m != me.m || in.W_int != me.W_int || std::memcmp(&in.W_f, &me.W_f, 8) != 0)
+        return mismatch("instance shape or weights");
+    if (in.K != me.K || in.C != me.C || in.c0 != me.c0 || in.c1 != me.c1)
+        return mismatch("temperatures, copies or shard");
+    if (in.seed != me.seed)
+        return mismatch("seed");
+    if (in.fingerprint != me.fingerprint)
+        return mismatch("instance/colouring/ladder fingerprint");
+    if (in.payload != me.payload || bytes < (int64_t)sizeof(in) + in.payload)
+        return fail(ISING_E_ARG, "checkpoint is truncated");
+    CK(cudaStreamSynchronize(h->st));  // nothing in flight may still touch the state
+    const char *src = (const char *)buf + sizeof(in);
+    for (const auto &p : ckpt_parts(h)) {
+        CK(cudaMemcpyAsync(p.first, src, p.second, cudaMemcpyHostToDevice, h->st));
+        src += p.second;
+    }
+    CK(cudaStreamSynchronize(h->st));
+    h->t = in.t;
+    h->e = in.e;
+    h->f = in.f;
     return ISING_OK;
 }
 

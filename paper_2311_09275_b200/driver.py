@@ -119,6 +119,15 @@ class Engine:
     def sync(self):
         L.ising_sync(self.h)
 
+    # ---- checkpoint / resume (include/ising.h ising_state_*)
+    def save_state(self) -> bytes:
+        """Complete dynamic state (spins, energies, walkers, counters, best records)."""
+        return L.ising_state_save(self.h)
+
+    def load_state(self, blob: bytes):
+        """Resume from save_state of an Engine built from the same instance and arguments."""
+        L.ising_state_load(self.h, blob)
+
     def close(self):
         if getattr(self, "h", None):
             L.ising_destroy(self.h)

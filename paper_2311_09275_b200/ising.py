@@ -27,6 +27,7 @@ EXPORTED = [
     "ising_best", "ising_copy_best", "ising_get_spins", "ising_set_spins", "ising_get_walkers", "ising_info",
     "ising_sync", "ising_last_error", "ising_destroy", "ising_greedy_colour", "ising_greedy_colour_sl", "ising_threshold",
     "ising_version", "ising_debug_philox", "ising_debug_exp_bound",
+    "ising_state_size", "ising_state_save", "ising_state_load",
 ]
 
 
@@ -90,6 +91,9 @@ def lib(build_if_missing: bool = True):
         "ising_set_spins": ([vp, i64, vp], C.c_int),
         "ising_get_walkers": ([vp, vp], C.c_int),
         "ising_info": ([vp, C.POINTER(Info)], C.c_int),
+        "ising_state_size": ([vp, C.POINTER(i64)], C.c_int),
+        "ising_state_save": ([vp, vp, i64], C.c_int),
+        "ising_state_load": ([vp, vp, i64], C.c_int),
         "ising_sync": ([vp], C.c_int),
         "ising_last_error": ([], C.c_char_p),
         "ising_destroy": ([vp], None),
@@ -262,6 +266,25 @@ def ising_get_walkers(h) -> np.ndarray:
     out = np.zeros(info.n_slots, np.int64)
     _check(lib().ising_get_walkers(h, _ptr(out)))
     return out
+
+
+def ising_state_size(h) -> int:
+    n = C.c_int64(0)
+    _check(lib().ising_state_size(h, C.byref(n)))
+    return n.value
+
+
+def ising_state_save(h) -> bytes:
+    """Checkpoint blob of the handle's complete dynamic state (include/ising.h)."""
+    buf = np.zeros(ising_state_size(h), np.uint8)
+    _check(lib().ising_state_save(h, _ptr(buf), buf.size))
+    return buf.tobytes()
+
+
+def ising_state_load(h, blob: bytes):
+    """Restore a blob written by ising_state_save on a handle of the same instance/desc."""
+    buf = np.frombuffer(bytes(blob), np.uint8).copy()
+    _check(lib().ising_state_load(h, _ptr(buf), buf.size))
 
 
 def ising_sync(h):

@@ -419,3 +419,69 @@ def test_certify_cut_on_gpu_matches_definition():
     s = gset.bits_to_spins(bits)
     rep = gset.certify(500, u, v, w, s, claimed=gset.cut_of(u, v, w, s))
     assert rep["cut"] == rep["cut_gpu"] and rep["matches_claim"]
+
+
+def _state_tuple(eng):
+    n_copies = eng.R // eng.K
+    return (eng.energies(), eng.walkers(), [eng.spins(eng.slot0 + r) for r in range(eng.R)],
+            eng.best(spins=True), eng.copy_best(), (eng.info.n_slots, n_copies),
+            (L.ising_info(eng.h).sweeps_done, L.ising_info(eng.h).exchanges_done))
+
+
+def _assert_same_state(a, b):
+    for x, y in zip(a[0:2], b[0:2]):
+        assert np.array_equal(x, y)
+    assert all(np.array_equal(x, y) for x, y in zip(a[2], b[2]))
+    assert {k: a[3][k] for k in ("E", "slot", "sweep")} == {k: b[3][k] for k in ("E", "slot", "sweep")}
+    assert np.array_equal(a[3]["spins"], b[3]["spins"])
+    for x, y in zip(a[4], b[4]):
+        assert np.array_equal(x, y)
+    assert a[5:] == b[5:]
+
+
+@pytest.mark.parametrize("kind,layout,K,C,kex,icm", [
+    ("grid", "bits", 64, 2, 10, None),   # fused PT launch (ising_run)
+    ("grid", "bits", 64, 4, 5, 32),      # per-round exchange + Houdayer moves (counter f)
+    ("csr", "bits", 32, 2, 10, None),
+    ("csr", "i8", 16, 2, 10, None),
+])
+def test_checkpoint_resume_parity(kind, layout, K, C, kex, icm):
+    """SURVEY §5 checkpoint/resume: a fresh handle that loads a checkpoint continues bit for bit
+    as the saving handle, and both equal the oracle's uninterrupted run."""
+    inst = grid(16, 12, 31) if kind == "grid" else csr_pm1(400, 500, 32, signed=True)
+    betas = synth.beta_ladder(K)
+    kw = dict(seed=KEY, layout=layout)
+    a = Engine(inst, K, C, betas, **kw)
+    run_pt(a, 30, kex, icm_k_min=icm)
+    blob = a.save_state()
+    assert len(blob) == L.ising_state_size(a.h)
+    run_pt(a, 40, kex, icm_k_min=icm)
+    b = Engine(inst, K, C, betas, **kw)
+    b.load_state(blob)
+    run_pt(b, 40, kex, icm_k_min=icm)
+    sa, sb = _state_tuple(a), _state_tuple(b)
+    _assert_same_state(sa, sb)
+    if icm is None:
+        rng = oracle.RNG_PLANE if layout == "bits" else oracle.RNG_WORD
+        o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=rng).run(70, kex)
+        compare_copies(b, o)
+
+
+def test_checkpoint_rejects_other_handles():
+    inst = grid(8, 8, 33)
+    betas = synth.beta_ladder(32)
+    a = Engine(inst, 32, 2, betas, seed=KEY)
+    blob = a.save_state()
+    for other in (Engine(inst, 32, 2, betas, seed=KEY + 1),          # seed
+                  Engine(inst, 32, 2, betas * 1.01, seed=KEY),       # ladder
+                  Engine(grid(8, 8, 34), 32, 2, betas, seed=KEY),    # couplings
+                  Engine(inst, 32, 2, betas, seed=KEY, copy_begin=1)):  # shard
+        with pytest.raises(L.IsingError) as e:
+            other.load_state(blob)
+        assert e.value.code == L.ISING_E_STATE
+    with pytest.raises(L.IsingError) as e:
+        a.load_state(blob[:-1])
+    assert e.value.code == L.ISING_E_ARG
+    with pytest.raises(L.IsingError) as e:
+        a.load_state(b"x" * len(blob))
+    assert e.value.code == L.ISING_E_STATE
