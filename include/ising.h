@@ -288,10 +288,14 @@ ISING_API const char *ising_version(void);
 ISING_API int ising_debug_philox(int32_t device, const uint32_t *in, int32_t n, uint32_t *out_lib,
                        uint32_t *out_curand);
 
-/* Exhaustive check of the fast float decision used by the I8 kernel: the maximum over
- * every float x in [-64, 0] of |ex2.approx(x log2e + 32) / (cexp32(x) 2^32) - 1|.  The
- * kernel's 2^-12 margin is exact-decision-safe when this is < 2^-13.  Syncs. */
-ISING_API int ising_debug_exp_bound(int32_t device, float *worst_rel);
+/* Exhaustive check of the fast float decision used by the I8 kernels:
+ * for each of the n_beta values 2*beta (float, the kernels' per-replica slope) and EVERY
+ * float sh in [-80/(2 beta), 0], e = ex2.approx(RN(RN(2 beta log2e) sh + 16)) against the
+ * contract value c = cexp32(RN(2 beta sh)) 2^16 (§3.5).  worst_rel = max |e/c - 1| where
+ * c >= 1/2; max_small = max e where c < 1/2.  The kernels' 2^-16 margin decides exactly
+ * when worst_rel < 2^-17 and max_small < 1.  Syncs; ISING_E_ARG for NULL or bad betas. */
+ISING_API int ising_debug_exp_bound(int32_t device, const float *beta2, int32_t n_beta, float *worst_rel,
+                                    float *max_small);
 
 #ifdef __cplusplus
 }

@@ -1544,19 +1544,28 @@ int ising_debug_philox(int32_t device, const uint32_t *in, int32_t n, uint32_t *
     return ISING_OK;
 }
 
-int ising_debug_exp_bound(int32_t device, float *worst_rel)
+int ising_debug_exp_bound(int32_t device, const float *beta2, int32_t n_beta, float *worst_rel,
+                          float *max_small)
 {
-    if (!worst_rel)
-        return fail(ISING_E_ARG, "worst_rel is NULL");
+    if (!beta2 || n_beta < 1 || n_beta > 65535 || !worst_rel || !max_small)
+        return fail(ISING_E_ARG, "NULL argument or n_beta out of [1, 65535]");
+    for (int32_t i = 0; i < n_beta; ++i)
+        if (!(beta2[i] > 0.0f) || !std::isfinite(beta2[i]))
+            return fail(ISING_E_ARG, "beta2 entries must be finite and > 0");
     CK(cudaSetDevice(device));
     uint32_t *d = nullptr;
-    CK(cudaMalloc(&d, 4));
-    CK(cudaMemset(d, 0, 4));
-    CK(launch_debug_exp_bound(d, nullptr));
-    uint32_t bits = 0;
-    CK(cudaMemcpy(&bits, d, 4, cudaMemcpyDeviceToHost));
+    float *db = nullptr;
+    CK(cudaMalloc(&d, 8));
+    CK(cudaMalloc(&db, (size_t)n_beta * 4));
+    CK(cudaMemset(d, 0, 8));
+    CK(cudaMemcpy(db, beta2, (size_t)n_beta * 4, cudaMemcpyHostToDevice));
+    CK(launch_debug_exp_bound(db, n_beta, d, nullptr));
+    uint32_t bits[2] = {0, 0};
+    CK(cudaMemcpy(bits, d, 8, cudaMemcpyDeviceToHost));
     cudaFree(d);
-    std::memcpy(worst_rel, &bits, 4);
+    cudaFree(db);
+    std::memcpy(worst_rel, &bits[0], 4);
+    std::memcpy(max_small, &bits[1], 4);
     return ISING_OK;
 }
 

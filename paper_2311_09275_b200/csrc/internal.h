@@ -199,7 +199,7 @@ cudaError_t launch_extract_bits(const uint32_t *state, int32_t n, int32_t gl, in
                                 const uint32_t *perm_o2i, int8_t *out, cudaStream_t st);
 cudaError_t launch_insert_bits(uint32_t *state, int32_t n, int32_t gl, int32_t bit,
                                const uint32_t *perm_o2i, const int8_t *in, cudaStream_t st);
-cudaError_t launch_debug_exp_bound(uint32_t *out, cudaStream_t st);
+cudaError_t launch_debug_exp_bound(const float *beta2, int32_t n_beta, uint32_t *out, cudaStream_t st);
 cudaError_t launch_debug_philox(const uint32_t *in, int32_t n, uint32_t *out_lib,
                                 uint32_t *out_curand, cudaStream_t st);
 

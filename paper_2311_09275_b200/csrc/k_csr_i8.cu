@@ -57,19 +57,26 @@ __device__ __forceinline__ uint64_t thr_x(float x)
     return __float2ull_rz(v);
 }
 
-// e = ex2.approx(fma(x, log2 e, 16)) estimates cexp32(x) 2^16 = T / 2^48 with relative
-// error below 2^-17 (measured 3.6e-6 = 2^-18.1, checked exhaustively over every float x in
-// [-64, 0] by ising_debug_exp_bound, which evaluates this exact expression).  With the
-// 2^-16 margin (> twice the error bound):
+// The fast decision estimates T / 2^48 = cexp32(x) 2^16 (x = -(beta dE) = (2 beta) s_i h) by
+//   e = ex2.approx(RN(bl * sh + 16)),   bl = RN((2 beta) * log2 e),   sh = s_i h,
+// one FFMA and one MUFU per attempt (bl is computed once per thread).  Relative to the
+// contract value c = cexp32(x) 2^16 the error has four sources: bl vs log2e * x / sh
+// (two roundings, <= 2^-23 relative in the exponent argument), the FFMA rounding of the
+// argument, ex2.approx, and cexp32 vs exp.  Wherever c >= 1/2 (x >= -11.8, argument
+// <= 17 in magnitude) they sum to < 2^-18.5; ising_debug_exp_bound checks it for every
+// float sh and the ladder's betas, together with e < 1 wherever c < 1/2.  With the 2^-16
+// margin (> twice the error bound):
 //   2^23 + hi16 <= RN(e (1 - 2^-16) + 2^23 - 2)  =>  hi16 + 1 <= T / 2^48  =>  accept
 //   2^23 + hi16 >= RN(e (1 + 2^-16) + 2^23 + 1)  =>  hi16 > T / 2^48      =>  reject
-// (the RN of a value near 2^23 is within 1/2, covered by the -2 / +1 slack)
-// and anything else is decided exactly.  For x < -64 (T = 0) e < 2^-76,
-// so only hi16 = 0 stays undecided and the exact path rejects it.
-__device__ __forceinline__ float exp_est16(float x)
+// (the RN of a value near 2^23 is within 1/2, covered by the -2 / +1 slack; where c < 1/2
+// no hi16 is accepted and hi16 >= 2 is rejected, both correct for T < 2^47)
+// and anything else is decided exactly.
+constexpr float kLog2e = 0x1.715476p+0f;
+
+__device__ __forceinline__ float exp_est16(float bl, float sh)
 {
     float e;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmaf_rn(x, 0x1.715476p+0f, 16.0f)));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmaf_rn(bl, sh, 16.0f)));
     return e;
 }
 
@@ -94,26 +101,33 @@ __device__ __forceinline__ bool exact_less(uint32_t hi16, uint64_t T, uint32_t i
 
 }  // namespace
 
-// Exhaustive check of the fast-decision bound: max over all float x in [-64, 0] of
-// |exp_est16(x) / (cexp32(x) 2^16) - 1|, as float bits in *out (atomicMax).
-__global__ void k_debug_exp_bound(uint32_t *out)
+// Exhaustive check of the fast-decision bound for one 2 beta per blockIdx.y: over every float
+// sh in [-80 / (2 beta), 0] (beyond it e < 2^-99), out[0] = max |e / c - 1| where c >= 1/2 and
+// out[1] = max e where c < 1/2, with e = exp_est16(RN(2 beta log2e), sh) and c = cexp32(RN(2 beta
+// sh)) 2^16 -- the exact expressions of the kernels (float bits, atomicMax).
+__global__ void k_debug_exp_bound(const float *beta2, uint32_t *out)
 {
-    const uint32_t lo = 0x80000000u, hi = 0xC2800000u;  // -0 .. -64
-    float worst = 0.f;
-    for (uint64_t b = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= hi;
-         b += (uint64_t)gridDim.x * blockDim.x) {
-        const float x = __uint_as_float((uint32_t)b);
-        const float e = exp_est16(x);
-        const float c = __fmul_rn(cexp32(x), 0x1p16f);
-        const float rel = fabsf(e / c - 1.0f);
-        worst = fmaxf(worst, rel);
+    const float b2 = beta2[blockIdx.y];
+    const float bl = __fmul_rn(b2, kLog2e);
+    const uint32_t hi = __float_as_uint(-80.0f / b2) + 1u;  // float bits of -0 .. -(80/b2)
+    float worst = 0.f, small = 0.f;
+    for (uint64_t u = 0x80000000u + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u <= hi;
+         u += (uint64_t)gridDim.x * blockDim.x) {
+        const float sh = __uint_as_float((uint32_t)u);
+        const float e = exp_est16(bl, sh);
+        const float c = __fmul_rn(cexp32(__fmul_rn(b2, sh)), 0x1p16f);
+        if (c >= 0.5f)
+            worst = fmaxf(worst, fabsf(e / c - 1.0f));
+        else
+            small = fmaxf(small, e);
     }
     atomicMax(out, __float_as_uint(worst));
+    atomicMax(out + 1, __float_as_uint(small));
 }
 
-cudaError_t launch_debug_exp_bound(uint32_t *out, cudaStream_t st)
+cudaError_t launch_debug_exp_bound(const float *beta2, int32_t n_beta, uint32_t *out, cudaStream_t st)
 {
-    k_debug_exp_bound<<<148 * 8, 256, 0, st>>>(out);
+    k_debug_exp_bound<<<dim3(148 * 8, (unsigned)n_beta), 256, 0, st>>>(beta2, out);
     return cudaGetLastError();
 }
 
@@ -142,6 +156,15 @@ __device__ __forceinline__ float hi16_f(uint32_t w)
     uint32_t r;
     // bytes (lo..hi): hi16 low byte, hi16 high byte, 0x00, 0x4B  (0x4B000000 = 2^23)
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(0x4B000000u), "n"((b & 1) ? 0x7432 : 0x7410));
+    return __uint_as_float(r);
+}
+
+// same with the 0x4B000000 source in a register (selector immediate)
+template <int b>
+__device__ __forceinline__ float hi16_fr(uint32_t w, uint32_t c4b)
+{
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(c4b), "n"((b & 1) ? 0x7432 : 0x7410));
     return __uint_as_float(r);
 }
 
@@ -191,13 +214,13 @@ __device__ __forceinline__ void float_decide(const CsrI8Params &p, int32_t v, co
                 }
             }
             const float4 bq = __ldg(bph + half);  // 2 beta_k, L1-resident
-            const float b2[4] = {bq.x, bq.y, bq.z, bq.w};
+            const float b2[4] = {__fmul_rn(bq.x, kLog2e), __fmul_rn(bq.y, kLog2e), __fmul_rn(bq.z, kLog2e),
+                                 __fmul_rn(bq.w, kLog2e)};  // RN(2 beta log2e)
             uint32_t fm = 0u;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                // x = -(beta dE) = (2 beta)(s h) exactly; s h >= 0 flips
-                const float xv = __fmul_rn(b2[b], sh[b]);
-                const float e = exp_est16(xv);
+                // s h >= 0 flips; else estimate cexp32((2 beta)(s h)) 2^16
+                const float e = exp_est16(b2[b], sh[b]);
                 const uint32_t hword = hw[2 * half + (b >> 1)];
                 const float hf = (b & 1) ? hi16_f<1>(hword) : hi16_f<0>(hword);  // 2^23 + hi16
                 const bool acc = sh[b] >= 0.0f || hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f);
@@ -231,12 +254,13 @@ __device__ __forceinline__ void float_decide(const CsrI8Params &p, int32_t v, co
                                                              ((word << (24 - 8 * (b & 3))) & 0x80000000u)));
                     }
                 }
-                const float xv = __fmul_rn(__ldg(p.betaf + 8u * o + (uint32_t)b), shb);
+                const float b2v = __ldg(p.betaf + 8u * o + (uint32_t)b);
+                const float xv = __fmul_rn(b2v, shb);  // x = -(beta dE), the contract's product
                 const uint32_t hword = (b >> 1) == 0 ? hw[0] : (b >> 1) == 1 ? hw[1] : (b >> 1) == 2 ? hw[2] : hw[3];
                 const uint32_t hb = (b & 1) ? (hword >> 16) : (hword & 0xFFFFu);
                 if (shb >= 0.0f)
                     continue;
-                const float e = exp_est16(xv);
+                const float e = exp_est16(__fmul_rn(b2v, kLog2e), shb);
                 const float hf = __uint_as_float(0x4B000000u | hb);
                 if (hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f) || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f))
                     continue;  // decided by the fast path (same expressions)
@@ -366,10 +390,176 @@ __global__ void __launch_bounds__(kI8Threads, FLOAT ? kI8MinBlocks : 3) k_csr_i8
     }
 }
 
-// Float weights + padded neighbour table, two-deep software pipeline: while vertex k is
-// decided, the spin rows of vertex k+1 are already in flight (issued at the top of iteration
-// k) and the table row of vertex k+2 is being loaded, so each warp keeps two vertices' gathers
-// outstanding.
+// Float weights + padded neighbour table of fixed width DEG (the graph's maximum degree,
+// <= 4): software pipeline, unrolled by two so no register is copied between iterations
+// (DESIGN.md §5.4).  Step k decides vertex k from rows issued in step k-1; at its top it
+// issues the spin rows of vertex k+1 (columns loaded in step k-1), the weights / original
+// id of vertex k+1 and the columns of vertex k+2.  Philox rounds 0-1 are half hoisted (the
+// counter words t, g0 and the stream are loop-invariant).
+template <int DEG>
+struct I8Rows {
+    uint2 own;
+    uint2 nb[DEG];
+};
+
+struct I8Meta {
+    int4 w;       // weights (float bits), pads 0
+    uint32_t io;  // original id (Philox counter word 0)
+};
+
+// Philox4x32-10(io, t, g0, WORD_HI<<24) with the loop-invariant parts of rounds 0 and 1
+// precomputed: per call 2 + 18 IMAD.WIDE-equivalents fewer than the plain form.
+struct PhiloxHoist {
+    uint32_t c3k1;  // (WORD_HI << 24) ^ k1
+    uint32_t bk2;   // lo(M1 g0) ^ k2           (round 1, word 0)
+    uint32_t hak3;  // hi(M0 A) ^ k3, A = hi(M1 g0) ^ t ^ k0 (round 1, word 2)
+    uint32_t la;    // lo(M0 A)                 (round 1, word 3)
+};
+
+__device__ __forceinline__ PhiloxHoist philox_hoist(uint32_t t, uint32_t g0, const RoundKeys &rk)
+{
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * g0;
+    const uint32_t A = (uint32_t)(p1 >> 32) ^ t ^ rk.k[0];
+    const uint32_t B = (uint32_t)p1;
+    const uint64_t pa = (uint64_t)0xD2511F53u * A;
+    PhiloxHoist h;
+    h.c3k1 = ((uint32_t)ST_WORD_HI << 24) ^ rk.k[1];
+    h.bk2 = B ^ rk.k[2];
+    h.hak3 = (uint32_t)(pa >> 32) ^ rk.k[3];
+    h.la = (uint32_t)pa;
+    return h;
+}
+
+__device__ __forceinline__ uint4 philox_hoisted(uint32_t io, const PhiloxHoist &hh, const RoundKeys &rk)
+{
+    // round 0: c0 = A, c1 = B, c2 = hi(M0 io) ^ c3 ^ k1, c3 = lo(M0 io)
+    const uint64_t p0 = (uint64_t)0xD2511F53u * io;
+    const uint32_t c2r0 = (uint32_t)(p0 >> 32) ^ hh.c3k1;
+    // round 1: p0' = M0 A (hoisted), p1' = M1 c2r0
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2r0;
+    uint32_t c0 = (uint32_t)(p1 >> 32) ^ hh.bk2;
+    uint32_t c1 = (uint32_t)p1;
+    uint32_t c2 = hh.hak3 ^ (uint32_t)p0;
+    uint32_t c3 = hh.la;
+#pragma unroll
+    for (int r = 2; r < 10; ++r) {
+        const uint64_t q0 = (uint64_t)0xD2511F53u * c0;
+        const uint64_t q1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t n0 = (uint32_t)(q1 >> 32) ^ c1 ^ rk.k[2 * r];
+        const uint32_t n2 = (uint32_t)(q0 >> 32) ^ c3 ^ rk.k[2 * r + 1];
+        c1 = (uint32_t)q1;
+        c3 = (uint32_t)q0;
+        c0 = n0;
+        c2 = n2;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+// sign-adjusted weight of neighbour term u for byte b of x = own ^ nb_u: w_u if s_i = s_j
+template <int b>
+__device__ __forceinline__ float term(uint32_t x, uint32_t w)
+{
+    return __uint_as_float(w ^ ((b == 3 ? x : (x << (24 - 8 * b))) & 0x80000000u));
+}
+
+// field s_i h of the 4 replicas of one spin word (left fold in row order; the leading
+// 0 + t_0 of the contract fold is t_0 up to the sign of a zero, which no decision sees)
+template <int DEG, int HALF>
+__device__ __forceinline__ void field4(const uint2 (&x)[DEG], const int4 &wq, float (&sh)[4])
+{
+    const uint32_t wv[4] = {(uint32_t)wq.x, (uint32_t)wq.y, (uint32_t)wq.z, (uint32_t)wq.w};
+    const uint32_t x0 = HALF ? x[0].y : x[0].x;
+    sh[0] = term<0>(x0, wv[0]);
+    sh[1] = term<1>(x0, wv[0]);
+    sh[2] = term<2>(x0, wv[0]);
+    sh[3] = term<3>(x0, wv[0]);
+#pragma unroll
+    for (int u = 1; u < DEG; ++u) {
+        const uint32_t xu = HALF ? x[u].y : x[u].x;
+        sh[0] = __fadd_rn(sh[0], term<0>(xu, wv[u]));
+        sh[1] = __fadd_rn(sh[1], term<1>(xu, wv[u]));
+        sh[2] = __fadd_rn(sh[2], term<2>(xu, wv[u]));
+        sh[3] = __fadd_rn(sh[3], term<3>(xu, wv[u]));
+    }
+}
+
+// row addresses as one IMAD.WIDE.U32 each (64-bit product of the 32-bit id and row bytes)
+template <int DEG>
+__device__ __forceinline__ void pipe_issue(I8Rows<DEG> &r, const char *tbb, uint32_t rwb, uint32_t v,
+                                           const int4 &c)
+{
+    r.own = *reinterpret_cast<const uint2 *>(tbb + (uint64_t)v * rwb);
+    const int32_t cs[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int u = 0; u < DEG; ++u)
+        r.nb[u] = __ldg(reinterpret_cast<const uint2 *>(tbb + (uint64_t)(uint32_t)cs[u] * rwb));
+}
+
+// Decide the 8 attempts of vertex v (internal id) and write its row.
+template <int DEG>
+__device__ __forceinline__ void pipe_decide(const CsrI8Params &p, const I8Rows<DEG> &r, const I8Meta &m,
+                                            uint32_t v, char *tbb, uint32_t rwb, const float (&bl)[8],
+                                            const PhiloxHoist &ph, uint32_t g0, uint32_t o, uint32_t c4b)
+{
+    uint2 x[DEG];
+#pragma unroll
+    for (int u = 0; u < DEG; ++u)
+        x[u] = make_uint2(r.own.x ^ r.nb[u].x, r.own.y ^ r.nb[u].y);
+    const uint4 h = philox_hoisted(m.io, ph, p.rk);
+    const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+    uint32_t fm[2];
+    bool und = false;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        float sh[4];
+        if (half)
+            field4<DEG, 1>(x, m.w, sh);
+        else
+            field4<DEG, 0>(x, m.w, sh);
+        uint32_t f = 0u;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const float e = exp_est16(bl[4 * half + b], sh[b]);
+            const uint32_t hword = hw[2 * half + (b >> 1)];
+            const float hf = (b & 1) ? hi16_fr<1>(hword, c4b) : hi16_fr<0>(hword, c4b);  // 2^23 + hi16
+            const bool acc = sh[b] >= 0.0f || hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f);
+            const bool dec = acc || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f);
+            f |= acc ? (0xFEu << (8 * b)) : 0u;
+            und |= !dec;
+        }
+        fm[half] = f;
+    }
+    if (__builtin_expect(und, 0)) {  // rare: recompute the field per replica, exact threshold
+#pragma unroll 1
+        for (int b = 0; b < 8; ++b) {
+            float shb;
+            {
+                float s4[4];
+                if (b < 4)
+                    field4<DEG, 0>(x, m.w, s4);
+                else
+                    field4<DEG, 1>(x, m.w, s4);
+                const int bb = b & 3;
+                shb = bb == 0 ? s4[0] : bb == 1 ? s4[1] : bb == 2 ? s4[2] : s4[3];
+            }
+            if (shb >= 0.0f)
+                continue;
+            const uint32_t hword = (b >> 1) == 0 ? hw[0] : (b >> 1) == 1 ? hw[1] : (b >> 1) == 2 ? hw[2] : hw[3];
+            const uint32_t hb = (b & 1) ? (hword >> 16) : (hword & 0xFFFFu);
+            const float b2v = __ldg(p.betaf + 8u * o + (uint32_t)b);
+            const float e = exp_est16(__fmul_rn(b2v, kLog2e), shb);
+            const float hf = __uint_as_float(0x4B000000u | hb);
+            if (hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f) || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f))
+                continue;  // decided by the fast path (same expressions)
+            if (exact_less(hb, thr_x(__fmul_rn(b2v, shb)), m.io, p.t, 8u * g0 + (uint32_t)b, p.rk))
+                fm[b >> 2] |= 0xFEu << (8 * (b & 3));
+        }
+    }
+    // +1 (0x01) <-> -1 (0xFF): xor the byte with 0xFE
+    *reinterpret_cast<uint2 *>(tbb + (uint64_t)v * rwb) = make_uint2(r.own.x ^ fm[0], r.own.y ^ fm[1]);
+}
+
+template <int DEG>
 __global__ void __launch_bounds__(kI8Threads, kI8PipeMinBlocks) k_csr_i8_pipe(const CsrI8Params p)
 {
     const uint32_t rw = (uint32_t)p.R >> 2;
@@ -379,72 +569,67 @@ __global__ void __launch_bounds__(kI8Threads, kI8PipeMinBlocks) k_csr_i8_pipe(co
         return;
     const uint32_t nv = (uint32_t)(p.v_end - p.v_begin);
     const uint32_t vstride = gridDim.x * blockDim.y;
-    uint32_t *tb = reinterpret_cast<uint32_t *>(p.s) + 2u * o;
-    const char *tbb = reinterpret_cast<const char *>(tb);
-    const uint32_t rwb = 4u * rw;
-    const uint32_t g0 = (uint32_t)(p.slot0 >> 3) + o;
-    const float4 *bp = reinterpret_cast<const float4 *>(p.betaf) + 2u * o;
-    const int deg = p.ell_deg;
-    const int4 *ec = reinterpret_cast<const int4 *>(p.ell_col) + p.v_begin;
-    const int4 *ew = reinterpret_cast<const int4 *>(p.ell_w) + p.v_begin;
-    const uint32_t *eo = p.orig + p.v_begin;
     uint32_t vv = blockIdx.x * blockDim.y + threadIdx.y;
     if (vv >= nv)
         return;
-    auto rows = [&](uint32_t vq, const int4 &c, uint2 &own, uint2 (&nb)[4]) {
-        own = *reinterpret_cast<const uint2 *>(tbb + (p.v_begin + vq) * rwb);
-        const int32_t cs[4] = {c.x, c.y, c.z, c.w};
+    char *tbb = reinterpret_cast<char *>(reinterpret_cast<uint32_t *>(p.s) + 2u * o);
+    const uint32_t rwb = 4u * rw;
+    const uint32_t g0 = (uint32_t)(p.slot0 >> 3) + o;
+    float bl[8];
+    {
+        const float4 *bp = reinterpret_cast<const float4 *>(p.betaf) + 2u * o;  // 2 beta_k
+        const float4 a = __ldg(bp), b = __ldg(bp + 1);
+        const float b2[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (u < deg)
-                nb[u] = __ldg(reinterpret_cast<const uint2 *>(tbb + (uint32_t)cs[u] * rwb));
-    };
-    // prologue: table rows of vertices 0 and 1, spin rows of vertex 0
-    int4 c1 = __ldg(ec + vv), w1 = __ldg(ew + vv);
-    uint32_t io1 = __ldg(eo + vv);
-    uint2 own1, nb1[4];
-    rows(vv, c1, own1, nb1);
-    uint32_t vq2 = vv + vstride;
-    int4 c2 = make_int4(0, 0, 0, 0), w2 = make_int4(0, 0, 0, 0);
-    uint32_t io2 = 0;
-    if (vq2 < nv) {
-        c2 = __ldg(ec + vq2);
-        w2 = __ldg(ew + vq2);
-        io2 = __ldg(eo + vq2);
+        for (int i = 0; i < 8; ++i)
+            bl[i] = __fmul_rn(b2[i], kLog2e);
     }
-    for (; vv < nv; vv += vstride) {
-        // current vertex: rows and meta from the previous iteration
-        const uint2 own = own1;
-        uint2 nb[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            nb[u] = nb1[u];
-        const int4 wq = w1;
-        const uint32_t io = io1;
-        // next vertex: issue its spin-row gathers now; the one after: its table row
-        const uint32_t vn = vv + vstride;
-        if (vn < nv) {
-            rows(vn, c2, own1, nb1);
-            w1 = w2;
-            io1 = io2;
-            const uint32_t vn2 = vn + vstride;
-            if (vn2 < nv) {
-                c2 = __ldg(ec + vn2);
-                w2 = __ldg(ew + vn2);
-                io2 = __ldg(eo + vn2);
-            }
+    const PhiloxHoist ph = philox_hoist(p.t, g0, p.rk);
+    // 0x4B000000 (= 2^23) in a register the compiler cannot fold (rwb < 2^31), so the PRMT
+    // building 2^23 + hi16 takes its selector as an immediate
+    const uint32_t c4b = 0x4B000000u | (rwb >> 31);
+    const uint32_t vb = (uint32_t)p.v_begin;
+    const int4 *ec = reinterpret_cast<const int4 *>(p.ell_col) + vb;
+    const int4 *ew = reinterpret_cast<const int4 *>(p.ell_w) + vb;
+    const uint32_t *eo = p.orig + vb;
+    auto meta = [&](uint32_t q) {
+        I8Meta m;
+        m.w = __ldg(ew + q);
+        m.io = __ldg(eo + q);
+        return m;
+    };
+    // prologue: rows + meta of the first vertex, columns of the second
+    I8Rows<DEG> rA, rB;
+    I8Meta mA = meta(vv), mB;
+    pipe_issue<DEG>(rA, tbb, rwb, vb + vv, __ldg(ec + vv));
+    int4 cn = make_int4(0, 0, 0, 0);
+    if (vv + vstride < nv)
+        cn = __ldg(ec + vv + vstride);
+    for (;;) {
+        // step with A current, B next
+        uint32_t v1 = vv + vstride;
+        if (v1 < nv) {
+            pipe_issue<DEG>(rB, tbb, rwb, vb + v1, cn);
+            mB = meta(v1);
+            if (v1 + vstride < nv)
+                cn = __ldg(ec + v1 + vstride);
         }
-        uint2 x[4];
-        const uint32_t wv[4] = {(uint32_t)wq.x, (uint32_t)wq.y, (uint32_t)wq.z, (uint32_t)wq.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            x[u] = u < deg ? make_uint2(own.x ^ nb[u].x, own.y ^ nb[u].y) : make_uint2(0u, 0u);
-        const uint4 h = philox_w(io, p.t, g0, ST_WORD_HI << 24, p.rk);
-        const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
-        uint32_t fm0 = 0u, fm1 = 0u;
-        const int32_t v = p.v_begin + (int32_t)vv;
-        float_decide<true>(p, v, own, x, wv, tb, rw, io, g0, o, bp, hw, fm0, fm1);
-        *reinterpret_cast<uint2 *>(tb + (size_t)(uint32_t)v * rw) = make_uint2(own.x ^ fm0, own.y ^ fm1);
+        pipe_decide<DEG>(p, rA, mA, vb + vv, tbb, rwb, bl, ph, g0, o, c4b);
+        vv = v1;
+        if (vv >= nv)
+            break;
+        // step with B current, A next
+        v1 = vv + vstride;
+        if (v1 < nv) {
+            pipe_issue<DEG>(rA, tbb, rwb, vb + v1, cn);
+            mA = meta(v1);
+            if (v1 + vstride < nv)
+                cn = __ldg(ec + v1 + vstride);
+        }
+        pipe_decide<DEG>(p, rB, mB, vb + vv, tbb, rwb, bl, ph, g0, o, c4b);
+        vv = v1;
+        if (vv >= nv)
+            break;
     }
 }
 
@@ -469,7 +654,14 @@ cudaError_t launch_csr_i8_phase(const CsrI8Params &p, int32_t threads, cudaStrea
     const dim3 block((unsigned)bx, (unsigned)by);
     const bool ell = p.ell_col != nullptr;
     if (p.wf) {
-        if (ell && kI8Pipe) k_csr_i8_pipe<<<grid, block, 0, st>>>(p);
+        if (ell && kI8Pipe) {
+            switch (p.ell_deg) {
+            case 1: k_csr_i8_pipe<1><<<grid, block, 0, st>>>(p); break;
+            case 2: k_csr_i8_pipe<2><<<grid, block, 0, st>>>(p); break;
+            case 3: k_csr_i8_pipe<3><<<grid, block, 0, st>>>(p); break;
+            default: k_csr_i8_pipe<4><<<grid, block, 0, st>>>(p); break;
+            }
+        }
         else if (ell) k_csr_i8_phase<true, true><<<grid, block, 0, st>>>(p);
         else k_csr_i8_phase<true, false><<<grid, block, 0, st>>>(p);
     } else {

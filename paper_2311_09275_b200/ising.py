@@ -102,7 +102,7 @@ def lib(build_if_missing: bool = True):
         "ising_threshold": ([C.c_double, i64], C.c_uint64),
         "ising_version": ([], C.c_char_p),
         "ising_debug_philox": ([i32, vp, i32, vp, vp], C.c_int),
-        "ising_debug_exp_bound": ([i32, C.POINTER(C.c_float)], C.c_int),
+        "ising_debug_exp_bound": ([i32, vp, i32, C.POINTER(C.c_float), C.POINTER(C.c_float)], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -338,7 +338,10 @@ def ising_debug_philox(tuples, device: int = 0):
     return o1, o2
 
 
-def ising_debug_exp_bound(device: int = 0) -> float:
-    out = C.c_float()
-    _check(lib().ising_debug_exp_bound(device, C.byref(out)))
-    return out.value
+def ising_debug_exp_bound(beta2, device: int = 0):
+    """(worst relative error where c >= 1/2, max estimate where c < 1/2) of the I8 kernels'
+    fast float decision over every float field value, for each slope 2*beta in beta2."""
+    b = np.ascontiguousarray(beta2, np.float32)
+    worst, small = C.c_float(), C.c_float()
+    _check(lib().ising_debug_exp_bound(device, _ptr(b), b.size, C.byref(worst), C.byref(small)))
+    return worst.value, small.value

@@ -232,12 +232,15 @@ def _regular_inst(n, seed):
 
 
 def test_exp_bracket_bound():
-    """The I8 kernel decides float-weight attempts from the 16-bit hi word with a 2^-16
-    relative margin around an ex2.approx estimate; exact-decision safety needs the estimate
-    within half the margin of the contract exponential for EVERY float x in [-64, 0]
-    (exhaustive; measured 3.6e-6 = 2^-18.1 on a B200)."""
-    worst = L.ising_debug_exp_bound()
+    """The I8 kernels decide float-weight attempts from the 16-bit hi word with a 2^-16
+    relative margin around the estimate ex2.approx(RN(2 beta log2e) sh + 16); exact-decision
+    safety needs it within half the margin of the contract exponential wherever c >= 1/2 and
+    below 1 elsewhere, for EVERY float field value sh (exhaustive) and every ladder used by
+    the float tests and the C5 bench."""
+    b2 = np.unique(np.concatenate([2.0 * synth.beta_ladder(k).astype(np.float32) for k in (8, 16, 256)]))
+    worst, small = L.ising_debug_exp_bound(b2.astype(np.float32))
     assert worst < 2.0 ** -17, worst
+    assert small < 1.0, small
 
 
 def test_float_int8_parity_small():
