@@ -23,7 +23,10 @@ constexpr int32_t kCsrMaxThreads = 768;
 constexpr int32_t kI8Threads = 256, kI8MinBlocks = 4;
 // float + padded-table graphs: two-deep pipelined kernel and its resident CTAs per SM
 constexpr bool kI8Pipe = true;
-constexpr int32_t kI8PipeMinBlocks = 3;
+constexpr int32_t kI8PipeMinBlocks = 4;
+// float + padded-table graphs with R % 256 == 0: cp.async ring kernel with this many vertices
+// in flight per warp (0 = use the register pipeline)
+constexpr int32_t kI8Ring = 4;
 
 // Rows of a colour class per pass of the 2-D thread mapping: threads / (Lx/2), rounded
 // down to an even number when >= 2 so that the parity (c + y) & 1 of a thread's sites is

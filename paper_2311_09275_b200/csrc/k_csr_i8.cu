@@ -551,8 +551,12 @@ __device__ __forceinline__ void pipe_decide(const CsrI8Params &p, const I8Rows<D
             const float hf = __uint_as_float(0x4B000000u | hb);
             if (hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f) || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f))
                 continue;  // decided by the fast path (same expressions)
-            if (exact_less(hb, thr_x(__fmul_rn(b2v, shb)), m.io, p.t, 8u * g0 + (uint32_t)b, p.rk))
-                fm[b >> 2] |= 0xFEu << (8 * (b & 3));
+            if (exact_less(hb, thr_x(__fmul_rn(b2v, shb)), m.io, p.t, 8u * g0 + (uint32_t)b, p.rk)) {
+                if (b < 4)  // scalar updates: a dynamically indexed fm[] would live in local memory
+                    fm[0] |= 0xFEu << (8 * (b & 3));
+                else
+                    fm[1] |= 0xFEu << (8 * (b & 3));
+            }
         }
     }
     // +1 (0x01) <-> -1 (0xFF): xor the byte with 0xFE
@@ -633,6 +637,193 @@ __global__ void __launch_bounds__(kI8Threads, kI8PipeMinBlocks) k_csr_i8_pipe(co
     }
 }
 
+// ---------------------------------------------------------------- cp.async ring variant
+// Float weights, padded table, R a multiple of 256 (every warp = 32 threads x 8 replicas of
+// one vertex): each warp sweeps a CONTIGUOUS chunk of the colour class and keeps S vertices'
+// spin rows in flight through a per-warp shared-memory ring filled by cp.async (LDGSTS), so
+// the memory-level parallelism no longer costs registers (the register pipeline above keeps
+// one vertex in flight and stalls on load latency).  The table rows (columns,
+// weights, original ids) of 32 consecutive vertices arrive by one cp.async per lane into a
+// double buffer, 32 vertices ahead.  Each lane reads back only the row bytes it copied
+// itself; table entries are read by every lane after a __syncwarp.
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr uint32_t kRingMetaBuf = 32 * 16 + 32 * 16 + 32 * 4;  // columns, weights, ids of 32 vertices
+
+template <int DEG, int S>
+__host__ __device__ constexpr uint32_t ring_warp_bytes()
+{
+    return (uint32_t)S * (DEG + 1) * 256u + 2u * kRingMetaBuf;
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t a)
+{
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int4 lds128(uint32_t a)
+{
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+template <int DEG, int S>
+__global__ void __launch_bounds__(256, 4) k_csr_i8_ring(const CsrI8Params p, uint32_t nslice, uint32_t chunk)
+{
+    extern __shared__ __align__(16) unsigned char ring_smem[];
+    constexpr uint32_t kSlot = (DEG + 1) * 256u;
+    constexpr uint32_t kRing = S * kSlot;
+    const uint32_t lane = threadIdx.x;
+    const uint32_t gw = blockIdx.x * blockDim.y + threadIdx.y;
+    const uint32_t nv = (uint32_t)(p.v_end - p.v_begin);
+    const uint32_t slice = gw % nslice;
+    const uint32_t j0 = (gw / nslice) * chunk;
+    if (j0 >= nv)
+        return;
+    const uint32_t cnt = min(chunk, nv - j0);
+    const uint32_t o = slice * 32u + lane;
+    const uint32_t rwb = (uint32_t)p.R;  // row bytes (one int8 per replica)
+    // this thread's column of the spin rows, held in a register pair (an opaque copy: the
+    // compiler would otherwise re-derive it from threadIdx and the parameter every vertex)
+    char *tbb;
+    asm volatile("mov.b64 %0, %1;" : "=l"(tbb) : "l"(reinterpret_cast<char *>(p.s) + 8u * o));
+    const uint32_t g0 = (uint32_t)(p.slot0 >> 3) + o;
+    float bl[8];
+    {
+        const float4 *bp = reinterpret_cast<const float4 *>(p.betaf) + 2u * o;
+        const float4 a = __ldg(bp), b = __ldg(bp + 1);
+        const float b2[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            bl[i] = __fmul_rn(b2[i], kLog2e);
+    }
+    const PhiloxHoist ph = philox_hoist(p.t, g0, p.rk);
+    const uint32_t c4b = 0x4B000000u | (rwb >> 31);
+    // shared addresses: this lane's bytes of ring slot 0, and the warp's table double buffer
+    const uint32_t wsh = (uint32_t)__cvta_generic_to_shared(ring_smem) + threadIdx.y * ring_warp_bytes<DEG, S>();
+    const uint32_t ring0 = wsh + lane * 8u;
+    const uint32_t meta0 = wsh + kRing;
+    const uint32_t vb = (uint32_t)p.v_begin + j0;  // internal id of the chunk's first vertex
+    auto meta_issue = [&](uint32_t blk) {
+        const uint32_t j = blk * 32u + lane;
+        if (j < cnt) {
+            const uint32_t mb = meta0 + (blk & 1u) * kRingMetaBuf;
+            cp_async16(mb + lane * 16u, p.ell_col + 4u * (vb + j));
+            cp_async16(mb + 512u + lane * 16u, p.ell_w + 4u * (vb + j));
+            cp_async4(mb + 1024u + lane * 4u, p.orig + vb + j);
+        }
+    };
+    // table entry address of chunk vertex j (column int4 at +0, weights at +512, id at +1024)
+    auto entry = [&](uint32_t j) { return meta0 + ((j >> 5) & 1u) * kRingMetaBuf + (j & 31u) * 16u; };
+    auto rows_issue = [&](uint32_t j, uint32_t sl) {
+        const int4 c = lds128(entry(j));
+        const int32_t cs[4] = {c.x, c.y, c.z, c.w};
+        cp_async8(sl, tbb + (uint64_t)(vb + j) * rwb);
+#pragma unroll
+        for (int u = 0; u < DEG; ++u)
+            cp_async8(sl + (u + 1) * 256u, tbb + (uint64_t)(uint32_t)cs[u] * rwb);
+    };
+    meta_issue(0);
+    cp_commit();
+    cp_wait<0>();
+    __syncwarp();
+    uint32_t sl_iss = ring0;  // ring slot of the vertex issued next
+#pragma unroll
+    for (uint32_t j = 0; j + 1 < S; ++j) {
+        if (j < cnt)
+            rows_issue(j, sl_iss);
+        cp_commit();
+        sl_iss += kSlot;
+    }
+    uint32_t sl_cur = ring0;  // ring slot of the vertex decided now
+    for (uint32_t j = 0; j < cnt; ++j) {
+        if ((j & 31u) == 0) {
+            __syncwarp();  // every lane is done with the buffer this block overwrites
+            meta_issue((j >> 5) + 1);
+        }
+        if (j + S - 1 < cnt)
+            rows_issue(j + S - 1, sl_iss);
+        cp_commit();
+        sl_iss = sl_iss + kSlot == ring0 + kRing ? ring0 : sl_iss + kSlot;
+        cp_wait<S - 1>();
+        // the table block issued at the start of this 32-vertex block is complete from here on
+        // (S - 1 steps later); one __syncwarp makes every lane's part visible to all lanes
+        if ((j & 31u) == S - 1)
+            __syncwarp();
+        I8Rows<DEG> r;
+        r.own = lds64(sl_cur);
+#pragma unroll
+        for (int u = 0; u < DEG; ++u)
+            r.nb[u] = lds64(sl_cur + (u + 1) * 256u);
+        sl_cur = sl_cur + kSlot == ring0 + kRing ? ring0 : sl_cur + kSlot;
+        I8Meta m;
+        const uint32_t e = entry(j);
+        m.w = lds128(e + 512u);
+        m.io = lds32(meta0 + ((j >> 5) & 1u) * kRingMetaBuf + 1024u + (j & 31u) * 4u);
+        pipe_decide<DEG>(p, r, m, vb + j, tbb, rwb, bl, ph, g0, o, c4b);
+    }
+    cp_wait<0>();
+}
+
+template <int DEG, int S>
+cudaError_t launch_ring(const CsrI8Params &p, cudaStream_t st)
+{
+    const uint32_t nv = (uint32_t)(p.v_end - p.v_begin);
+    const uint32_t nslice = (uint32_t)p.R / 256u;
+    const size_t smem = (size_t)8 * ring_warp_bytes<DEG, S>();
+    static int per_sm = 0;  // resident CTAs per SM (once per instantiation)
+    if (!per_sm) {
+        cudaError_t e = cudaFuncSetAttribute(k_csr_i8_ring<DEG, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_csr_i8_ring<DEG, S>, 256, smem);
+        if (e != cudaSuccess)
+            return e;
+        if (per_sm < 1)
+            return cudaErrorInvalidConfiguration;
+    }
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t want = (uint32_t)nsm * (uint32_t)per_sm * 8u;  // one wave of resident warps
+    uint32_t nch = want / nslice;
+    if (nch < 1)
+        nch = 1;
+    if (nch > nv)
+        nch = nv;
+    // at least 40 vertices per warp: the prologue / drain stay a small share of a warp's work
+    // (and every chunk of more than 32 vertices crosses a table double-buffer boundary)
+    uint32_t chunk = (nv + nch - 1) / nch;
+    if (chunk < 40u)
+        chunk = 40u;
+    nch = (nv + chunk - 1) / chunk;
+    const uint32_t warps = nch * nslice;
+    k_csr_i8_ring<DEG, S><<<(warps + 7) / 8, dim3(32, 8), smem, st>>>(p, nslice, chunk);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_csr_i8_phase(const CsrI8Params &p, int32_t threads, cudaStream_t st)
 {
     if (p.R % 8 != 0 || p.slot0 % 8 != 0)
@@ -654,7 +845,14 @@ cudaError_t launch_csr_i8_phase(const CsrI8Params &p, int32_t threads, cudaStrea
     const dim3 block((unsigned)bx, (unsigned)by);
     const bool ell = p.ell_col != nullptr;
     if (p.wf) {
-        if (ell && kI8Pipe) {
+        if (ell && kI8Ring > 0 && p.R % 256 == 0) {
+            switch (p.ell_deg) {
+            case 1: return launch_ring<1, kI8Ring>(p, st);
+            case 2: return launch_ring<2, kI8Ring>(p, st);
+            case 3: return launch_ring<3, kI8Ring>(p, st);
+            default: return launch_ring<4, kI8Ring>(p, st);
+            }
+        } else if (ell && kI8Pipe) {
             switch (p.ell_deg) {
             case 1: k_csr_i8_pipe<1><<<grid, block, 0, st>>>(p); break;
             case 2: k_csr_i8_pipe<2><<<grid, block, 0, st>>>(p); break;
