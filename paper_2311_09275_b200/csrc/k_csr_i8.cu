@@ -560,7 +560,11 @@ __device__ __forceinline__ void pipe_decide(const CsrI8Params &p, const I8Rows<D
         }
     }
     // +1 (0x01) <-> -1 (0xFF): xor the byte with 0xFE
-    *reinterpret_cast<uint2 *>(tbb + (uint64_t)v * rwb) = make_uint2(r.own.x ^ fm[0], r.own.y ^ fm[1]);
+    // st.global on the (global-space) row address: the ring kernel's row base is an opaque
+    // register copy the compiler would otherwise store through with a generic ST
+    asm volatile("st.global.v2.u32 [%0], {%1, %2};" ::"l"(tbb + (uint64_t)v * rwb), "r"(r.own.x ^ fm[0]),
+                 "r"(r.own.y ^ fm[1])
+                 : "memory");
 }
 
 template <int DEG>
@@ -662,7 +666,9 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr uint32_t kRingMetaBuf = 32 * 16 + 32 * 16 + 32 * 4;  // columns, weights, ids of 32 vertices
+// table entry of one vertex in shared memory: columns (16 B), weights (16 B), original id, pad
+constexpr uint32_t kRingEntry = 48;
+constexpr uint32_t kRingMetaBuf = 32 * kRingEntry;  // one block of 32 vertices
 
 template <int DEG, int S>
 __host__ __device__ constexpr uint32_t ring_warp_bytes()
@@ -690,7 +696,7 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a)
 }
 
 template <int DEG, int S>
-__global__ void __launch_bounds__(256, 4) k_csr_i8_ring(const CsrI8Params p, uint32_t nslice, uint32_t chunk)
+__global__ void __launch_bounds__(256, 3) k_csr_i8_ring(const CsrI8Params p, uint32_t nslice, uint32_t chunk)
 {
     extern __shared__ __align__(16) unsigned char ring_smem[];
     constexpr uint32_t kSlot = (DEG + 1) * 256u;
@@ -729,16 +735,17 @@ __global__ void __launch_bounds__(256, 4) k_csr_i8_ring(const CsrI8Params p, uin
     auto meta_issue = [&](uint32_t blk) {
         const uint32_t j = blk * 32u + lane;
         if (j < cnt) {
-            const uint32_t mb = meta0 + (blk & 1u) * kRingMetaBuf;
-            cp_async16(mb + lane * 16u, p.ell_col + 4u * (vb + j));
-            cp_async16(mb + 512u + lane * 16u, p.ell_w + 4u * (vb + j));
-            cp_async4(mb + 1024u + lane * 4u, p.orig + vb + j);
+            const uint32_t me = meta0 + (blk & 1u) * kRingMetaBuf + lane * kRingEntry;
+            cp_async16(me, p.ell_col + 4u * (vb + j));
+            cp_async16(me + 16u, p.ell_w + 4u * (vb + j));
+            cp_async4(me + 32u, p.orig + vb + j);
         }
     };
-    // table entry address of chunk vertex j (column int4 at +0, weights at +512, id at +1024)
-    auto entry = [&](uint32_t j) { return meta0 + ((j >> 5) & 1u) * kRingMetaBuf + (j & 31u) * 16u; };
-    auto rows_issue = [&](uint32_t j, uint32_t sl) {
-        const int4 c = lds128(entry(j));
+    // table entries of the two 32-vertex blocks form one circular list of 64 entries
+    const uint32_t meta_end = meta0 + 2u * kRingMetaBuf;
+    auto next_entry = [&](uint32_t e) { return e + kRingEntry == meta_end ? meta0 : e + kRingEntry; };
+    auto rows_issue = [&](uint32_t j, uint32_t sl, uint32_t e) {
+        const int4 c = lds128(e);
         const int32_t cs[4] = {c.x, c.y, c.z, c.w};
         cp_async8(sl, tbb + (uint64_t)(vb + j) * rwb);
 #pragma unroll
@@ -750,23 +757,27 @@ __global__ void __launch_bounds__(256, 4) k_csr_i8_ring(const CsrI8Params p, uin
     cp_wait<0>();
     __syncwarp();
     uint32_t sl_iss = ring0;  // ring slot of the vertex issued next
+    uint32_t e_iss = meta0;   // its table entry
 #pragma unroll
     for (uint32_t j = 0; j + 1 < S; ++j) {
         if (j < cnt)
-            rows_issue(j, sl_iss);
+            rows_issue(j, sl_iss, e_iss);
         cp_commit();
         sl_iss += kSlot;
+        e_iss += kRingEntry;
     }
     uint32_t sl_cur = ring0;  // ring slot of the vertex decided now
+    uint32_t e_cur = meta0;   // its table entry
     for (uint32_t j = 0; j < cnt; ++j) {
         if ((j & 31u) == 0) {
             __syncwarp();  // every lane is done with the buffer this block overwrites
             meta_issue((j >> 5) + 1);
         }
         if (j + S - 1 < cnt)
-            rows_issue(j + S - 1, sl_iss);
+            rows_issue(j + S - 1, sl_iss, e_iss);
         cp_commit();
         sl_iss = sl_iss + kSlot == ring0 + kRing ? ring0 : sl_iss + kSlot;
+        e_iss = next_entry(e_iss);
         cp_wait<S - 1>();
         // the table block issued at the start of this 32-vertex block is complete from here on
         // (S - 1 steps later); one __syncwarp makes every lane's part visible to all lanes
@@ -779,9 +790,9 @@ __global__ void __launch_bounds__(256, 4) k_csr_i8_ring(const CsrI8Params p, uin
             r.nb[u] = lds64(sl_cur + (u + 1) * 256u);
         sl_cur = sl_cur + kSlot == ring0 + kRing ? ring0 : sl_cur + kSlot;
         I8Meta m;
-        const uint32_t e = entry(j);
-        m.w = lds128(e + 512u);
-        m.io = lds32(meta0 + ((j >> 5) & 1u) * kRingMetaBuf + 1024u + (j & 31u) * 4u);
+        m.w = lds128(e_cur + 16u);
+        m.io = lds32(e_cur + 32u);
+        e_cur = next_entry(e_cur);
         pipe_decide<DEG>(p, r, m, vb + j, tbb, rwb, bl, ph, g0, o, c4b);
     }
     cp_wait<0>();
