@@ -338,7 +338,9 @@ def run_ours(args):
     per_launch_attempts = n * R * (rounds * kex if fused else (kex if kex > 0 else sweeps))
     roof = roofline_entry(avg_launch_ms, per_launch_attempts, cfg["layout"], clk, args.workload)
     roof["kernel"] = "k_grid_bits" if (inst["kind"] == "grid" and cfg["layout"] == "bits") else \
-        ("k_csr_bits" if cfg["layout"] == "bits" else "k_csr_i8_phase")
+        ("k_csr_bits" if cfg["layout"] == "bits" else
+         ("k_csr_i8_ring" if inst.get("w") is not None and inst["w"].dtype == np.float32 and R % 256 == 0
+          else "k_csr_i8_phase"))
     roof["kernel_share_of_step"] = kernel_ms / max(total_ms * (1 if world == 1 else 1), 1e-9)
     roof["avg_launch_ms"] = avg_launch_ms
 
@@ -401,7 +403,10 @@ def run_ours(args):
             "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
                        "n": n, "replicas_per_gpu": R, "sweeps_per_step": sweeps, "exchange_every": kex,
                        "parallelism": f"copies sharded over {world} GPU(s), weak scaling",
-                       "l2": "flushed between timed steps (state is SMEM/L2-resident by design)"},
+                       "l2": ("flushed between timed steps (256 MB write); the state is SMEM/L2-resident "
+                              "by design" if cfg["layout"] == "bits" or n * R < (64 << 20) else
+                              "flushed between timed steps (256 MB write); spins (%.2f GB) exceed L2"
+                              % (n * R / 1e9))},
             "roofline": roof,
             "hbm_frac": value / world * bpa / 1e9 / peaks.get("hbm_gbs", 6551.4),
             "cpu_baseline": cpu,
