@@ -55,6 +55,18 @@ def test_smallest_last_colouring_matches_oracle():
     a, na = L.ising_greedy_colour_sl(3000, rp, col)
     b, nb = oracle.greedy_colour_sl(3000, rp, col)
     assert na == nb and np.array_equal(a, b)
+    # the library's bitmap buckets give way to its heap when (max degree + 1) x n / 64
+    # words exceed 2^25: a star on 2^16 vertices plus a sparse random part takes that path
+    n = 1 << 16
+    hub = np.zeros(n - 1, np.int64)
+    leaves = np.arange(1, n, dtype=np.int64)
+    x, y = synth.gnm(n - 1, 4000, 11)
+    u = np.concatenate([hub, x + 1])
+    v = np.concatenate([leaves, y + 1])
+    rp, col, _ = synth.edges_to_csr(n, u, v, np.ones(u.size, np.int32))
+    a, na = L.ising_greedy_colour_sl(n, rp, col)
+    b, nb = oracle.greedy_colour_sl(n, rp, col)
+    assert na == nb and np.array_equal(a, b)
 
 
 def _desc(**kw):
