@@ -169,11 +169,11 @@ def all_gather(recv, send, group=None):
         dist.all_gather_into_tensor(recv, send, group=group)
         return
     world = dist.get_world_size(group)
-    parts = list(torch.chunk(recv, world, dim=0))
-    bufs = [torch.empty_like(p) for p in parts]
-    dist.all_gather(bufs, send, group=group)
-    for p, b in zip(parts, bufs):
-        p.copy_(b)
+    host = send.device.type != "cpu"  # gloo: gather host copies of device records
+    src = send.cpu() if host else send
+    bufs = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(bufs, src, group=group)
+    recv.copy_(torch.cat(bufs, dim=0))
 
 
 def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True, fused: bool = True,
