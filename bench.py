@@ -11,7 +11,10 @@ Workload at N=1 (BASELINE.json configs[1], the metric's config): 80x100 +-1 toru
 spins.  One step = that whole schedule (1,000 rounds of 10 sweeps + best check +
 exchange) on inputs already resident on the GPU.  N>1: weak scaling -- every rank
 runs its own 64-copy shard (distinct global copy ids), local exchanges, and one NCCL
-all-gather of the per-rank best records per step.
+all-gather of the per-rank best records per step.  C4 (--workload c4a|c4b) is strong
+scaling as BASELINE.json configs[3] states: 128 copies = 16,384 replicas in total, split
+over the N ranks (--copies overrides the copy count, e.g. --workload c4b --copies 16 runs
+one rank's share of the 8-GPU job on one GPU).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4a|c4b|c1|c5]
     python bench.py --impl reference ...   # the CPU oracle on the host cores
@@ -34,6 +37,8 @@ import synth  # noqa: E402
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 PROFILE_FILE = os.path.join(ROOT, "profiles", "inst_per_attempt.json")
+
+STRONG = ("c4a", "c4b")  # fixed total replicas sharded over the GPUs (BASELINE.json configs[3])
 
 WORKLOADS = {
     "c1": "16x16 +-1 torus, 64 temps x 1 copy, 1000 sweeps, exchange every 10, int8 spins",
@@ -58,6 +63,9 @@ def parse():
     ap.add_argument("--sweeps", type=int, default=0, help="override sweeps per step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--copies", type=int, default=0,
+                    help="copies override: per rank (weak-scaling workloads) or in total (c4a/c4b); "
+                         "e.g. --workload c4b --copies 16 measures one rank's share at 8 GPUs")
     ap.add_argument("--threads", type=int, default=0, help="CTA size override")
     return ap.parse_args()
 
@@ -260,17 +268,27 @@ def run_ours(args):
     cfg = workload_params(args.workload, args.sweeps)
     inst = synth.make_instance(cfg)
     K, C = cfg["K"], cfg["C"]
+    if args.copies:
+        C = args.copies
     betas = synth.beta_ladder(K)
-    Cg = C * world  # weak scaling: every rank runs a C-copy shard with distinct global ids
+    strong = args.workload in STRONG
+    if strong:  # BASELINE configs[3]: the 128 copies (16,384 replicas) are sharded over the ranks
+        if C % world:
+            raise SystemExit(f"{args.workload}: {C} copies do not split over {world} ranks")
+        Cg = C
+        c_lo, c_hi = rank * C // world, (rank + 1) * C // world
+    else:  # weak scaling: every rank runs a C-copy shard with distinct global ids
+        Cg = C * world
+        c_lo, c_hi = rank * C, (rank + 1) * C
     stream = torch.cuda.current_stream()
-    eng = Engine(inst, K, Cg, betas, seed=synth.PHILOX_KEY, copy_begin=rank * C,
-                 copy_end=(rank + 1) * C, layout=cfg["layout"], device=local,
+    eng = Engine(inst, K, Cg, betas, seed=synth.PHILOX_KEY, copy_begin=c_lo,
+                 copy_end=c_hi, layout=cfg["layout"], device=local,
                  block_threads=args.threads, stream=stream.cuda_stream, colour=cfg.get("colouring"))
     n, R = inst["n"], eng.R
     sweeps, kex = cfg["sweeps"], cfg["k_ex"]
     rounds = sweeps // kex if kex > 0 else 0
     rem = sweeps - rounds * kex if kex > 0 else sweeps
-    attempts_step = n * R * sweeps
+    attempts_step = n * R * sweeps  # this rank's attempts per step
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
     fused = cfg["layout"] == "bits" and kex > 0  # bit-packed kernels run all rounds in one launch
@@ -332,7 +350,7 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    value = attempts_step * world * args.steps / (total_ms * 1e-3)
+    value = n * K * Cg * sweeps * args.steps / (total_ms * 1e-3)  # all ranks' attempts
     ms_step = total_ms / args.steps
     avg_launch_ms = kernel_ms / max(nk, 1)
     per_launch_attempts = n * R * (rounds * kex if fused else (kex if kex > 0 else sweeps))
@@ -355,8 +373,8 @@ def run_ours(args):
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            e = Engine(inst, K, Cg, betas, seed=synth.PHILOX_KEY + s, copy_begin=rank * C,
-                       copy_end=(rank + 1) * C, layout=cfg["layout"], device=local,
+            e = Engine(inst, K, Cg, betas, seed=synth.PHILOX_KEY + s, copy_begin=c_lo,
+                       copy_end=c_hi, layout=cfg["layout"], device=local,
                        block_threads=args.threads, stream=stream.cuda_stream,
                        colour=cfg.get("colouring"))
             if fused:
@@ -383,7 +401,7 @@ def run_ours(args):
         t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = {"value": attempts_step * world * args.steps / (float(t.item()) * 1e-3),
+        e2e = {"value": n * K * Cg * sweeps * args.steps / (float(t.item()) * 1e-3),
                "unit": "attempts/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "includes": "create (validate, tables, upload, init) + full schedule + best/energy readback"}
 
@@ -397,12 +415,14 @@ def run_ours(args):
         json_line({
             "metric": "spin-flip attempts/s", "value": value, "unit": "attempts/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "u32" if cfg["layout"] == "bits" else ("f32" if cfg["kind"] == "regular" else "int32"),
             "data": "synthetic",
             "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
                        "n": n, "replicas_per_gpu": R, "sweeps_per_step": sweeps, "exchange_every": kex,
-                       "parallelism": f"copies sharded over {world} GPU(s), weak scaling",
+                       "copies_total": Cg, "copies_per_gpu": c_hi - c_lo,
+                       "parallelism": f"copies sharded over {world} GPU(s), "
+                                      + ("strong scaling (fixed total)" if strong else "weak scaling"),
                        "l2": ("flushed between timed steps (256 MB write); the state is SMEM/L2-resident "
                               "by design" if cfg["layout"] == "bits" or n * R < (64 << 20) else
                               "flushed between timed steps (256 MB write); spins (%.2f GB) exceed L2"
