@@ -291,7 +291,10 @@ def run_ours(args):
     attempts_step = n * R * sweeps  # this rank's attempts per step
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
-    fused = cfg["layout"] == "bits" and kex > 0  # bit-packed kernels run all rounds in one launch
+    # bit-packed kernels run all rounds in one launch (unless a band-split handle's clusters
+    # would not all be resident: then ising_run takes per-round launches, counted as such)
+    fused = cfg["layout"] == "bits" and kex > 0
+    fused_one_launch = fused and bool(eng.info.fused_pt)
 
     def timed(kev, fn, *a):
         if kev is None:
@@ -308,7 +311,7 @@ def run_ours(args):
         if fused:
             # all rounds in ONE k_grid_bits launch (clusters exchange through DSMEM) + merge
             timed(kev, eng.run, rounds, kex)
-            launches += 2
+            launches += 2 if fused_one_launch else 3 * rounds
         else:
             for _ in range(rounds):
                 timed(kev, eng.sweep, kex)
@@ -355,7 +358,8 @@ def run_ours(args):
     avg_launch_ms = kernel_ms / max(nk, 1)
     per_launch_attempts = n * R * (rounds * kex if fused else (kex if kex > 0 else sweeps))
     roof = roofline_entry(avg_launch_ms, per_launch_attempts, cfg["layout"], clk, args.workload)
-    roof["kernel"] = "k_grid_bits" if (inst["kind"] == "grid" and cfg["layout"] == "bits") else \
+    roof["kernel"] = ("k_grid_bands" if eng.info.bands > 1 else "k_grid_bits") \
+        if (inst["kind"] == "grid" and cfg["layout"] == "bits") else \
         ("k_csr_bits" if cfg["layout"] == "bits" else
          ("k_csr_i8_ring" if inst.get("w") is not None and inst["w"].dtype == np.float32 and R % 256 == 0
           else "k_csr_i8_phase"))

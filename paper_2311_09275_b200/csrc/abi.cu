@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -97,6 +98,8 @@ struct ising_handle {
     int32_t cnt_levels = 8;
     int32_t qmax = 0;
     int32_t ell_deg = 0;  // I8: width of the padded neighbour table (0 = CSR path)
+    int32_t bands = 1;    // grid BITS: row bands per word group (CTA pairs with DSMEM halos)
+    bool fused_ok = true; // grid BITS: the fused PT launch's clusters (K/32 x bands CTAs per copy) fit one wave
     std::vector<int32_t> class_off;
     // device buffers
     uint32_t *d_state[2] = {nullptr, nullptr};
@@ -325,6 +328,7 @@ GridBitsParams grid_params(ising_handle *h, int32_t n_rounds, int32_t k_ex, bool
     p.Tx_off = h->d_Tx_off;
     p.Tx_len = h->d_Tx_len;
     p.rk = h->rk;
+    p.bands = h->bands;
     return p;
 }
 
@@ -352,11 +356,18 @@ CsrBitsParams csr_params(ising_handle *h, int32_t n_rounds, int32_t k_ex, bool p
     return p;
 }
 
+// Torus sweep launch: the band-split kernel when the handle's groups are split over CTA pairs.
+cudaError_t launch_grid(const ising_handle *h, const GridBitsParams &p)
+{
+    return h->bands > 1 ? launch_grid_bands(p, h->G, h->threads, h->smem, h->st)
+                        : launch_grid_bits(p, h->G, h->threads, h->smem, h->st);
+}
+
 // Energies after a state change (set_spins / create).
 int refresh_energy(ising_handle *h)
 {
     if (h->kernel == KER_GRID_BITS) {
-        CK(launch_grid_bits(grid_params(h, 1, 0, false), h->G, h->threads, h->smem, h->st));
+        CK(launch_grid(h, grid_params(h, 1, 0, false)));
         h->cur ^= 1;
     } else if (h->kernel == KER_CSR_BITS) {
         CK(launch_csr_bits(csr_params(h, 1, 0, false), h->G, h->threads, h->smem, h->st));
@@ -636,7 +647,7 @@ int launch_sweeps_i8(ising_handle *h, int32_t ns, const void *sched)
 int launch_sweeps(ising_handle *h, int32_t ns)
 {
     if (h->kernel == KER_GRID_BITS) {
-        CK(launch_grid_bits(grid_params(h, 1, ns, false), h->G, h->threads, h->smem, h->st));
+        CK(launch_grid(h, grid_params(h, 1, ns, false)));
         h->cur ^= 1;
     } else if (h->kernel == KER_CSR_BITS) {
         CK(launch_csr_bits(csr_params(h, 1, ns, false), h->G, h->threads, h->smem, h->st));
@@ -956,6 +967,24 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
         return fail(ISING_E_UNSUPPORTED, "BITS grid: lattice too large for shared memory (n=" +
                                              std::to_string(n) + ")");
     const int32_t hx = Lx / 2, half = n / 2;
+    // band split: with at most half as many word groups as SMs, each group's
+    // rows are split over a CTA pair (halo rows through DSMEM), so twice as many SMs work.
+    // ISING_GRID_BANDS=1|2 overrides the choice (tests, measurements).
+    {
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device);
+        const bool can2 = h->wpc * 2 <= 8;  // portable cluster size with the fused PT launch
+        h->bands = (can2 && 2 * (int64_t)h->G <= nsm) ? 2 : 1;
+        if (const char *env = std::getenv("ISING_GRID_BANDS")) {
+            const int want = std::atoi(env);
+            if (want != 1 && want != 2)
+                return fail(ISING_E_ARG, "ISING_GRID_BANDS must be 1 or 2");
+            if (want == 2 && !can2)
+                return fail(ISING_E_UNSUPPORTED, "ISING_GRID_BANDS=2 needs n_temps <= 128");
+            h->bands = want;
+        }
+    }
+    const int32_t band_rows = Ly / h->bands;
     h->ymagic = (uint32_t)((((uint64_t)1 << 32) + hx - 1) / hx);
     for (int32_t l = 0; l < half; ++l)
         if ((int32_t)(((uint64_t)l * h->ymagic) >> 32) != l / hx)
@@ -966,8 +995,8 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
     // warps run ~5% slower than 24 on C2).
     if (desc->block_threads == 0) {
         h->threads = 0;
-        for (int32_t np = 1; np <= Ly && !h->threads; ++np) {
-            int32_t rows = (Ly + np - 1) / np;
+        for (int32_t np = 1; np <= band_rows && !h->threads; ++np) {
+            int32_t rows = (band_rows + np - 1) / np;
             if (rows >= 2)
                 rows += rows & 1;  // grid_rows_per_pass keeps rows per pass even
             const int32_t nt = ((hx * rows + 127) / 128) * 128;
@@ -981,9 +1010,16 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
         return fail(ISING_E_ARG, "BITS grid: block_threads must be <= " + std::to_string(kGridMaxThreads));
     if (2 * hx > h->threads)  // two class rows per pass at least (even rows per pass)
         return fail(ISING_E_UNSUPPORTED, "BITS grid needs block_threads >= Lx");
-    const int32_t rpp = grid_rows_per_pass(h->threads, hx), npass = (Ly + rpp - 1) / rpp;
+    const int32_t rpp = grid_rows_per_pass(h->threads, hx), npass = (band_rows + rpp - 1) / rpp;
     if (npass > 31)
         return fail(ISING_E_UNSUPPORTED, "BITS grid: too many rows per thread (Ly/(threads/(Lx/2)) > 31)");
+    // the fused PT launch runs one cluster of K/32 x bands CTAs per copy: with bands it only
+    // pays when every copy's cluster is resident at once (else ising_run takes per-round
+    // launches, whose clusters are the band pairs alone)
+    if (h->bands > 1 && h->K >= 2) {
+        CK(cudaSetDevice(h->device));
+        h->fused_ok = grid_bands_max_clusters(h->wpc * h->bands, h->threads, h->smem) >= h->C_local;
+    }
     // J bytes in colour-separated order: bit 0..3 = (right, left, down, up) bond has J = -1
     std::vector<uint8_t> jb(n);
     for (int32_t c = 0; c < 2; ++c)
@@ -1148,10 +1184,11 @@ int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
         return fail(ISING_E_UNSUPPORTED, "replica exchange requires integer weights");
     if (n_rounds == 0)
         return ISING_OK;
-    if ((h->kernel == KER_GRID_BITS || h->kernel == KER_CSR_BITS) && h->K >= 2) {
+    if ((h->kernel == KER_GRID_BITS || h->kernel == KER_CSR_BITS) && h->K >= 2 &&
+        (h->kernel != KER_GRID_BITS || h->fused_ok)) {
         // one launch: clusters of K/32 CTAs (one copy each) run all rounds on chip
         if (h->kernel == KER_GRID_BITS)
-            CK(launch_grid_bits(grid_params(h, n_rounds, k_ex, true), h->G, h->threads, h->smem, h->st));
+            CK(launch_grid(h, grid_params(h, n_rounds, k_ex, true)));
         else
             CK(launch_csr_bits(csr_params(h, n_rounds, k_ex, true), h->G, h->threads, h->smem, h->st));
         h->cur ^= 1;
@@ -1236,7 +1273,7 @@ int ising_anneal(ising_handle *h, int32_t n_sweeps, const double *sched)
     if (h->kernel == KER_GRID_BITS) {
         GridBitsParams p = grid_params(h, 1, n_sweeps, false);
         p.planes_sched = (const uint32_t *)h->d_sched;
-        CK(launch_grid_bits(p, h->G, h->threads, h->smem, h->st));
+        CK(launch_grid(h, p));
         h->cur ^= 1;
         h->t += (uint32_t)n_sweeps;
     } else if (h->kernel == KER_CSR_BITS) {
@@ -1463,6 +1500,8 @@ int ising_info(const ising_handle *h, ising_info_t *out)
     out->exchanges_done = h->e;
     out->W_int = h->W_int;
     out->W_f64 = h->W_f;
+    out->bands = h->bands;
+    out->fused_pt = (h->kernel == KER_CSR_BITS || (h->kernel == KER_GRID_BITS && h->fused_ok)) && h->K >= 2;
     return ISING_OK;
 }
 

@@ -206,19 +206,35 @@ __device__ __forceinline__ void pt_init(PtShared &ps, const int64_t *walker, int
 // move configurations: within-word pairs by a delta swap, the cross-word pair through the
 // neighbours' boundary bit planes B0 / B31 (n bits each).  Same result as k_exchange +
 // k_swap_bits.
-template <class Snap>
+//
+// Band split (torus kernel, NB = 2): the cluster holds NB CTAs per word type (rank = wt * NB +
+// band), each owning the rows of one band; a word type's energy is the sum of its bands'
+// counts.  Every CTA applies the swaps to its whole local lattice copy: its own rows and the
+// halo rows it holds are current, and the halo rows' boundary bits come from the same band of
+// the neighbouring word type, whose copy of those rows is current as well.
+template <int NB = 1, class Snap>
 __device__ void pt_step(PtShared &ps, const int32_t *Ucnt, int64_t m_edges, uint32_t *S, int n,
                         uint32_t *B0, uint32_t *B31, int KW, int wt, uint32_t c_global, uint32_t t_now,
                         uint32_t e_now, const uint64_t *Tx, const int64_t *Tx_off, const int32_t *Tx_len,
-                        const RoundKeys &rk, Snap snap)
+                        const RoundKeys &rk, Snap snap, int band = 0)
 {
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int K = 32 * KW;
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();  // every CTA's Ucnt complete
-    for (int k = tid; k < K; k += nt) {
-        const int32_t *rem = cluster.map_shared_rank(Ucnt, k >> 5);
-        ps.Ecopy[k] = 2 * (int64_t)rem[k & 31] - m_edges;
+    if (NB == 1) {
+        for (int k = tid; k < K; k += nt) {
+            const int32_t *rem = cluster.map_shared_rank(Ucnt, k >> 5);
+            ps.Ecopy[k] = 2 * (int64_t)rem[k & 31] - m_edges;
+        }
+    } else {
+        for (int k = tid; k < K; k += nt) {
+            int64_t u = 0;
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+                u += cluster.map_shared_rank(Ucnt, (k >> 5) * NB + b)[k & 31];
+            ps.Ecopy[k] = 2 * u - m_edges;
+        }
     }
     for (int q = tid; q < KW; q += nt)
         ps.Mswap[q] = 0u;
@@ -296,8 +312,8 @@ __device__ void pt_step(PtShared &ps, const int32_t *Ucnt, int64_t m_edges, uint
             }
         }
         cluster.sync();
-        const uint32_t *nB31 = cross_lo ? cluster.map_shared_rank(B31, wt - 1) : B31;
-        const uint32_t *nB0 = cross_hi ? cluster.map_shared_rank(B0, wt + 1) : B0;
+        const uint32_t *nB31 = cross_lo ? cluster.map_shared_rank(B31, NB == 1 ? wt - 1 : (wt - 1) * NB + band) : B31;
+        const uint32_t *nB0 = cross_hi ? cluster.map_shared_rank(B0, NB == 1 ? wt + 1 : (wt + 1) * NB + band) : B0;
         for (int l = tid; l < n; l += nt) {
             uint32_t w = S[l];
             const uint32_t tt = (w ^ (w >> 1)) & Min;
@@ -318,11 +334,15 @@ __device__ void pt_step(PtShared &ps, const int32_t *Ucnt, int64_t m_edges, uint
     __syncthreads();
 }
 
+template <int NB = 1>
 __device__ __forceinline__ void pt_finish(const PtShared &ps, bool pt, int n_rounds, const int32_t *Ucnt,
                                           int64_t m_edges, int64_t *E_out, int64_t *walker,
-                                          int64_t *copy_best, int gl, int wt, int c_local, int K)
+                                          int64_t *copy_best, int gl, int wt, int c_local, int K,
+                                          int band = 0)
 {
     const int tid = threadIdx.x;
+    if (NB > 1 && band != 0)  // band 0 writes the word type's results (every band holds the same)
+        return;
     if (tid < 32) {
         E_out[(size_t)gl * 32 + tid] =
             pt && n_rounds > 0 ? ps.Ecopy[32 * wt + tid] : 2 * (int64_t)Ucnt[tid] - m_edges;

@@ -73,6 +73,7 @@ struct GridBitsParams {
     const int64_t *Tx_off;
     const int32_t *Tx_len;
     RoundKeys rk;
+    int32_t bands;             // row bands per word group (1, or 2: CTA pairs with DSMEM halo rows)
 };
 
 struct CsrBitsParams {
@@ -177,6 +178,10 @@ cudaError_t launch_init_i8(int8_t *s, int32_t n, int32_t R, const uint32_t *orig
 cudaError_t launch_grid_bits(const GridBitsParams &p, int32_t G, int32_t threads, size_t smem,
                              cudaStream_t st);
 size_t grid_bits_smem(int32_t n);
+// band-split torus kernel (k_grid_bands.cu): G word groups on 2 G CTAs
+cudaError_t launch_grid_bands(const GridBitsParams &p, int32_t G, int32_t threads, size_t smem,
+                              cudaStream_t st);
+int32_t grid_bands_max_clusters(int32_t cluster, int32_t threads, size_t smem);
 int32_t grid_bits_qcap(int32_t n);
 cudaError_t launch_csr_bits(const CsrBitsParams &p, int32_t G, int32_t threads, size_t smem,
                             cudaStream_t st);

@@ -54,7 +54,7 @@ class Info(C.Structure):
                 ("copy_end", C.c_int32), ("slot_begin", C.c_int64), ("n_slots", C.c_int64),
                 ("layout", C.c_int32), ("rng", C.c_int32), ("wtype", C.c_int32),
                 ("kernel", C.c_int32), ("sweeps_done", C.c_int64), ("exchanges_done", C.c_int64),
-                ("W_int", C.c_int64), ("W_f64", C.c_double)]
+                ("W_int", C.c_int64), ("W_f64", C.c_double), ("bands", C.c_int32), ("fused_pt", C.c_int32)]
 
 
 _lib = None
