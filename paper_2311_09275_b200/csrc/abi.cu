@@ -15,6 +15,7 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 #include <queue>
 #include <functional>
@@ -277,20 +278,37 @@ int build_common_device(ising_handle *h, int64_t sum_abs_w)
     // exchange tables (integer weights): d from -1 down while the threshold is
     // non-zero, capped by the largest possible energy difference 2*sum|w|.
     if (h->wtype == ISING_W_I32 && h->K >= 2) {
-        std::vector<uint64_t> Tx;
-        std::vector<int64_t> off(h->K - 1);
-        std::vector<int32_t> len(h->K - 1);
+        // rows are independent (hundreds of thousands of libm exp calls for a 64-rung
+        // ladder): built on host threads, then concatenated in pair order
+        const int32_t npair = h->K - 1;
+        std::vector<std::vector<uint64_t>> rows(npair);
         const int64_t dmax = 2 * sum_abs_w;
-        for (int32_t k = 0; k + 1 < h->K; ++k) {
+        auto build_rows = [&](int32_t k0, int32_t step) {
+            for (int32_t k = k0; k < npair; k += step)
+                for (int64_t d = -1; -d <= dmax; --d) {
+                    const uint64_t T = exchange_threshold(h->betas[k], h->betas[k + 1], d);
+                    if (T == 0)
+                        break;
+                    rows[k].push_back(T);
+                }
+        };
+        const int32_t nthr = std::max(1, std::min<int32_t>(npair, (int32_t)std::thread::hardware_concurrency()));
+        if (nthr > 1 && dmax > 256) {
+            std::vector<std::thread> pool;
+            for (int32_t t = 0; t < nthr; ++t)
+                pool.emplace_back(build_rows, t, nthr);
+            for (auto &th : pool)
+                th.join();
+        } else {
+            build_rows(0, 1);
+        }
+        std::vector<uint64_t> Tx;
+        std::vector<int64_t> off(npair);
+        std::vector<int32_t> len(npair);
+        for (int32_t k = 0; k < npair; ++k) {
             off[k] = (int64_t)Tx.size();
-            int64_t d = -1;
-            for (; -d <= dmax; --d) {
-                const uint64_t T = exchange_threshold(h->betas[k], h->betas[k + 1], d);
-                if (T == 0)
-                    break;
-                Tx.push_back(T);
-            }
-            len[k] = (int32_t)(-d - 1);
+            len[k] = (int32_t)rows[k].size();
+            Tx.insert(Tx.end(), rows[k].begin(), rows[k].end());
         }
         CK(h->alloc(&h->d_Tx, Tx.size()));
         CK(h->alloc(&h->d_Tx_off, off.size()));
