@@ -357,7 +357,9 @@ def run_ours(args):
     ms_step = total_ms / args.steps
     avg_launch_ms = kernel_ms / max(nk, 1)
     per_launch_attempts = n * R * (rounds * kex if fused else (kex if kex > 0 else sweeps))
-    roof = roofline_entry(avg_launch_ms, per_launch_attempts, cfg["layout"], clk, args.workload)
+    # instruction counts per attempt are kernel-specific: the band-split kernel has its own entry
+    ipa_key = args.workload + ("_bands" if eng.info.bands > 1 else "")
+    roof = roofline_entry(avg_launch_ms, per_launch_attempts, cfg["layout"], clk, ipa_key)
     roof["kernel"] = ("k_grid_bands" if eng.info.bands > 1 else "k_grid_bits") \
         if (inst["kind"] == "grid" and cfg["layout"] == "bits") else \
         ("k_csr_bits" if cfg["layout"] == "bits" else
