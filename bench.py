@@ -293,7 +293,8 @@ def run_ours(args):
 
     # bit-packed kernels run all rounds in one launch (unless a band-split handle's clusters
     # would not all be resident: then ising_run takes per-round launches, counted as such)
-    fused = cfg["layout"] == "bits" and kex > 0
+    # (small int8 instances with integer weights, C1, also run all rounds in one launch)
+    fused = kex > 0 and (cfg["layout"] == "bits" or bool(eng.info.fused_pt))
     fused_one_launch = fused and bool(eng.info.fused_pt)
 
     def timed(kev, fn, *a):
@@ -359,12 +360,13 @@ def run_ours(args):
     per_launch_attempts = n * R * (rounds * kex if fused else (kex if kex > 0 else sweeps))
     # instruction counts per attempt are kernel-specific: the band-split kernel has its own entry
     ipa_key = args.workload + ("_bands" if eng.info.bands > 1 else "")
-    roof = roofline_entry(avg_launch_ms, per_launch_attempts, cfg["layout"], clk, ipa_key)
+    roof = roofline_entry(avg_launch_ms, per_launch_attempts,
+                          "bits" if fused_one_launch else cfg["layout"], clk, ipa_key)
     roof["kernel"] = ("k_grid_bands" if eng.info.bands > 1 else "k_grid_bits") \
         if (inst["kind"] == "grid" and cfg["layout"] == "bits") else \
         ("k_csr_bits" if cfg["layout"] == "bits" else
          ("k_csr_i8_ring" if inst.get("w") is not None and inst["w"].dtype == np.float32 and R % 256 == 0
-          else "k_csr_i8_phase"))
+          else ("k_i8_small" if fused_one_launch else "k_csr_i8_phase")))
     roof["kernel_share_of_step"] = kernel_ms / max(total_ms * (1 if world == 1 else 1), 1e-9)
     roof["avg_launch_ms"] = avg_launch_ms
 

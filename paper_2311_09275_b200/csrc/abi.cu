@@ -374,6 +374,15 @@ CsrBitsParams csr_params(ising_handle *h, int32_t n_rounds, int32_t k_ex, bool p
     return p;
 }
 
+// Small int8 instances with integer weights run a whole PT schedule in one k_i8_small launch
+// (one CTA per copy, the copy's n x K spins in shared memory).
+bool small_i8(const ising_handle *h)
+{
+    return h->kernel == KER_CSR_I8 && h->wtype == ISING_W_I32 && h->K >= 2 && h->K <= 256 &&
+           h->K % 8 == 0 && (int64_t)h->n * h->K <= kI8SmallMaxBytes &&
+           (int64_t)h->K * (h->qmax + 1) * 8 <= 64 * 1024;  // threshold rows in shared memory
+}
+
 // Torus sweep launch: the band-split kernel when the handle's groups are split over CTA pairs.
 cudaError_t launch_grid(const ising_handle *h, const GridBitsParams &p)
 {
@@ -606,6 +615,10 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
             CK(cudaStreamSynchronize(h->st));  // host vectors die at scope end
         }
         CK(h->alloc(&h->d_s8, (size_t)n * h->R));
+        if (small_i8(h.get())) {  // fused PT launch scratch (k_i8_small)
+            CK(h->alloc(&h->d_copy_best, (size_t)h->C_local * 3));
+            CK(h->alloc(&h->d_snap, (size_t)h->C_local * n));
+        }
         h->scratch_bytes = energy_i8_scratch(n, (int32_t)h->R);
         CK(h->alloc((char **)&h->d_scratch, h->scratch_bytes));
         CK(launch_init_i8(h->d_s8, n, (int32_t)h->R, h->d_orig, h->slot0, h->rk, h->st));
@@ -1202,6 +1215,21 @@ int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
         return fail(ISING_E_UNSUPPORTED, "replica exchange requires integer weights");
     if (n_rounds == 0)
         return ISING_OK;
+    if (small_i8(h)) {
+        SmallI8Params p{};
+        p.s = h->d_s8; p.rp = h->d_rp; p.col = h->d_col; p.wi = h->d_wi; p.orig = h->d_orig;
+        p.class_off = h->d_class_off; p.T = h->d_T;
+        p.E_out = h->d_E; p.walker = h->d_walker; p.copy_best = h->d_copy_best; p.snap = h->d_snap;
+        p.Tx = h->d_Tx; p.Tx_off = h->d_Tx_off; p.Tx_len = h->d_Tx_len;
+        p.n = h->n; p.R = (int32_t)h->R; p.K = h->K; p.qmax = h->qmax; p.ncol = h->ncol;
+        p.slot0 = h->slot0; p.t0 = h->t; p.e0 = h->e; p.n_rounds = n_rounds; p.k_ex = k_ex; p.rk = h->rk;
+        CK(launch_i8_small(p, h->C_local, h->st));
+        CK(launch_merge_copy_best(h->d_copy_best, h->d_snap, h->C_local, h->n, h->d_best,
+                                  h->d_best_spins, h->d_cbest, h->st));
+        h->t += (uint32_t)(n_rounds * k_ex);
+        h->e += (uint32_t)n_rounds;
+        return ISING_OK;
+    }
     if ((h->kernel == KER_GRID_BITS || h->kernel == KER_CSR_BITS) && h->K >= 2 &&
         (h->kernel != KER_GRID_BITS || h->fused_ok)) {
         // one launch: clusters of K/32 CTAs (one copy each) run all rounds on chip
@@ -1519,7 +1547,8 @@ int ising_info(const ising_handle *h, ising_info_t *out)
     out->W_int = h->W_int;
     out->W_f64 = h->W_f;
     out->bands = h->bands;
-    out->fused_pt = (h->kernel == KER_CSR_BITS || (h->kernel == KER_GRID_BITS && h->fused_ok)) && h->K >= 2;
+    out->fused_pt = ((h->kernel == KER_CSR_BITS || (h->kernel == KER_GRID_BITS && h->fused_ok)) && h->K >= 2) ||
+                    small_i8(h);
     return ISING_OK;
 }
 

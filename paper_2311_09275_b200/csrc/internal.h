@@ -126,6 +126,28 @@ struct CsrI8Params {
     RoundKeys rk;
 };
 
+// Fused PT run of a small int8 instance (k_i8_small): one CTA per local copy.
+struct SmallI8Params {
+    int8_t *s;                 // [n][R] internal order (the copy's K columns are contiguous)
+    const int32_t *rp, *col, *wi;  // internal CSR, integer weights
+    const uint32_t *orig;      // internal -> original id
+    const int32_t *class_off;  // [ncol+1]
+    const uint64_t *T;         // [R][qmax+1] per local replica
+    int64_t *E_out, *walker, *copy_best;
+    int8_t *snap;              // [C_local][n] original order
+    const uint64_t *Tx;
+    const int64_t *Tx_off;
+    const int32_t *Tx_len;
+    int32_t n, R, K, qmax, ncol;
+    int64_t slot0;
+    uint32_t t0, e0;
+    int32_t n_rounds, k_ex;
+    RoundKeys rk;
+};
+constexpr int32_t kI8SmallThreads = 512;
+// largest n x K (bytes of one copy's spins) the fused int8 launch keeps in shared memory
+constexpr int64_t kI8SmallMaxBytes = 96 * 1024;
+
 struct ExchangeParams {
     int64_t *E;                // [R_local] (int64 or double bits)
     int64_t *walker;           // [R_local]
@@ -194,6 +216,7 @@ cudaError_t launch_energy_i8(const int8_t *s, const int32_t *rp, const int32_t *
                              cudaStream_t st);
 size_t energy_i8_scratch(int32_t n, int32_t R);
 cudaError_t launch_exchange(const ExchangeParams &p, cudaStream_t st);
+cudaError_t launch_i8_small(const SmallI8Params &p, int32_t C_local, cudaStream_t st);
 cudaError_t launch_merge_copy_best(const int64_t *copy_best, const int8_t *snap, int32_t C_local,
                                    int32_t n, BestDev *best, int8_t *best_spins, int64_t *cbest,
                                    cudaStream_t st);

@@ -880,6 +880,216 @@ cudaError_t launch_csr_i8_phase(const CsrI8Params &p, int32_t threads, cudaStrea
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- fused small int8 PT
+// Small instances with integer weights (C1: a 16x16 torus, 64 slots = 16 KB): one CTA per
+// copy keeps the copy's n x K spins in shared memory for ALL rounds of a PT run -- k_ex
+// sweeps (the k_csr_i8_phase arithmetic: relative-sign integer field, WORD contract, host
+// threshold table), the energies of the K slots, the copy's best-so-far check, the exchange
+// decisions and the configuration swaps -- instead of ~24 launches per
+// round, each a few microseconds of work.  Per-copy best records are merged afterwards by
+// k_merge_copy_best, as for the bit-packed fused launch.
+__global__ void __launch_bounds__(kI8SmallThreads, 1) k_i8_small(const SmallI8Params p)
+{
+    extern __shared__ __align__(16) unsigned char small_smem[];
+    const int K = p.K, n = p.n, tid = threadIdx.x, nt = blockDim.x;
+    const int c = blockIdx.x;  // local copy
+    int8_t *S = reinterpret_cast<int8_t *>(small_smem);                       // [n][K]
+    int64_t *E = reinterpret_cast<int64_t *>(small_smem + (((size_t)n * K + 15) & ~(size_t)15));  // [K]
+    int64_t *W = E + K;                                                         // [K] walker ids
+    const int nparts = nt / K;
+    int64_t *part = W + K;                                                      // [nparts][K]
+    uint64_t *Ts = reinterpret_cast<uint64_t *>(part + (size_t)nparts * K);    // [K][qmax+1]
+    __shared__ uint32_t mswap[8];
+    __shared__ int64_t bestE, bestSlot, bestSweep;
+    __shared__ int32_t kmin, improve;
+    const int64_t slot_c = p.slot0 + (int64_t)c * K;  // global slot of the copy's slot 0
+    const uint32_t c_global = (uint32_t)(slot_c / K);
+    for (int x = tid; x < n * K; x += nt) {
+        const int v = x / K, k = x - v * K;
+        S[x] = p.s[(size_t)v * p.R + (size_t)c * K + k];
+    }
+    for (int k = tid; k < K; k += nt)
+        W[k] = p.walker[(size_t)c * K + k];
+    for (int x = tid; x < K * (p.qmax + 1); x += nt)  // this copy's rows of the threshold table
+        Ts[x] = p.T[(size_t)c * K * (p.qmax + 1) + x];
+    if (tid == 0) {
+        bestE = INT64_MAX;
+        bestSlot = -1;
+        bestSweep = -1;
+    }
+    __syncthreads();
+    const int ng = K / 8;  // 8-replica groups per vertex
+    for (int round = 0; round < p.n_rounds; ++round) {
+        for (int sw = 0; sw < p.k_ex; ++sw) {
+            const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + sw);
+            for (int cl = 0; cl < p.ncol; ++cl) {
+                const int v0 = p.class_off[cl], nvc = p.class_off[cl + 1] - v0;
+                for (int task = tid; task < nvc * ng; task += nt) {
+                    const int v = v0 + task / ng, o = task - (task / ng) * ng;
+                    uint2 *own_p = reinterpret_cast<uint2 *>(S + (size_t)v * K + 8 * o);
+                    const uint2 own = *own_p;
+                    int32_t sh[8];
+#pragma unroll
+                    for (int b = 0; b < 8; ++b)
+                        sh[b] = 0;
+                    for (int e = __ldg(p.rp + v); e < __ldg(p.rp + v + 1); ++e) {
+                        const uint2 nb = *reinterpret_cast<const uint2 *>(S + (size_t)__ldg(p.col + e) * K + 8 * o);
+                        const int32_t w = __ldg(p.wi + e);
+                        const uint32_t x0 = own.x ^ nb.x, x1 = own.y ^ nb.y;
+#pragma unroll
+                        for (int b = 0; b < 8; ++b) {
+                            const uint32_t word = b < 4 ? x0 : x1;
+                            const int32_t m = (int32_t)(word << (24 - 8 * (b & 3))) >> 31;  // -1 iff s_i != s_j
+                            sh[b] += (w ^ m) - m;
+                        }
+                    }
+                    const uint32_t io = __ldg(p.orig + v);
+                    const uint32_t g = (uint32_t)(slot_c >> 3) + (uint32_t)o;
+                    const uint4 h = philox(io, t, g, ST_WORD_HI << 24, p.rk);
+                    const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+                    uint32_t fm0 = 0u, fm1 = 0u;
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        bool acc = sh[b] >= 0;  // dE = -2 s h <= 0
+                        if (!acc) {
+                            const uint32_t hb = (b & 1) ? (hw[b >> 1] >> 16) : (hw[b >> 1] & 0xFFFFu);
+                            const uint64_t T = Ts[(size_t)(8 * o + b) * (p.qmax + 1) + (uint32_t)(-sh[b])];
+                            acc = exact_less(hb, T, io, t, (uint32_t)(slot_c + 8 * o + b), p.rk);
+                        }
+                        if (acc) {
+                            if (b < 4)
+                                fm0 |= 0xFEu << (8 * (b & 3));
+                            else
+                                fm1 |= 0xFEu << (8 * (b & 3));
+                        }
+                    }
+                    *own_p = make_uint2(own.x ^ fm0, own.y ^ fm1);
+                }
+                __syncthreads();
+            }
+        }
+        // energies of the K slots: each edge once (from its lower internal endpoint)
+        {
+            const int k = tid % K, pt = tid / K;
+            int64_t acc = 0;
+            if (pt < nparts)
+                for (int v = pt; v < n; v += nparts) {
+                    const int32_t sv = S[(size_t)v * K + k];
+                    for (int e = __ldg(p.rp + v); e < __ldg(p.rp + v + 1); ++e) {
+                        const int j = __ldg(p.col + e);
+                        if (j > v)
+                            acc += (int64_t)__ldg(p.wi + e) * sv * S[(size_t)j * K + k];
+                    }
+                }
+            if (pt < nparts)
+                part[pt * K + k] = acc;
+            __syncthreads();
+            for (int kk = tid; kk < K; kk += nt) {
+                int64_t e = 0;
+                for (int q = 0; q < nparts; ++q)
+                    e += part[q * K + kk];
+                E[kk] = e;
+            }
+            if (tid < 8)
+                mswap[tid] = 0u;
+            __syncthreads();
+        }
+        const uint32_t t_now = p.t0 + (uint32_t)((round + 1) * p.k_ex);
+        const uint32_t e_now = p.e0 + (uint32_t)round;
+        if (tid < 32) {  // the copy's best-so-far: argmin, ties -> lowest slot; strict <
+            int64_t bE = INT64_MAX;
+            int bk = -1;
+            for (int k = tid; k < K; k += 32)
+                if (bk < 0 || E[k] < bE) {
+                    bE = E[k];
+                    bk = k;
+                }
+            for (int off = 16; off > 0; off >>= 1) {
+                const int64_t oE = __shfl_down_sync(0xFFFFFFFFu, bE, off);
+                const int ok = __shfl_down_sync(0xFFFFFFFFu, bk, off);
+                if (ok >= 0 && (bk < 0 || oE < bE || (oE == bE && ok < bk))) {
+                    bE = oE;
+                    bk = ok;
+                }
+            }
+            if (tid == 0) {
+                improve = bE < bestE;
+                kmin = bk;
+                if (bE < bestE) {
+                    bestE = bE;
+                    bestSlot = slot_c + bk;
+                    bestSweep = t_now;
+                }
+            }
+        }
+        __syncthreads();
+        if (improve)
+            for (int v = tid; v < n; v += nt)
+                p.snap[(size_t)c * n + __ldg(p.orig + v)] = S[(size_t)v * K + kmin];
+        // exchange e_now: pairs (k, k+1), k = e % 2 + 2 j (identical rule to k_exchange)
+        const int par = (int)(e_now & 1u);
+        for (int k = par + 2 * tid; k + 1 < K; k += 2 * nt) {
+            const int64_t d = E[k + 1] - E[k];
+            bool accept = d >= 0;
+            if (!accept) {
+                const int64_t j = -d - 1;
+                if (j < __ldg(p.Tx_len + k)) {
+                    const uint4 w = philox((uint32_t)k, e_now, c_global, ST_EXCH << 24, p.rk);
+                    const uint64_t Ux = ((uint64_t)w.x << 32) | (uint64_t)w.y;
+                    accept = Ux < __ldg(p.Tx + __ldg(p.Tx_off + k) + j);
+                }
+            }
+            if (accept) {
+                atomicOr(&mswap[k >> 5], 1u << (k & 31));
+                const int64_t te = E[k];
+                E[k] = E[k + 1];
+                E[k + 1] = te;
+                const int64_t tw = W[k];
+                W[k] = W[k + 1];
+                W[k + 1] = tw;
+            }
+        }
+        __syncthreads();
+        // configurations of accepted pairs trade places (the slot temperatures stay)
+        const int npair = (K - par) / 2;
+        for (int x = tid; x < n * npair; x += nt) {
+            const int v = x / npair, k = par + 2 * (x - v * npair);
+            if ((mswap[k >> 5] >> (k & 31)) & 1u) {
+                int8_t *a = S + (size_t)v * K + k;
+                const int8_t ta = a[0];
+                a[0] = a[1];
+                a[1] = ta;
+            }
+        }
+        __syncthreads();
+    }
+    for (int x = tid; x < n * K; x += nt) {
+        const int v = x / K, k = x - v * K;
+        p.s[(size_t)v * p.R + (size_t)c * K + k] = S[x];
+    }
+    for (int k = tid; k < K; k += nt) {
+        p.E_out[(size_t)c * K + k] = E[k];
+        p.walker[(size_t)c * K + k] = W[k];
+    }
+    if (tid == 0) {
+        p.copy_best[3 * c + 0] = bestE;
+        p.copy_best[3 * c + 1] = bestSlot;
+        p.copy_best[3 * c + 2] = bestSweep;
+    }
+}
+
+cudaError_t launch_i8_small(const SmallI8Params &p, int32_t C_local, cudaStream_t st)
+{
+    const int nparts = kI8SmallThreads / p.K;
+    const size_t smem = (((size_t)p.n * p.K + 15) & ~(size_t)15) + (size_t)(2 + nparts) * p.K * 8 +
+                        (size_t)p.K * (p.qmax + 1) * 8;
+    cudaError_t e = cudaFuncSetAttribute(k_i8_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return e;
+    k_i8_small<<<C_local, kI8SmallThreads, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- a6: energy
 // E_r = sum over edges {v, j}, j > v (internal ids; each edge once) of
 // w s_v s_j.  Two passes with a fixed reduction order (deterministic for

@@ -247,6 +247,28 @@ def test_int8_general_integer_weights_parity():
     compare_copies(eng, o)
 
 
+@pytest.mark.parametrize("n,m,K,C,sweeps,kex", [(300, 700, 128, 2, 47, 10), (96, 200, 8, 5, 30, 3)])
+def test_int8_fused_small_pt_parity(n, m, K, C, sweeps, kex):
+    """k_i8_small (one launch for all rounds, one CTA per copy) == per-round launches == oracle:
+    spins, energies, walkers, best record and per-copy best, with a tail of sweeps."""
+    u, v = synth.gnm(n, m, n + m)
+    w = (synth._below(synth.splitmix64(n, u.size), 5) - 2).astype(np.int32)
+    w[w == 0] = 3
+    rp, col, ww = synth.edges_to_csr(n, u, v, w)
+    inst = dict(kind="csr", n=n, row_ptr=rp, col=col, w=ww.astype(np.int32))
+    betas = synth.beta_ladder(K)
+    a = Engine(inst, K, C, betas, seed=KEY, layout="i8")
+    assert a.info.fused_pt == 1
+    run_pt(a, sweeps, kex, fused=True)
+    b = Engine(inst, K, C, betas, seed=KEY, layout="i8")
+    run_pt(b, sweeps, kex, fused=False)
+    o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=oracle.RNG_WORD).run(sweeps, kex)
+    compare_copies(a, o)
+    compare_copies(b, o)
+    for x, y in zip(a.copy_best(), b.copy_best()):
+        assert np.array_equal(x, y)
+
+
 def _regular_inst(n, seed):
     u, v = synth.random_regular(n, 3, seed)
     w = synth.gaussian_f32(u.size, seed + 5)

@@ -121,3 +121,16 @@ def test_no_cpu_fallback_without_gpu():
     Jr, Jd = synth.torus_pm1(8, 8, 1)
     c, msg = _code(L.ising_create_grid, 8, 8, Jr, Jd, **_desc())
     assert c in (L.ISING_E_CUDA, L.ISING_E_OOM)
+
+
+def test_grid_band_override_is_validated(monkeypatch):
+    """ISING_GRID_BANDS (torus band split) accepts only 1 or 2, and 2 only
+    where the fused PT clusters stay within 8 CTAs (n_temps <= 128); checked before any
+    device work, so it fails the same way with or without a GPU."""
+    Jr, Jd = synth.torus_pm1(8, 8, 1)
+    monkeypatch.setenv("ISING_GRID_BANDS", "3")
+    c, msg = _code(L.ising_create_grid, 8, 8, Jr, Jd, **_desc())
+    assert c == L.ISING_E_ARG and "ISING_GRID_BANDS" in msg
+    monkeypatch.setenv("ISING_GRID_BANDS", "2")
+    c, msg = _code(L.ising_create_grid, 8, 8, Jr, Jd, **_desc(n_temps=256, betas=synth.beta_ladder(256)))
+    assert c == L.ISING_E_UNSUPPORTED and "ISING_GRID_BANDS" in msg
