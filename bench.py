@@ -213,7 +213,8 @@ def run_reference(args):
         "impl": "reference", "metric": "spin-flip attempts/s", "value": v, "unit": "attempts/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": float(np.median([r["seconds"] for r in vals]) * 1e3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.workload in STRONG else "weak",
+        "vs_baseline": None,
         "dtype": "int8 spins / int64 energies (scalar C)", "data": "synthetic",
         "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
                    "note": "CPU oracle on host cores, bounded sample per step"},
