@@ -158,9 +158,13 @@ ISING_API int ising_cut(ising_handle *h, void *out);
 
 /* n_rounds x (k_ex sweeps, then ising_exchange) in as few launches as possible (async).
  * Identical results to calling ising_sweep(h, k_ex); ising_exchange(h) n_rounds times.
- * Bit-packed tori run the whole sequence in ONE launch: clusters of K/32 CTAs (one copy
- * each) keep the copy on chip and exchange energies and boundary bit planes through
- * distributed shared memory.  Errors: ISING_E_UNSUPPORTED for float weights. */
+ * Bit-packed layouts run the whole sequence in ONE launch: clusters of K/32 CTAs (one copy
+ * each; K/32 x 2 for the band-split torus kernel) keep the copy on chip and exchange
+ * energies and boundary bit planes through distributed shared memory -- unless those
+ * clusters would not all be resident at once, in which case the rounds run as per-round
+ * launches.  Small int8 instances with integer weights (n*K <= 96 KB per copy) also run in
+ * ONE launch (one CTA per copy).  ising_info.fused_pt says which.  Errors:
+ * ISING_E_UNSUPPORTED for float weights. */
 ISING_API int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex);
 
 /* Local PT step (async, single process): best-so-far check over the local slots,
