@@ -76,3 +76,39 @@ def test_two_ranks_on_library_equal_oracle(kind, layout, gather):
     assert np.array_equal(W, ref.walker)
     for r in recs:  # every rank reports the same global record
         assert (r[0], r[1], r[2]) == (ref.best.E, ref.best.slot, ref.best.sweep)
+
+
+def _nccl_worker(rank, world, port, out):
+    from paper_2311_09275_b200 import Engine
+    from paper_2311_09275_b200.driver import all_gather
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", 0))
+    inst = _inst("grid")
+    eng = Engine(inst, K, C, synth.beta_ladder(K), seed=KEY, layout="bits")
+    send, recv = eng.record_buffers(world)
+    for _ in range(4):  # north-star round: sweeps, NCCL all-gather of the records, exchange
+        eng.sweep(10)
+        eng.exchange_begin(send)
+        all_gather(recv, send, None)
+        eng.exchange_end(recv)
+    torch.cuda.synchronize()
+    np.save(os.path.join(out, "E.npy"), eng.energies())
+    np.save(os.path.join(out, "W.npy"), eng.walkers())
+    b = eng.best(spins=False)
+    np.save(os.path.join(out, "rec.npy"), np.array([b["E"], b["slot"], b["sweep"]]))
+    dist.destroy_process_group()
+
+
+def test_nccl_record_gather_single_rank():
+    """The NCCL branch of the record all-gather (all_gather_into_tensor on device buffers)
+    feeding ising_exchange_end, on one rank: equal to the oracle's local exchanges."""
+    with tempfile.TemporaryDirectory() as out:
+        mp.spawn(_nccl_worker, args=(1, _free_port(), out), nprocs=1, join=True)
+        E = np.load(os.path.join(out, "E.npy"))
+        W = np.load(os.path.join(out, "W.npy"))
+        rec = np.load(os.path.join(out, "rec.npy"))
+    ref = oracle.Oracle(_inst("grid"), K, synth.beta_ladder(K), KEY, 0, C, rng=oracle.RNG_PLANE).run(40, 10)
+    assert np.array_equal(E, ref.energies())
+    assert np.array_equal(W, ref.walker)
+    assert (rec[0], rec[1], rec[2]) == (ref.best.E, ref.best.slot, ref.best.sweep)
