@@ -113,7 +113,8 @@ typedef struct {
     int64_t W_int;        /* sum of weights (integer weights) */
     double W_f64;         /* sum of weights (float weights, float64 sum in edge order) */
     int32_t bands;        /* grid BITS: rows of a word group split over this many CTAs (1 or 2) */
-    int32_t fused_pt;     /* 1 if ising_run runs all rounds in one launch (BITS kernels) */
+    int32_t fused_pt;     /* 1 if ising_run runs all rounds in one launch; 2: one cooperative launch
+                             whose copies span K/32 clusters (band split); 0: per-round launches */
 } ising_info_t;
 
 /* Create from a periodic Lx x Ly grid (torus).  Site i = x + Lx*y; J_right[i]

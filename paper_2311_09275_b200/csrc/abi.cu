@@ -101,6 +101,9 @@ struct ising_handle {
     int32_t ell_deg = 0;  // I8: width of the padded neighbour table (0 = CSR path)
     int32_t bands = 1;    // grid BITS: row bands per word group (CTA pairs with DSMEM halos)
     bool fused_ok = true; // grid BITS: the fused PT launch's clusters (K/32 x bands CTAs per copy) fit one wave
+    bool xc_ok = false;   // grid BITS, 2 bands: cooperative fused launch with copies over K/32 clusters
+    int64_t *d_xc_E = nullptr;
+    uint32_t *d_xc_B = nullptr, *d_xc_bar = nullptr;
     std::vector<int32_t> class_off;
     // device buffers
     uint32_t *d_state[2] = {nullptr, nullptr};
@@ -347,6 +350,10 @@ GridBitsParams grid_params(ising_handle *h, int32_t n_rounds, int32_t k_ex, bool
     p.Tx_len = h->d_Tx_len;
     p.rk = h->rk;
     p.bands = h->bands;
+    p.xc = 0;
+    p.xc_E = h->d_xc_E;
+    p.xc_B = h->d_xc_B;
+    p.xc_bar = h->d_xc_bar;
     return p;
 }
 
@@ -1050,6 +1057,15 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
     if (h->bands > 1 && h->K >= 2) {
         CK(cudaSetDevice(h->device));
         h->fused_ok = grid_bands_max_clusters(h->wpc * h->bands, h->threads, h->smem) >= h->C_local;
+        // otherwise one copy spans K/32 clusters of 2 (the band pairs) that meet at global-memory
+        // copy barriers: needs every cluster resident (cooperative launch)
+        if (!h->fused_ok && grid_bands_max_clusters(2, h->threads, h->smem) >= h->G) {
+            const size_t nbw = ((size_t)n + 31) / 32;
+            CK(h->alloc(&h->d_xc_E, (size_t)h->C_local * 2 * h->K));
+            CK(h->alloc(&h->d_xc_B, (size_t)h->C_local * 2 * h->wpc * 4 * nbw));
+            CK(h->alloc(&h->d_xc_bar, (size_t)h->C_local));
+            h->xc_ok = true;
+        }
     }
     // J bytes in colour-separated order: bit 0..3 = (right, left, down, up) bond has J = -1
     std::vector<uint8_t> jb(n);
@@ -1230,7 +1246,18 @@ int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
         h->e += (uint32_t)n_rounds;
         return ISING_OK;
     }
-    if ((h->kernel == KER_GRID_BITS || h->kernel == KER_CSR_BITS) && h->K >= 2 &&
+    if (h->kernel == KER_GRID_BITS && h->K >= 2 && !h->fused_ok && h->xc_ok) {
+        GridBitsParams p = grid_params(h, n_rounds, k_ex, true);
+        p.xc = 1;
+        CK(launch_grid(h, p));
+        h->cur ^= 1;
+        CK(launch_merge_copy_best(h->d_copy_best, h->d_snap, h->C_local, h->n, h->d_best,
+                                  h->d_best_spins, h->d_cbest, h->st));
+        h->t += (uint32_t)(n_rounds * k_ex);
+        h->e += (uint32_t)n_rounds;
+        return ISING_OK;
+    }
+    if ((h->kernel == KER_CSR_BITS || h->kernel == KER_GRID_BITS) && h->K >= 2 &&
         (h->kernel != KER_GRID_BITS || h->fused_ok)) {
         // one launch: clusters of K/32 CTAs (one copy each) run all rounds on chip
         if (h->kernel == KER_GRID_BITS)
@@ -1549,6 +1576,8 @@ int ising_info(const ising_handle *h, ising_info_t *out)
     out->bands = h->bands;
     out->fused_pt = ((h->kernel == KER_CSR_BITS || (h->kernel == KER_GRID_BITS && h->fused_ok)) && h->K >= 2) ||
                     small_i8(h);
+    if (h->kernel == KER_GRID_BITS && h->K >= 2 && !h->fused_ok && h->xc_ok)
+        out->fused_pt = 2;  // one cooperative launch; each copy spans K/32 clusters
     return ISING_OK;
 }
 

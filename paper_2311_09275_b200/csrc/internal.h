@@ -74,6 +74,12 @@ struct GridBitsParams {
     const int32_t *Tx_len;
     RoundKeys rk;
     int32_t bands;             // row bands per word group (1, or 2: CTA pairs with DSMEM halo rows)
+    // band split with a copy spread over K/32 clusters of 2 (cooperative launch): the PT
+    // step exchanges energies and boundary bit planes through global memory
+    int32_t xc;
+    int64_t *xc_E;             // [C_local][2][K] word types' energies, by round parity
+    uint32_t *xc_B;            // [C_local][2][K/32][2 bands][2 planes][nbw], by round parity
+    uint32_t *xc_bar;          // [C_local] copy barrier counters (zero at launch)
 };
 
 struct CsrBitsParams {

@@ -94,6 +94,148 @@ __device__ __forceinline__ void site_unsat(const uint32_t *S, const uint8_t *JB,
 
 constexpr int kGridQItem = 16;  // tail-queue item, as k_grid_bits
 
+// Copy-wide barrier over the copy's clusters through a global counter (the launch is
+// cooperative, so every CTA of the grid is resident and the spin cannot deadlock).
+__device__ __forceinline__ void copy_barrier(uint32_t *bar, uint32_t target)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        uint32_t v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < target);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// PT step of a copy spread over K/32 clusters (one per word type, each the CTA pair of the
+// two bands): as bits::pt_step, with the word types' energies and boundary bit planes passed
+// through global memory (double-buffered by round parity) between copy barriers.
+template <class Snap>
+__device__ void pt_step_xc(PtShared &ps, const int32_t *Ucnt, int64_t m_edges, uint32_t *S, int n,
+                           uint32_t *B0, uint32_t *B31, int KW, int wt, int band, uint32_t c_global,
+                           uint32_t t_now, uint32_t e_now, int round, const GridBitsParams &p, int c_local,
+                           uint32_t &bar_target, Snap snap)
+{
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int K = 32 * KW;
+    const int nbw = (n + 31) / 32;
+    const int par_r = round & 1;
+    int64_t *Eg = p.xc_E + ((size_t)c_local * 2 + par_r) * K;
+    uint32_t *Bg = p.xc_B + ((size_t)c_local * 2 + par_r) * (size_t)KW * 4 * nbw;
+    uint32_t *bar = p.xc_bar + c_local;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();  // both bands' counts complete
+    if (band == 0 && tid < 32) {
+        const int32_t u = Ucnt[tid] + cl.map_shared_rank(Ucnt, cl.block_rank() + 1u)[tid];
+        Eg[32 * wt + tid] = 2 * (int64_t)u - m_edges;
+    }
+    bar_target += 2u * (uint32_t)KW;
+    copy_barrier(bar, bar_target);
+    for (int k = tid; k < K; k += nt)
+        ps.Ecopy[k] = __ldcg(Eg + k);
+    for (int q = tid; q < KW; q += nt)
+        ps.Mswap[q] = 0u;
+    __syncthreads();
+    if (warp == 0) {  // best-so-far of the copy: argmin, ties -> lowest slot
+        int64_t bE = INT64_MAX;
+        int bk = -1;
+        for (int k = lane; k < K; k += 32)
+            if (bk < 0 || ps.Ecopy[k] < bE) {
+                bE = ps.Ecopy[k];
+                bk = k;
+            }
+        for (int o = 16; o > 0; o >>= 1) {
+            const int64_t oE = __shfl_down_sync(0xFFFFFFFFu, bE, o);
+            const int ok = __shfl_down_sync(0xFFFFFFFFu, bk, o);
+            if (ok >= 0 && (bk < 0 || oE < bE || (oE == bE && ok < bk))) {
+                bE = oE;
+                bk = ok;
+            }
+        }
+        if (lane == 0) {
+            ps.improve = bE < ps.bestE;
+            ps.kmin = bk;
+            if (bE < ps.bestE) {
+                ps.bestE = bE;
+                ps.bestSlot = (int64_t)c_global * K + bk;
+                ps.bestSweep = t_now;
+            }
+        }
+    }
+    __syncthreads();
+    if (ps.improve && (ps.kmin >> 5) == wt)
+        snap(ps.kmin & 31);
+    const int par = (int)(e_now & 1u);
+    const int npairs = (K - par) / 2;
+    for (int pi = tid; pi < npairs; pi += nt) {
+        const int k = par + 2 * pi;
+        const int64_t d = ps.Ecopy[k + 1] - ps.Ecopy[k];
+        bool accept = d >= 0;
+        if (!accept) {
+            const int64_t j = -d - 1;
+            if (j < p.Tx_len[k]) {
+                const uint4 w = philox((uint32_t)k, e_now, c_global, ST_EXCH << 24, p.rk);
+                const uint64_t Ux = ((uint64_t)w.x << 32) | (uint64_t)w.y;
+                accept = Ux < p.Tx[p.Tx_off[k] + j];
+            }
+        }
+        if (accept) {
+            atomicOr(&ps.Mswap[k >> 5], 1u << (k & 31));
+            const int64_t te = ps.Ecopy[k];
+            ps.Ecopy[k] = ps.Ecopy[k + 1];
+            ps.Ecopy[k + 1] = te;
+            const int64_t tw = ps.Wcopy[k];
+            ps.Wcopy[k] = ps.Wcopy[k + 1];
+            ps.Wcopy[k + 1] = tw;
+        }
+    }
+    __syncthreads();
+    const uint32_t Min = ps.Mswap[wt] & 0x7FFFFFFFu;
+    const bool cross_lo = wt > 0 && ((ps.Mswap[wt - 1] >> 31) & 1u);
+    const bool cross_hi = wt + 1 < KW && ((ps.Mswap[wt] >> 31) & 1u);
+    bool any_cross = false;
+    for (int q = 0; q + 1 < KW; ++q)
+        any_cross |= (ps.Mswap[q] >> 31) & 1u;
+    if (any_cross) {  // uniform over the copy
+        uint32_t *mine = Bg + ((size_t)wt * 2 + band) * 2 * nbw;
+        for (int b = warp * 32; b < nbw * 32; b += nt) {
+            const int l = b + lane;
+            const uint32_t w = l < n ? S[l] : 0u;
+            const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, w & 1u);
+            const uint32_t b31 = __ballot_sync(0xFFFFFFFFu, w >> 31);
+            if (lane == 0) {
+                mine[b >> 5] = b0;
+                mine[nbw + (b >> 5)] = b31;
+            }
+        }
+        bar_target += 2u * (uint32_t)KW;
+        copy_barrier(bar, bar_target);
+        const uint32_t *nB31 = Bg + ((size_t)(wt - 1) * 2 + band) * 2 * nbw + nbw;  // used iff cross_lo
+        const uint32_t *nB0 = Bg + ((size_t)(wt + 1) * 2 + band) * 2 * nbw;         // used iff cross_hi
+        for (int l = tid; l < n; l += nt) {
+            uint32_t w = S[l];
+            const uint32_t tt = (w ^ (w >> 1)) & Min;
+            w ^= tt ^ (tt << 1);
+            if (cross_lo)
+                w = (w & ~1u) | ((__ldcg(nB31 + (l >> 5)) >> (l & 31)) & 1u);
+            if (cross_hi)
+                w = (w & 0x7FFFFFFFu) | (((__ldcg(nB0 + (l >> 5)) >> (l & 31)) & 1u) << 31);
+            S[l] = w;
+        }
+    } else if (Min) {
+        for (int l = tid; l < n; l += nt) {
+            const uint32_t w = S[l];
+            const uint32_t tt = (w ^ (w >> 1)) & Min;
+            S[l] = w ^ tt ^ (tt << 1);
+        }
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBitsParams p)
 {
     extern __shared__ __align__(16) uint32_t sm[];
@@ -167,6 +309,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBit
         pt_init(ps, p.walker, c_local, K);
     __syncthreads();
 
+    uint32_t bar_target = 0;  // xc mode: the copy barrier's count after the next arrival
     for (int round = 0; round < p.n_rounds; ++round) {
         // ---- k_ex sweeps
         for (int s = 0; s < p.k_ex; ++s) {
@@ -375,9 +518,14 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBit
                 dst[i] = ((S[((x + y) & 1) * G.half + y * G.hx + (x >> 1)] >> bit) & 1u) ? -1 : 1;
             }
         };
-        pt_step<NB>(ps, Ucnt, 2 * (int64_t)n, S, n, B0, B31, KW, wt, c_global,
-                p.t0 + (uint32_t)((round + 1) * p.k_ex), p.e0 + (uint32_t)round, p.Tx, p.Tx_off,
-                p.Tx_len, p.rk, snap, band);
+        if (p.xc)
+            pt_step_xc(ps, Ucnt, 2 * (int64_t)n, S, n, B0, B31, KW, wt, band, c_global,
+                       p.t0 + (uint32_t)((round + 1) * p.k_ex), p.e0 + (uint32_t)round, round, p, c_local,
+                       bar_target, snap);
+        else
+            pt_step<NB>(ps, Ucnt, 2 * (int64_t)n, S, n, B0, B31, KW, wt, c_global,
+                        p.t0 + (uint32_t)((round + 1) * p.k_ex), p.e0 + (uint32_t)round, p.Tx, p.Tx_off,
+                        p.Tx_len, p.rk, snap, band);
     }
 
     // ---- outputs
@@ -440,13 +588,20 @@ cudaError_t launch_grid_bands(const GridBitsParams &p, int32_t G, int32_t thread
     cfg.blockDim = dim3((unsigned)threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (p.pt ? (unsigned)p.words_per_copy : 1u) * 2u;
+    attr[0].val.clusterDim.x = (p.pt && !p.xc ? (unsigned)p.words_per_copy : 1u) * 2u;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;  // xc: copy barriers need every CTA resident
+    attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = p.pt && p.xc ? 2 : 1;
+    if (p.pt && p.xc) {
+        e = cudaMemsetAsync(p.xc_bar, 0, (size_t)(G / p.words_per_copy) * sizeof(uint32_t), st);
+        if (e != cudaSuccess)
+            return e;
+    }
     return cudaLaunchKernelEx(&cfg, k_grid_bands, p);
 }
 

@@ -172,6 +172,33 @@ def test_c4b_eight_gpu_share_band_split():
         compare_copies(eng, o, check_best=False)
 
 
+def test_band_split_multicluster_pt_parity(monkeypatch):
+    """36 copies of K = 64 on a 100x100 torus (one CTA per SM): 72 word groups -> band split
+    (144 CTAs); the copies' clusters of 4 CTAs do not all fit at once (33 on a B200), so
+    ising_run uses ONE cooperative launch whose copies span 2 clusters (band pairs) meeting at
+    global-memory copy barriers (ising_info.fused_pt == 2).  Sampled copies equal the oracle
+    and every copy equals the single-band fused launch, bit for bit."""
+    inst = grid(100, 100, 2024)
+    K, C, sweeps, kex = 64, 36, 20, 10
+    betas = synth.beta_ladder(K)
+    eng = Engine(inst, K, C, betas, seed=KEY, layout="bits")
+    assert eng.info.bands == 2 and eng.info.fused_pt == 2
+    run_pt(eng, sweeps, kex)
+    for c0 in (0, 17, 35):
+        o = oracle.Oracle(inst, K, betas, KEY, c0, c0 + 1, rng=oracle.RNG_PLANE).run(sweeps, kex)
+        compare_copies(eng, o, check_best=False)
+    monkeypatch.setenv("ISING_GRID_BANDS", "1")
+    one = Engine(inst, K, C, betas, seed=KEY, layout="bits")
+    run_pt(one, sweeps, kex)
+    assert np.array_equal(one.energies(), eng.energies())
+    assert np.array_equal(one.walkers(), eng.walkers())
+    for x, y in zip(one.copy_best(), eng.copy_best()):
+        assert np.array_equal(x, y)
+    b1, b2 = one.best(), eng.best()
+    assert (b1["E"], b1["slot"], b1["sweep"]) == (b2["E"], b2["slot"], b2["sweep"])
+    assert np.array_equal(b1["spins"], b2["spins"])
+
+
 def test_grid_kernel_equals_csr_kernel_on_torus():
     inst = grid(12, 8, 3)
     rp, col, w = synth.torus_csr(12, 8, inst["J_right"], inst["J_down"])
