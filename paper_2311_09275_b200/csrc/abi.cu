@@ -22,9 +22,17 @@
 
 #include "internal.h"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges for nsys / ncu --nvtx (SURVEY.md §5 tracing)
+
 using namespace ising;
 
 namespace {
+
+// NVTX range for the lifetime of a scope (no-op unless a tool is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 thread_local std::string g_err;
 
@@ -942,6 +950,7 @@ int ising_greedy_colour_sl(int32_t n, const int64_t *row_ptr, const int32_t *col
 int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_t *J_down,
                       const ising_run_desc *desc, ising_handle **out)
 {
+    NvtxRange nvtx_range("ising_create_grid");
     g_err.clear();
     if (!out)
         return fail(ISING_E_ARG, "out is NULL");
@@ -1119,6 +1128,7 @@ int ising_create_csr(int32_t n, const int64_t *row_ptr, const int32_t *col, cons
                      int32_t wtype, const int32_t *colour, const ising_run_desc *desc,
                      ising_handle **out)
 {
+    NvtxRange nvtx_range("ising_create_csr");
     g_err.clear();
     if (!out)
         return fail(ISING_E_ARG, "out is NULL");
@@ -1176,6 +1186,7 @@ int ising_create_csr(int32_t n, const int64_t *row_ptr, const int32_t *col, cons
 
 int ising_sweep(ising_handle *h, int32_t n_sweeps)
 {
+    NvtxRange nvtx_range("ising_sweep");
     int rc = check_handle(h);
     if (rc)
         return rc;
@@ -1220,6 +1231,7 @@ int ising_cut(ising_handle *h, void *out)
 
 int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
 {
+    NvtxRange nvtx_range("ising_run");
     int rc = check_handle(h);
     if (rc)
         return rc;
@@ -1284,6 +1296,7 @@ int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
 
 int ising_anneal(ising_handle *h, int32_t n_sweeps, const double *sched)
 {
+    NvtxRange nvtx_range("ising_anneal");
     int rc = check_handle(h);
     if (rc)
         return rc;
@@ -1366,6 +1379,7 @@ int ising_anneal(ising_handle *h, int32_t n_sweeps, const double *sched)
 
 int ising_icm(ising_handle *h, int32_t k_min)
 {
+    NvtxRange nvtx_range("ising_icm");
     int rc = check_handle(h);
     if (rc)
         return rc;
@@ -1402,6 +1416,7 @@ int ising_icm(ising_handle *h, int32_t k_min)
 
 int ising_exchange(ising_handle *h)
 {
+    NvtxRange nvtx_range("ising_exchange");
     int rc = check_handle(h);
     if (rc)
         return rc;
@@ -1410,6 +1425,7 @@ int ising_exchange(ising_handle *h)
 
 int ising_exchange_begin(ising_handle *h, void *dev_send)
 {
+    NvtxRange nvtx_range("ising_exchange_begin");
     int rc = check_handle(h);
     if (rc)
         return rc;
@@ -1421,6 +1437,7 @@ int ising_exchange_begin(ising_handle *h, void *dev_send)
 
 int ising_exchange_end(ising_handle *h, const void *dev_recv, int64_t n_records)
 {
+    NvtxRange nvtx_range("ising_exchange_end");
     int rc = check_handle(h);
     if (rc)
         return rc;

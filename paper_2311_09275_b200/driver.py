@@ -166,7 +166,9 @@ def all_gather(recv, send, group=None):
     import torch
     import torch.distributed as dist
     if dist.get_backend(group) == "nccl":
+        torch.cuda.nvtx.range_push("record_all_gather")  # NVTX, next to the library's ranges
         dist.all_gather_into_tensor(recv, send, group=group)
+        torch.cuda.nvtx.range_pop()
         return
     world = dist.get_world_size(group)
     host = send.device.type != "cpu"  # gloo: gather host copies of device records
