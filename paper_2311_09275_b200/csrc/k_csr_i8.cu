@@ -766,34 +766,43 @@ __global__ void __launch_bounds__(256, 3) k_csr_i8_ring(const CsrI8Params p, uin
         sl_iss += kSlot;
         e_iss += kRingEntry;
     }
-    uint32_t sl_cur = ring0;  // ring slot of the vertex decided now
-    uint32_t e_cur = meta0;   // its table entry
-    for (uint32_t j = 0; j < cnt; ++j) {
-        if ((j & 31u) == 0) {
-            __syncwarp();  // every lane is done with the buffer this block overwrites
-            meta_issue((j >> 5) + 1);
-        }
-        if (j + S - 1 < cnt)
-            rows_issue(j + S - 1, sl_iss, e_iss);
-        cp_commit();
-        sl_iss = sl_iss + kSlot == ring0 + kRing ? ring0 : sl_iss + kSlot;
-        e_iss = next_entry(e_iss);
-        cp_wait<S - 1>();
-        // the table block issued at the start of this 32-vertex block is complete from here on
-        // (S - 1 steps later); one __syncwarp makes every lane's part visible to all lanes
-        if ((j & 31u) == S - 1)
-            __syncwarp();
-        I8Rows<DEG> r;
-        r.own = lds64(sl_cur);
+    // main loop, unrolled by S: the ring slot of vertex j is j % S (a constant per unrolled
+    // step), and its table entry is j % 64 of the circular list (S divides 32, so a group of S
+    // vertices never straddles the wrap of the decide-side entry pointer)
+    static_assert(32 % S == 0, "ring depth must divide the 32-vertex table block");
+    (void)sl_iss;
+    (void)e_iss;
+    uint32_t e_cur = meta0;  // table entry of vertex jb
+    for (uint32_t jb = 0; jb < cnt; jb += S) {
 #pragma unroll
-        for (int u = 0; u < DEG; ++u)
-            r.nb[u] = lds64(sl_cur + (u + 1) * 256u);
-        sl_cur = sl_cur + kSlot == ring0 + kRing ? ring0 : sl_cur + kSlot;
-        I8Meta m;
-        m.w = lds128(e_cur + 16u);
-        m.io = lds32(e_cur + 32u);
-        e_cur = next_entry(e_cur);
-        pipe_decide<DEG>(p, r, m, vb + j, tbb, rwb, bl, ph, g0, o, c4b);
+        for (uint32_t u = 0; u < S; ++u) {
+            const uint32_t j = jb + u;
+            if (j >= cnt)
+                break;
+            if (u == 0 && (jb & 31u) == 0) {
+                __syncwarp();  // every lane is done with the buffer this block overwrites
+                meta_issue((j >> 5) + 1);
+            }
+            if (j + S - 1 < cnt)
+                rows_issue(j + S - 1, ring0 + ((u + S - 1) % S) * kSlot, meta0 + ((j + S - 1) & 63u) * kRingEntry);
+            cp_commit();
+            cp_wait<S - 1>();
+            // the table block issued at the start of this 32-vertex block is complete from here on
+            // (S - 1 steps later); one __syncwarp makes every lane's part visible to all lanes
+            if (u == S - 1 && (jb & 31u) == 0)
+                __syncwarp();
+            I8Rows<DEG> r;
+            const uint32_t sl = ring0 + u * kSlot;
+            r.own = lds64(sl);
+#pragma unroll
+            for (int q = 0; q < DEG; ++q)
+                r.nb[q] = lds64(sl + (q + 1) * 256u);
+            I8Meta m;
+            m.w = lds128(e_cur + u * kRingEntry + 16u);
+            m.io = lds32(e_cur + u * kRingEntry + 32u);
+            pipe_decide<DEG>(p, r, m, vb + j, tbb, rwb, bl, ph, g0, o, c4b);
+        }
+        e_cur = e_cur + S * kRingEntry == meta_end ? meta0 : e_cur + S * kRingEntry;
     }
     cp_wait<0>();
 }
