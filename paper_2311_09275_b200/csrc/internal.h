@@ -27,6 +27,7 @@ constexpr int32_t kI8PipeMinBlocks = 4;
 // float + padded-table graphs with R % 256 == 0: cp.async ring kernel with this many vertices
 // in flight per warp (0 = use the register pipeline)
 constexpr int32_t kI8Ring = 4;
+constexpr int32_t kI8RingUnroll = 4;  // ring kernel main-loop unroll (multiple of kI8Ring, divides 32; 8 measured -1.3%)
 
 // Rows of a colour class per pass of the 2-D thread mapping: threads / (Lx/2), rounded
 // down to an even number when >= 2 so that the parity (c + y) & 1 of a thread's sites is

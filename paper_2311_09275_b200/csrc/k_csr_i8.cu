@@ -766,16 +766,17 @@ __global__ void __launch_bounds__(256, 3) k_csr_i8_ring(const CsrI8Params p, uin
         sl_iss += kSlot;
         e_iss += kRingEntry;
     }
-    // main loop, unrolled by S: the ring slot of vertex j is j % S (a constant per unrolled
-    // step), and its table entry is j % 64 of the circular list (S divides 32, so a group of S
-    // vertices never straddles the wrap of the decide-side entry pointer)
-    static_assert(32 % S == 0, "ring depth must divide the 32-vertex table block");
+    // main loop, unrolled by U (a multiple of S dividing 32): the ring slot of vertex j is
+    // j % S (a constant per unrolled step), and its table entry is j % 64 of the circular list
+    // (a group of U vertices never straddles the wrap of the decide-side entry pointer)
+    constexpr uint32_t U = kI8RingUnroll;
+    static_assert(U % S == 0 && 32 % U == 0, "unroll must be a multiple of the ring depth dividing 32");
     (void)sl_iss;
     (void)e_iss;
     uint32_t e_cur = meta0;  // table entry of vertex jb
-    for (uint32_t jb = 0; jb < cnt; jb += S) {
+    for (uint32_t jb = 0; jb < cnt; jb += U) {
 #pragma unroll
-        for (uint32_t u = 0; u < S; ++u) {
+        for (uint32_t u = 0; u < U; ++u) {
             const uint32_t j = jb + u;
             if (j >= cnt)
                 break;
@@ -792,7 +793,7 @@ __global__ void __launch_bounds__(256, 3) k_csr_i8_ring(const CsrI8Params p, uin
             if (u == S - 1 && (jb & 31u) == 0)
                 __syncwarp();
             I8Rows<DEG> r;
-            const uint32_t sl = ring0 + u * kSlot;
+            const uint32_t sl = ring0 + (u % S) * kSlot;
             r.own = lds64(sl);
 #pragma unroll
             for (int q = 0; q < DEG; ++q)
@@ -802,7 +803,7 @@ __global__ void __launch_bounds__(256, 3) k_csr_i8_ring(const CsrI8Params p, uin
             m.io = lds32(e_cur + u * kRingEntry + 32u);
             pipe_decide<DEG>(p, r, m, vb + j, tbb, rwb, bl, ph, g0, o, c4b);
         }
-        e_cur = e_cur + S * kRingEntry == meta_end ? meta0 : e_cur + S * kRingEntry;
+        e_cur = e_cur + U * kRingEntry == meta_end ? meta0 : e_cur + U * kRingEntry;
     }
     cp_wait<0>();
 }
