@@ -377,7 +377,7 @@ def run_ours(args):
         e2e_ms = 0.0
         h2d = d2h = 0
         Jr = torch.from_numpy(inst["J_right"]).pin_memory() if inst["kind"] == "grid" else None
-        for s in range(args.steps + 1):
+        for s in range(args.warmup + args.steps):  # W untimed warm-up steps, then K timed
             torch.cuda.synchronize()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
@@ -400,7 +400,7 @@ def run_ours(args):
             b.record(stream)
             torch.cuda.synchronize()
             e.close()
-            if s > 0:  # first iteration warms the allocator
+            if s >= args.warmup:
                 e2e_ms += a.elapsed_time(b)
         if inst["kind"] == "grid":
             h2d = 2 * n + 8 * K
