@@ -367,10 +367,11 @@ def run_ours(args):
         if (inst["kind"] == "grid" and cfg["layout"] == "bits") else \
         ("k_csr_bits" if cfg["layout"] == "bits" else
          ("k_csr_i8_ring" if inst.get("w") is not None and inst["w"].dtype == np.float32 and R % 256 == 0
-          else ("k_i8_small" if fused_one_launch else "k_csr_i8_phase")))
-    if roof["kernel"] == "k_i8_small":
-        roof["note"] = (f"one CTA per copy: {eng.R // K} copies use {eng.R // K} of the GPU's SMs; "
-                        "frac is against the whole-GPU issue peak")
+          else (("k_i8_cluster" if K <= 64 else "k_i8_small") if fused_one_launch else "k_csr_i8_phase")))
+    if roof["kernel"] in ("k_i8_small", "k_i8_cluster"):
+        per = K // 8 if roof["kernel"] == "k_i8_cluster" else 1
+        roof["note"] = (f"{per} CTA(s) per copy: {eng.R // K} copies use {per * (eng.R // K)} of the GPU's "
+                        "SMs; frac is against the whole-GPU issue peak")
     roof["kernel_share_of_step"] = kernel_ms / max(total_ms * (1 if world == 1 else 1), 1e-9)
     roof["avg_launch_ms"] = avg_launch_ms
 

@@ -154,6 +154,8 @@ struct SmallI8Params {
 constexpr int32_t kI8SmallThreads = 1024;  // one 8-replica task per thread on C1 (512: -15%)
 // largest n x K (bytes of one copy's spins) the fused int8 launch keeps in shared memory
 constexpr int64_t kI8SmallMaxBytes = 96 * 1024;
+// fused small int8 runs: spread each copy over a cluster of K/8 CTAs (K <= 64)
+constexpr bool kI8Cluster = true;
 
 struct ExchangeParams {
     int64_t *E;                // [R_local] (int64 or double bits)

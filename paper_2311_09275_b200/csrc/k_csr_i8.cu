@@ -22,6 +22,9 @@
 // exponential cexp32, which is only evaluated when a fast estimate cannot decide.
 #include "internal.h"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace ising {
 
 namespace {
@@ -1088,11 +1091,255 @@ __global__ void __launch_bounds__(kI8SmallThreads, 1) k_i8_small(const SmallI8Pa
     }
 }
 
+// The same PT run with each copy spread over a cluster of K/8 CTAs: CTA q holds the copy's
+// slots 8q .. 8q+7 (one 8-replica group: n x 8 bytes), so the sweeps of a small instance run on
+// K/8 SMs instead of one.  Only the exchange couples the CTAs: the slots' energies are gathered
+// through distributed shared memory, every CTA takes the same decisions, and the pair that
+// crosses two CTAs in odd exchanges (slots 8q+7, 8q+8) trades its byte columns over DSMEM
+// (both sides copy the other's column into a buffer, synchronise, then write).
+constexpr int kI8ClusterThreads = 128;
+
+__global__ void __launch_bounds__(kI8ClusterThreads, 1) k_i8_cluster(const SmallI8Params p)
+{
+    extern __shared__ __align__(16) unsigned char cl_smem[];
+    const int K = p.K, n = p.n, tid = threadIdx.x, nt = blockDim.x;
+    const int NC = K / 8;
+    cg::cluster_group cl = cg::this_cluster();
+    const int q = (int)cl.block_rank();              // this CTA's 8-slot group of the copy
+    const int c = (int)(blockIdx.x / (unsigned)NC);  // local copy
+    uint2 *S = reinterpret_cast<uint2 *>(cl_smem);                      // [n] 8 slots each
+    int8_t *xlo = reinterpret_cast<int8_t *>(S + n);                    // [n] prev CTA's slot 7
+    int8_t *xhi = xlo + n;                                              // [n] next CTA's slot 0
+    int64_t *Ecopy = reinterpret_cast<int64_t *>(cl_smem + (((size_t)n * 10 + 15) & ~(size_t)15));
+    int64_t *Wcopy = Ecopy + K;
+    int64_t *Eown = Wcopy + K;                                          // [8]
+    int64_t *part = Eown + 8;                                           // [nt]
+    uint64_t *Ts = reinterpret_cast<uint64_t *>(part + nt);            // [8][qmax+1]
+    __shared__ uint32_t mswap[2];
+    __shared__ int64_t bestE, bestSlot, bestSweep;
+    __shared__ int32_t kmin, improve;
+    const int64_t slot_c = p.slot0 + (int64_t)c * K;
+    const uint32_t c_global = (uint32_t)(slot_c / K);
+    const size_t col0 = (size_t)c * K + 8 * q;  // first local replica column of this CTA
+    for (int v = tid; v < n; v += nt)
+        S[v] = *reinterpret_cast<const uint2 *>(p.s + (size_t)v * p.R + col0);
+    for (int k = tid; k < K; k += nt)
+        Wcopy[k] = p.walker[(size_t)c * K + k];
+    for (int x = tid; x < 8 * (p.qmax + 1); x += nt)
+        Ts[x] = p.T[col0 * (p.qmax + 1) + x];
+    if (tid == 0) {
+        bestE = INT64_MAX;
+        bestSlot = -1;
+        bestSweep = -1;
+    }
+    __syncthreads();
+    const uint32_t g = (uint32_t)(slot_c >> 3) + (uint32_t)q;
+    int8_t *Sb = reinterpret_cast<int8_t *>(S);
+    for (int round = 0; round < p.n_rounds; ++round) {
+        for (int sw = 0; sw < p.k_ex; ++sw) {
+            const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + sw);
+            for (int ccl = 0; ccl < p.ncol; ++ccl) {
+                const int v0 = p.class_off[ccl], v1 = p.class_off[ccl + 1];
+                for (int v = v0 + tid; v < v1; v += nt) {
+                    const uint2 own = S[v];
+                    int32_t sh[8];
+#pragma unroll
+                    for (int b = 0; b < 8; ++b)
+                        sh[b] = 0;
+                    for (int e = __ldg(p.rp + v); e < __ldg(p.rp + v + 1); ++e) {
+                        const uint2 nb = S[__ldg(p.col + e)];
+                        const int32_t w = __ldg(p.wi + e);
+                        const uint32_t x0 = own.x ^ nb.x, x1 = own.y ^ nb.y;
+#pragma unroll
+                        for (int b = 0; b < 8; ++b) {
+                            const uint32_t word = b < 4 ? x0 : x1;
+                            const int32_t m = (int32_t)(word << (24 - 8 * (b & 3))) >> 31;  // -1 iff s_i != s_j
+                            sh[b] += (w ^ m) - m;
+                        }
+                    }
+                    const uint32_t io = __ldg(p.orig + v);
+                    const uint4 h = philox(io, t, g, ST_WORD_HI << 24, p.rk);
+                    const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+                    uint32_t fm0 = 0u, fm1 = 0u;
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        bool acc = sh[b] >= 0;  // dE = -2 s h <= 0
+                        if (!acc) {
+                            const uint32_t hb = (b & 1) ? (hw[b >> 1] >> 16) : (hw[b >> 1] & 0xFFFFu);
+                            const uint64_t T = Ts[(size_t)b * (p.qmax + 1) + (uint32_t)(-sh[b])];
+                            acc = exact_less(hb, T, io, t, (uint32_t)(slot_c + 8 * q + b), p.rk);
+                        }
+                        if (acc) {
+                            if (b < 4)
+                                fm0 |= 0xFEu << (8 * (b & 3));
+                            else
+                                fm1 |= 0xFEu << (8 * (b & 3));
+                        }
+                    }
+                    S[v] = make_uint2(own.x ^ fm0, own.y ^ fm1);
+                }
+                __syncthreads();
+            }
+        }
+        {  // energies of this CTA's 8 slots (each edge once, fixed-order partial sums)
+            const int b = tid & 7, pt = tid >> 3, np = nt >> 3;
+            int64_t acc = 0;
+            for (int v = pt; v < n; v += np) {
+                const int32_t sv = Sb[8 * v + b];
+                for (int e = __ldg(p.rp + v); e < __ldg(p.rp + v + 1); ++e) {
+                    const int j = __ldg(p.col + e);
+                    if (j > v)
+                        acc += (int64_t)__ldg(p.wi + e) * sv * Sb[8 * j + b];
+                }
+            }
+            part[tid] = acc;
+            __syncthreads();
+            if (tid < 8) {
+                int64_t e = 0;
+                for (int x = 0; x < np; ++x)
+                    e += part[8 * x + tid];
+                Eown[tid] = e;
+            }
+            if (tid < 2)
+                mswap[tid] = 0u;
+        }
+        cl.sync();  // every CTA's Eown complete
+        for (int k = tid; k < K; k += nt)
+            Ecopy[k] = cl.map_shared_rank(Eown, (unsigned)(k >> 3))[k & 7];
+        __syncthreads();
+        const uint32_t t_now = p.t0 + (uint32_t)((round + 1) * p.k_ex);
+        const uint32_t e_now = p.e0 + (uint32_t)round;
+        if (tid < 32) {  // the copy's best-so-far: argmin, ties -> lowest slot; strict <
+            int64_t bE = INT64_MAX;
+            int bk = -1;
+            for (int k = tid; k < K; k += 32)
+                if (bk < 0 || Ecopy[k] < bE) {
+                    bE = Ecopy[k];
+                    bk = k;
+                }
+            for (int off = 16; off > 0; off >>= 1) {
+                const int64_t oE = __shfl_down_sync(0xFFFFFFFFu, bE, off);
+                const int ok = __shfl_down_sync(0xFFFFFFFFu, bk, off);
+                if (ok >= 0 && (bk < 0 || oE < bE || (oE == bE && ok < bk))) {
+                    bE = oE;
+                    bk = ok;
+                }
+            }
+            if (tid == 0) {
+                improve = bE < bestE;
+                kmin = bk;
+                if (bE < bestE) {
+                    bestE = bE;
+                    bestSlot = slot_c + bk;
+                    bestSweep = t_now;
+                }
+            }
+        }
+        __syncthreads();
+        if (improve && (kmin >> 3) == q)
+            for (int v = tid; v < n; v += nt)
+                p.snap[(size_t)c * n + __ldg(p.orig + v)] = Sb[8 * v + (kmin & 7)];
+        const int par = (int)(e_now & 1u);
+        for (int k = par + 2 * tid; k + 1 < K; k += 2 * nt) {  // same rule as k_exchange
+            const int64_t d = Ecopy[k + 1] - Ecopy[k];
+            bool accept = d >= 0;
+            if (!accept) {
+                const int64_t j = -d - 1;
+                if (j < __ldg(p.Tx_len + k)) {
+                    const uint4 w = philox((uint32_t)k, e_now, c_global, ST_EXCH << 24, p.rk);
+                    const uint64_t Ux = ((uint64_t)w.x << 32) | (uint64_t)w.y;
+                    accept = Ux < __ldg(p.Tx + __ldg(p.Tx_off + k) + j);
+                }
+            }
+            if (accept) {
+                atomicOr(&mswap[k >> 5], 1u << (k & 31));
+                const int64_t te = Ecopy[k];
+                Ecopy[k] = Ecopy[k + 1];
+                Ecopy[k + 1] = te;
+                const int64_t tw = Wcopy[k];
+                Wcopy[k] = Wcopy[k + 1];
+                Wcopy[k + 1] = tw;
+            }
+        }
+        __syncthreads();
+        auto accepted = [&](int k) { return ((mswap[k >> 5] >> (k & 31)) & 1u) != 0u; };
+        // within-group pairs: local byte swaps
+        for (int x = tid; x < n * 4; x += nt) {
+            const int v = x >> 2, kk = par + 2 * (x & 3);  // kk, kk+1 inside this group
+            if (kk + 1 < 8 && accepted(8 * q + kk)) {
+                const int8_t a = Sb[8 * v + kk];
+                Sb[8 * v + kk] = Sb[8 * v + kk + 1];
+                Sb[8 * v + kk + 1] = a;
+            }
+        }
+        // the pairs across groups (odd exchanges): uniform over the cluster
+        bool any_cross = false;
+        for (int r = 0; r + 1 < NC; ++r)
+            any_cross |= par == 1 && accepted(8 * r + 7);
+        if (any_cross) {
+            const bool hi = par == 1 && q + 1 < NC && accepted(8 * q + 7);  // my slot 7 <-> next's slot 0
+            const bool lo = par == 1 && q > 0 && accepted(8 * q - 1);       // prev's slot 7 <-> my slot 0
+            cl.sync();  // every CTA's within-group swaps done (slots 0 and 7 are not touched by them)
+            const int8_t *nxt = hi ? reinterpret_cast<const int8_t *>(cl.map_shared_rank(S, (unsigned)(q + 1))) : nullptr;
+            const int8_t *prv = lo ? reinterpret_cast<const int8_t *>(cl.map_shared_rank(S, (unsigned)(q - 1))) : nullptr;
+            for (int v = tid; v < n; v += nt) {
+                if (hi)
+                    xhi[v] = nxt[8 * v + 0];
+                if (lo)
+                    xlo[v] = prv[8 * v + 7];
+            }
+            cl.sync();  // every CTA has copied what it takes before anything is overwritten
+            for (int v = tid; v < n; v += nt) {
+                if (hi)
+                    Sb[8 * v + 7] = xhi[v];
+                if (lo)
+                    Sb[8 * v + 0] = xlo[v];
+            }
+        }
+        __syncthreads();
+    }
+    for (int v = tid; v < n; v += nt)
+        *reinterpret_cast<uint2 *>(p.s + (size_t)v * p.R + col0) = S[v];
+    for (int b = tid; b < 8; b += nt)
+        p.E_out[col0 + b] = Ecopy[8 * q + b];
+    if (q == 0) {
+        for (int k = tid; k < K; k += nt)
+            p.walker[(size_t)c * K + k] = Wcopy[k];
+        if (tid == 0) {
+            p.copy_best[3 * c + 0] = bestE;
+            p.copy_best[3 * c + 1] = bestSlot;
+            p.copy_best[3 * c + 2] = bestSweep;
+        }
+    }
+    cl.sync();  // no CTA exits while a peer may still read its shared memory
+}
+
 cudaError_t launch_i8_small(const SmallI8Params &p, int32_t C_local, cudaStream_t st)
 {
     const int nparts = kI8SmallThreads / p.K;
     const size_t smem = (((size_t)p.n * p.K + 15) & ~(size_t)15) + (size_t)(2 + nparts) * p.K * 8 +
                         (size_t)p.K * (p.qmax + 1) * 8;
+    if (kI8Cluster && p.K / 8 <= 8) {  // each copy on a cluster of K/8 CTAs (8 slots each)
+        const int NC = p.K / 8;
+        const size_t cs = (((size_t)p.n * 10 + 15) & ~(size_t)15) + (size_t)(2 * p.K + 8 + kI8ClusterThreads) * 8 +
+                          (size_t)8 * (p.qmax + 1) * 8;
+        cudaError_t e = cudaFuncSetAttribute(k_i8_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+        if (e != cudaSuccess)
+            return e;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(C_local * NC));
+        cfg.blockDim = dim3(kI8ClusterThreads);
+        cfg.dynamicSmemBytes = cs;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)NC;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, k_i8_cluster, p);
+    }
     cudaError_t e = cudaFuncSetAttribute(k_i8_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
