@@ -95,14 +95,16 @@ def _nccl_worker(rank, world, port, out):
     torch.cuda.synchronize()
     np.save(os.path.join(out, "E.npy"), eng.energies())
     np.save(os.path.join(out, "W.npy"), eng.walkers())
-    b = eng.best(spins=False)
+    from paper_2311_09275_b200.driver import merge_best_over_ranks
+    b = merge_best_over_ranks(eng.best(spins=False), None)  # the bench's per-step NCCL merge
     np.save(os.path.join(out, "rec.npy"), np.array([b["E"], b["slot"], b["sweep"]]))
     dist.destroy_process_group()
 
 
 def test_nccl_record_gather_single_rank():
     """The NCCL branch of the record all-gather (all_gather_into_tensor on device buffers)
-    feeding ising_exchange_end, on one rank: equal to the oracle's local exchanges."""
+    feeding ising_exchange_end, and the NCCL best-record merge bench.py uses per step, on one
+    rank: equal to the oracle's local exchanges."""
     with tempfile.TemporaryDirectory() as out:
         mp.spawn(_nccl_worker, args=(1, _free_port(), out), nprocs=1, join=True)
         E = np.load(os.path.join(out, "E.npy"))
