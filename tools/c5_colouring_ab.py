@@ -1,3 +1,5 @@
+"""C5 on one GPU with the smallest-last vs the ascending greedy colouring: create time and
+attempts/s of 100 sweeps (R12b).  python tools/c5_colouring_ab.py"""
 import time, sys, numpy as np, torch
 sys.path.insert(0, '/root/repo')
 import synth

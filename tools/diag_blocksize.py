@@ -1,3 +1,5 @@
+"""Block-size invariance diagnostic of the torus kernel (energies/spins for several CTA sizes
+against the oracle).  python tools/diag_blocksize.py"""
 import sys; sys.path.insert(0, '.')
 import numpy as np, synth, oracle
 from paper_2311_09275_b200 import Engine, run_pt

@@ -1,3 +1,5 @@
+"""One bench e2e step of C2 split into create / run / readback (CUDA events on the stream).
+python tools/e2e_probe.py"""
 import sys, time, torch
 sys.path.insert(0, "/root/repo")
 import synth

@@ -1,3 +1,5 @@
+"""Hot SASS blocks of an ncu report by executed instructions and stall samples:
+python tools/ncu_source.py <rep> [threshold] [first-line last-line]"""
 import csv, subprocess, sys
 rep = sys.argv[1]
 thr = float(sys.argv[2]) if len(sys.argv) > 2 else 0.004
