@@ -147,12 +147,16 @@ struct ising_handle {
     uint64_t fingerprint = 0;  // FNV-1a of the instance, colouring and ladder (checkpoints)
 
     template <class T>
+    // Device buffers come from the device's stream-ordered memory pool (cudaMallocAsync on the
+    // handle's stream), which keeps freed memory for the next handle: creating and destroying
+    // handles in a loop (bench e2e, trial batches) costs no cudaMalloc / cudaFree (the latter
+    // synchronises the device) after the first time.
     cudaError_t alloc(T **p, size_t count)
     {
         *p = nullptr;
         if (count == 0)
             count = 1;
-        cudaError_t e = cudaMalloc((void **)p, count * sizeof(T));
+        cudaError_t e = cudaMallocAsync((void **)p, count * sizeof(T), st);
         if (e == cudaSuccess)
             allocs.push_back((void *)*p);
         return e;
@@ -160,9 +164,10 @@ struct ising_handle {
     ~ising_handle()
     {
         for (void *p : allocs)
-            cudaFree(p);
+            cudaFreeAsync(p, st);
         if (d_sched)
             cudaFree(d_sched);
+        cudaStreamSynchronize(st);
     }
 };
 
@@ -225,6 +230,18 @@ void fill_run(ising_handle *h, const ising_run_desc *d)
     h->rng = d->rng;
     h->device = d->device;
     h->st = (cudaStream_t)d->stream;
+    {  // keep freed pool memory for the next handle (default threshold 0 returns it at sync)
+        static bool retained[64] = {};
+        if (d->device >= 0 && d->device < 64 && !retained[d->device]) {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, d->device) == cudaSuccess) {
+                uint64_t thr = ~0ull;
+                if (cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) == cudaSuccess)
+                    retained[d->device] = true;
+            }
+            cudaGetLastError();  // no GPU: the first CUDA call of create reports it
+        }
+    }
     h->threads = d->block_threads ? d->block_threads : 1024;
 }
 
@@ -303,7 +320,8 @@ int build_common_device(ising_handle *h, int64_t sum_abs_w)
                     rows[k].push_back(T);
                 }
         };
-        const int32_t nthr = std::max(1, std::min<int32_t>(npair, (int32_t)std::thread::hardware_concurrency()));
+        const int32_t nthr =
+            std::max(1, std::min<int32_t>(std::min<int32_t>(npair, 16), (int32_t)std::thread::hardware_concurrency()));
         if (nthr > 1 && dmax > 256) {
             std::vector<std::thread> pool;
             for (int32_t t = 0; t < nthr; ++t)
