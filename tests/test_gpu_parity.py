@@ -585,3 +585,38 @@ def test_checkpoint_rejects_other_handles():
     with pytest.raises(L.IsingError) as e:
         a.load_state(b"x" * len(blob))
     assert e.value.code == L.ISING_E_STATE
+
+
+def _code_of(fn, *a):
+    with pytest.raises(L.IsingError) as e:
+        fn(*a)
+    return e.value.code
+
+
+def test_api_error_paths_on_live_handles():
+    """include/ising.h error contract on live handles: wrong call order, slots outside the
+    shard, bad values, and operations a layout / weight type does not support."""
+    inst = grid(8, 8, 9)
+    betas = synth.beta_ladder(32)
+    eng = Engine(inst, 32, 4, betas, seed=KEY, copy_begin=1, copy_end=3, layout="bits")
+    assert _code_of(L.ising_best, eng.h) == L.ISING_E_STATE               # no best check yet
+    assert _code_of(L.ising_get_spins, eng.h, 0) == L.ISING_E_STATE       # slot of copy 0: not held
+    assert _code_of(L.ising_get_spins, eng.h, 3 * 32) == L.ISING_E_STATE  # past the shard
+    bad = np.ones(64, np.int8)
+    bad[7] = 0
+    assert _code_of(L.ising_set_spins, eng.h, 32, bad) == L.ISING_E_ARG
+    assert _code_of(L.ising_sweep, eng.h, -1) == L.ISING_E_ARG
+    assert _code_of(L.ising_run, eng.h, 1, 0) == L.ISING_E_ARG
+    assert _code_of(L.ising_anneal, eng.h, -np.ones((2, 32))) == L.ISING_E_ARG
+    assert _code_of(L.ising_icm, eng.h, 0) == L.ISING_E_UNSUPPORTED      # shard [1, 3) splits pairs
+    eng.sweep(3)
+    eng.check_best()
+    b = eng.best(spins=True)
+    assert 32 <= b["slot"] < 96 and b["spins"].shape == (64,)
+    # float weights: no replica exchange (R15), no cluster moves on the int8 layout
+    finst = _regular_inst(200, 4)
+    f = Engine(finst, 8, 2, synth.beta_ladder(8), seed=KEY, layout="i8")
+    assert _code_of(L.ising_exchange, f.h) == L.ISING_E_UNSUPPORTED
+    assert _code_of(L.ising_run, f.h, 1, 10) == L.ISING_E_UNSUPPORTED
+    assert _code_of(L.ising_icm, f.h, 0) == L.ISING_E_UNSUPPORTED
+    assert "unsupported" in L.ising_last_error().lower() or L.ising_last_error() != ""
