@@ -249,8 +249,12 @@ def roofline_entry(kernel_ms, attempts_per_launch, layout, clocks, workload="c2"
                 "traffic": None, "note": "no ncu instruction count committed yet"}
     ach = attempts_per_launch * ipa["warp_inst_per_attempt"] / (kernel_ms * 1e-3) / 1e9
     traffic = ipa.get("dram_bytes_per_attempt")
+    if ipa.get("dram_bytes_per_launch") is not None:  # on-chip state: a fixed load/store per launch
+        traffic_launch = ipa["dram_bytes_per_launch"]
+    else:
+        traffic_launch = traffic * attempts_per_launch if traffic is not None else None
     return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "Ginst/s", "frac": ach / peak,
-            "traffic": traffic * attempts_per_launch if traffic is not None else None,
+            "traffic": traffic_launch,
             "peak_source": f"derived: 148 SMs x 4 issue/cycle x {mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
             "inst_per_attempt_source": ipa.get("source")}
 
