@@ -117,6 +117,15 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
             out, _ = self.proc.communicate()
+        note = None
+        if not out.strip():  # timed region shorter than nvidia-smi's start-up + period
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=10).stdout
+                note = "timed region shorter than the sampling period: one query right after it"
+            except Exception:
+                out = ""
         sm, mx, reasons = [], [], set()
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
@@ -133,8 +142,11 @@ class ClockSampler:
                     reasons.add(name)
         if not sm:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
-                "samples": len(sm), "reasons": sorted(reasons)}
+        r = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+             "samples": len(sm), "reasons": sorted(reasons)}
+        if note:
+            r["note"] = note
+        return r
 
 
 # ------------------------------------------------------------------ reference (oracle) arm
