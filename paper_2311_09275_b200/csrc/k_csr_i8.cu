@@ -759,23 +759,17 @@ __global__ void __launch_bounds__(256, 3) k_csr_i8_ring(const CsrI8Params p, uin
     cp_commit();
     cp_wait<0>();
     __syncwarp();
-    uint32_t sl_iss = ring0;  // ring slot of the vertex issued next
-    uint32_t e_iss = meta0;   // its table entry
 #pragma unroll
-    for (uint32_t j = 0; j + 1 < S; ++j) {
+    for (uint32_t j = 0; j + 1 < S; ++j) {  // vertices 0 .. S-2 into ring slots 0 .. S-2
         if (j < cnt)
-            rows_issue(j, sl_iss, e_iss);
+            rows_issue(j, ring0 + j * kSlot, meta0 + j * kRingEntry);
         cp_commit();
-        sl_iss += kSlot;
-        e_iss += kRingEntry;
     }
     // main loop, unrolled by U (a multiple of S dividing 32): the ring slot of vertex j is
     // j % S (a constant per unrolled step), and its table entry is j % 64 of the circular list
     // (a group of U vertices never straddles the wrap of the decide-side entry pointer)
     constexpr uint32_t U = kI8RingUnroll;
     static_assert(U % S == 0 && 32 % U == 0, "unroll must be a multiple of the ring depth dividing 32");
-    (void)sl_iss;
-    (void)e_iss;
     uint32_t e_cur = meta0;  // table entry of vertex jb
     for (uint32_t jb = 0; jb < cnt; jb += U) {
 #pragma unroll
