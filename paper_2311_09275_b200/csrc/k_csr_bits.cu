@@ -159,7 +159,6 @@ __global__ void __launch_bounds__(kCsrMaxThreads, 1) k_csr_bits(const CsrBitsPar
 {
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t Ucnt[32];
-    __shared__ int32_t wcount[33];
     __shared__ PtShared ps;
     const int n = p.n;
     const int nbw = (n + 31) / 32;
@@ -259,37 +258,15 @@ __global__ void __launch_bounds__(kCsrMaxThreads, 1) k_csr_bits(const CsrBitsPar
                         S[v] = own ^ acc;
                     }
                 }
-                if (lane == 0)
-                    wcount[warp] = min(wq, wcap);
-                __syncthreads();
-                // every warp scans the per-warp queue counts itself (no extra barrier):
-                // lane w holds the exclusive prefix of region w
-                const int cnt_l = lane < nwarps ? wcount[lane] : 0;
-                int incl = cnt_l;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                    if (lane >= o)
-                        incl += u;
-                }
-                const int excl = incl - cnt_l;
-                const int nq = __shfl_sync(0xFFFFFFFFu, incl, 31);
-                // stage 2: re-evaluate the queued vertices (neighbours are unchanged) and
-                // finish their comparisons from plane 8 on, all lanes busy
-                for (int qb = wbase; qb < nq; qb += nt) {
+                // stage 2: each warp re-evaluates its own queued vertices (their neighbours
+                // cannot change inside a colour phase) right after its stage 1, no barrier in
+                // between, and finishes their comparisons from plane 8 on
+                const int nown = min(wq, wcap);
+                for (int qb = 0; qb < nown; qb += 32) {
                     const int q = qb + lane;
-                    int lo = 0;  // region: last w with excl_w <= q (binary search over lanes)
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        const int cand = lo + step;
-                        const int ev = __shfl_sync(0xFFFFFFFFu, excl, cand < 32 ? cand : 31);
-                        if (cand < nwarps && ev <= q)
-                            lo = cand;
-                    }
-                    const int base_lo = __shfl_sync(0xFFFFFFFFu, excl, lo);
-                    if (q >= nq)
+                    if (q >= nown)
                         continue;
-                    const int qs = lo * wcap + (q - base_lo);
+                    const int qs = wq0 + q;
                     const int v = (int)q_idx[qs];
                     uint32_t D = q_D[qs], acc = q_acc[qs];
                     const CsrSite st = csr_eval(S, p, v);

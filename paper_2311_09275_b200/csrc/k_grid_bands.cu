@@ -240,8 +240,6 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBit
 {
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t Ucnt[32];
-    __shared__ int32_t wcount[33];
-    __shared__ int32_t wprefix[33];
     // fused PT rounds (cluster of words_per_copy CTAs = one copy): the copy's energies,
     // walker ids, swap mask and best record, held identically by every CTA of the cluster
     __shared__ PtShared ps;
@@ -395,40 +393,16 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBit
 #ifdef ISING_GRID_TIMING
                 long long tB = clock64();
 #endif
-                if (lane == 0)
-                    wcount[warp] = min(wq, wcap);
-                __syncthreads();
 #ifdef ISING_GRID_TIMING
                 long long tC = clock64();
 #endif
-                // every warp scans the per-warp queue counts itself (no extra barrier):
-                // lane w holds the exclusive prefix of region w
-                const int cnt_l = lane < nwarps ? wcount[lane] : 0;
-                int incl = cnt_l;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                    if (lane >= o)
-                        incl += u;
-                }
-                const int excl = incl - cnt_l;
-                const int nq = __shfl_sync(0xFFFFFFFFu, incl, 31);
-                // stage 2: the queued tail, one word per thread, all lanes busy; the first two
-                // further Philox calls are issued together (the tail is latency bound)
-                for (int qb = tid - lane; qb < nq; qb += nt) {
+                // stage 2: each warp finishes its own queued words right after its stage 1
+                const int nown = min(wq, wcap);
+                for (int qb = 0; qb < nown; qb += 32) {
                     const int q = qb + lane;
-                    int lo = 0;  // region: last w with excl_w <= q (binary search over lanes)
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        const int cand = lo + step;
-                        const int ev = __shfl_sync(0xFFFFFFFFu, excl, cand < 32 ? cand : 31);
-                        if (cand < nwarps && ev <= q)
-                            lo = cand;
-                    }
-                    const int base_lo = __shfl_sync(0xFFFFFFFFu, excl, lo);
-                    if (q >= nq)
+                    if (q >= nown)
                         continue;
-                    const uint4 item = Q4[lo * wcap + (q - base_lo)];
+                    const uint4 item = Q4[wq0 + q];
                     const int l = (int)(item.x & 0xFFFFu);
                     const uint32_t i_orig = item.x >> 16;
                     uint32_t D = item.y, acc = item.z;

@@ -25,9 +25,10 @@
 //
 // Work compaction of the RNG tail: a colour phase runs in two
 // stages.  Stage 1: every site draws planes 0..7 (two Philox calls); ~89% of
-// words are then decided and written.  The rest are pushed to a shared-memory
-// queue and stage 2 finishes them with all 32 lanes of a warp busy, instead of
-// leaving most lanes of a warp idle while one lane draws its 3rd/4th call.
+// words are then decided and written.  The rest are pushed to the warp's
+// shared-memory queue, and the warp finishes them right after its stage 1 with
+// all 32 lanes busy (no barrier in between), instead of leaving most lanes of a
+// warp idle while one lane draws its 3rd/4th call.
 // Philox rounds 0-1 are partially hoisted: the parts that depend only on the
 // CTA's group g, the sweep t or the site i are computed once, not per call.
 #include "bits_core.cuh"
@@ -108,8 +109,6 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
 {
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t Ucnt[32];
-    __shared__ int32_t wcount[33];
-    __shared__ int32_t wprefix[33];
     // fused PT rounds (cluster of words_per_copy CTAs = one copy): the copy's energies,
     // walker ids, swap mask and best record, held identically by every CTA of the cluster
     __shared__ PtShared ps;
@@ -256,40 +255,17 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
 #ifdef ISING_GRID_TIMING
                 long long tB = clock64();
 #endif
-                if (lane == 0)
-                    wcount[warp] = min(wq, wcap);
-                __syncthreads();
 #ifdef ISING_GRID_TIMING
                 long long tC = clock64();
 #endif
-                // every warp scans the per-warp queue counts itself (no extra barrier):
-                // lane w holds the exclusive prefix of region w
-                const int cnt_l = lane < nwarps ? wcount[lane] : 0;
-                int incl = cnt_l;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                    if (lane >= o)
-                        incl += u;
-                }
-                const int excl = incl - cnt_l;
-                const int nq = __shfl_sync(0xFFFFFFFFu, incl, 31);
-                // stage 2: the queued tail, one word per thread, all lanes busy; the first two
-                // further Philox calls are issued together (the tail is latency bound)
-                for (int qb = tid - lane; qb < nq; qb += nt) {
+                // stage 2 (own-queue variant): each warp finishes its own queued words right
+                // after its stage 1, no barrier in between
+                const int nown = min(wq, wcap);
+                for (int qb = 0; qb < nown; qb += 32) {
                     const int q = qb + lane;
-                    int lo = 0;  // region: last w with excl_w <= q (binary search over lanes)
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        const int cand = lo + step;
-                        const int ev = __shfl_sync(0xFFFFFFFFu, excl, cand < 32 ? cand : 31);
-                        if (cand < nwarps && ev <= q)
-                            lo = cand;
-                    }
-                    const int base_lo = __shfl_sync(0xFFFFFFFFu, excl, lo);
-                    if (q >= nq)
+                    if (q >= nown)
                         continue;
-                    const uint4 item = Q4[lo * wcap + (q - base_lo)];
+                    const uint4 item = Q4[wq0 + q];
                     const int l = (int)(item.x & 0xFFFFu);
                     const uint32_t i_orig = item.x >> 16;
                     uint32_t D = item.y, acc = item.z;
