@@ -158,7 +158,10 @@ size_t csr_bits_smem(int32_t n, int32_t qmax, int32_t words_per_copy)
 __global__ void __launch_bounds__(kCsrMaxThreads, 1) k_csr_bits(const CsrBitsParams p)
 {
     extern __shared__ __align__(16) uint32_t sm[];
-    __shared__ int32_t Ucnt[32];
+    // per-replica bond counts, double-buffered by round parity: peers of the cluster read a
+    // CTA's counts over DSMEM after a cluster barrier, and the next round writes the other
+    // buffer, so no write can overtake a slow peer's read
+    __shared__ int32_t Ubuf[2][32];
     __shared__ PtShared ps;
     const int n = p.n;
     const int nbw = (n + 31) / 32;
@@ -200,6 +203,7 @@ __global__ void __launch_bounds__(kCsrMaxThreads, 1) k_csr_bits(const CsrBitsPar
     __syncthreads();
 
     for (int round = 0; round < p.n_rounds; ++round) {
+        int32_t *Ucnt = Ubuf[round & 1];
         for (int s = 0; s < p.k_ex; ++s) {
             const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + s);
             const PlaneUniform U = plane_uniform(g, t, rkr);
@@ -329,6 +333,7 @@ __global__ void __launch_bounds__(kCsrMaxThreads, 1) k_csr_bits(const CsrBitsPar
                 p.Tx_len, p.rk, snap);
     }
 
+    int32_t *Ucnt = Ubuf[(p.n_rounds - 1) & 1];  // the last round's counts
     pt_finish(ps, pt, p.n_rounds, Ucnt, p.m, p.E_out, p.walker, p.copy_best, gl, wt, c_local, K);
     uint32_t *dst = p.state_out + (size_t)gl * n;
     for (int i = tid; i < n; i += nt)

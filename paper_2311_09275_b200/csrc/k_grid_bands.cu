@@ -239,7 +239,10 @@ __device__ void pt_step_xc(PtShared &ps, const int32_t *Ucnt, int64_t m_edges, u
 __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBitsParams p)
 {
     extern __shared__ __align__(16) uint32_t sm[];
-    __shared__ int32_t Ucnt[32];
+    // per-replica bond counts, double-buffered by round parity: peers of the cluster read a
+    // CTA's counts over DSMEM after a cluster barrier, and the next round writes the other
+    // buffer, so no write can overtake a slow peer's read
+    __shared__ int32_t Ubuf[2][32];
     // fused PT rounds (cluster of words_per_copy CTAs = one copy): the copy's energies,
     // walker ids, swap mask and best record, held identically by every CTA of the cluster
     __shared__ PtShared ps;
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBit
 
     uint32_t bar_target = 0;  // xc mode: the copy barrier's count after the next arrival
     for (int round = 0; round < p.n_rounds; ++round) {
+        int32_t *Ucnt = Ubuf[round & 1];
         // ---- k_ex sweeps
         for (int s = 0; s < p.k_ex; ++s) {
             const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + s);
@@ -503,6 +507,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBit
     }
 
     // ---- outputs
+    int32_t *Ucnt = Ubuf[(p.n_rounds - 1) & 1];  // the last round's counts
     if (NB > 1 && !(pt && p.n_rounds > 0)) {  // the group's counts: sum over its bands
         cg::cluster_group cl = cg::this_cluster();
         cl.sync();

@@ -108,7 +108,10 @@ size_t grid_bits_smem(int32_t n)
 __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBitsParams p)
 {
     extern __shared__ __align__(16) uint32_t sm[];
-    __shared__ int32_t Ucnt[32];
+    // per-replica bond counts, double-buffered by round parity: peers of the cluster read a
+    // CTA's counts over DSMEM after a cluster barrier, and the next round writes the other
+    // buffer, so no write can overtake a slow peer's read
+    __shared__ int32_t Ubuf[2][32];
     // fused PT rounds (cluster of words_per_copy CTAs = one copy): the copy's energies,
     // walker ids, swap mask and best record, held identically by every CTA of the cluster
     __shared__ PtShared ps;
@@ -171,6 +174,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
     __syncthreads();
 
     for (int round = 0; round < p.n_rounds; ++round) {
+        int32_t *Ucnt = Ubuf[round & 1];
         // ---- k_ex sweeps
         for (int s = 0; s < p.k_ex; ++s) {
             const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + s);
@@ -348,6 +352,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
     }
 
     // ---- outputs
+    int32_t *Ucnt = Ubuf[(p.n_rounds - 1) & 1];  // the last round's counts
     pt_finish(ps, pt, p.n_rounds, Ucnt, 2 * (int64_t)n, p.E_out, p.walker, p.copy_best, gl, wt,
               c_local, K);
     uint32_t *dst = p.state_out + (size_t)gl * n;
