@@ -204,6 +204,8 @@ __global__ void __launch_bounds__(kCsrMaxThreads, 1) k_csr_bits(const CsrBitsPar
 
     for (int round = 0; round < p.n_rounds; ++round) {
         int32_t *Ucnt = Ubuf[round & 1];
+        if (tid < 32)  // zeroed here: the colour-phase barriers order it before the atomicAdds
+            Ucnt[tid] = 0;
         for (int s = 0; s < p.k_ex; ++s) {
             const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + s);
             const PlaneUniform U = plane_uniform(g, t, rkr);
@@ -289,8 +291,6 @@ __global__ void __launch_bounds__(kCsrMaxThreads, 1) k_csr_bits(const CsrBitsPar
 
         // energy: each edge once, counted from its endpoint in the higher colour class
         {
-            if (tid < 32)
-                Ucnt[tid] = 0;
             uint32_t cnt[kCsrCnt];
 #pragma unroll
             for (int l = 0; l < kCsrCnt; ++l)
@@ -317,9 +317,11 @@ __global__ void __launch_bounds__(kCsrMaxThreads, 1) k_csr_bits(const CsrBitsPar
 #pragma unroll
             for (int l = 0; l < kCsrCnt; ++l)
                 acc += (int32_t)((cnt[l] >> lane) & 1u) << l;
-            __syncthreads();
+            if (p.k_ex == 0)  // no colour phase (hence no barrier) since the zeroing
+                __syncthreads();
             atomicAdd(&Ucnt[lane], acc);
-            __syncthreads();
+            if (!pt)  // pt_step opens with a cluster barrier
+                __syncthreads();
         }
         if (!pt)
             continue;

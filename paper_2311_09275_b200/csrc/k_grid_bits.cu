@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
 
     for (int round = 0; round < p.n_rounds; ++round) {
         int32_t *Ucnt = Ubuf[round & 1];
+        if (tid < 32)  // zeroed here: the colour-phase barriers order it before the atomicAdds
+            Ucnt[tid] = 0;
         // ---- k_ex sweeps
         for (int s = 0; s < p.k_ex; ++s) {
             const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + s);
@@ -301,8 +303,6 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
         // ---- energy: every bond joins a colour-0 and a colour-1 site, so the four
         // bonds of the colour-1 sites count each bond exactly once.  E = 2U - 2n.
         {
-            if (tid < 32)
-                Ucnt[tid] = 0;
             uint32_t c7[7];  // per-thread counts <= 4 * npass <= 124
 #pragma unroll
             for (int l = 0; l < 7; ++l)
@@ -331,9 +331,11 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
 #pragma unroll
             for (int l = 0; l < kCntLevels; ++l)
                 acc += (int32_t)((cnt[l] >> lane) & 1u) << l;
-            __syncthreads();  // Ucnt zeroed
+            if (p.k_ex == 0)  // no colour phase (hence no barrier) since the zeroing
+                __syncthreads();
             atomicAdd(&Ucnt[lane], acc);
-            __syncthreads();
+            if (!pt)  // pt_step opens with a cluster barrier
+                __syncthreads();
         }
         if (!pt)
             continue;
