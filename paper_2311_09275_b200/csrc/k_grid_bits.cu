@@ -105,6 +105,9 @@ size_t grid_bits_smem(int32_t n)
            (size_t)grid_bits_qcap(n) * kGridQItem + (size_t)8 * ((n + 31) / 32);
 }
 
+// SPILL: the lattice has leftover rows that the column-less warps take (grid_bits_spill);
+// a separate instantiation, so lattices without them keep the plain kernel's code
+template <bool SPILL>
 __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBitsParams p)
 {
     extern __shared__ __align__(16) uint32_t sm[];
@@ -146,6 +149,15 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
     // 2-D thread mapping: column m = tid % hx of a class row, rows ty + k*rpp
     const int rpp = grid_rows_per_pass(nt, G.hx);  // even when possible (host guarantees >= 1)
     const int npass = (G.Ly + rpp - 1) / rpp;
+    // leftover rows beyond the last full pass go to the warps without a class column when
+    // they can finish them within the full passes
+    const int full_passes = G.Ly / rpp, main_rows = full_passes * rpp;
+    const int idle_w0 = (rpp * G.hx + 31) / 32;  // first warp with no column thread
+    const int spill_sites = (G.Ly - main_rows) * G.hx;
+    const int nidle_all = (nwarps - idle_w0) * 32;
+    const int spill_iters = nidle_all > 0 ? (spill_sites + nidle_all - 1) / nidle_all : 0;
+    const bool spill = SPILL && spill_sites > 0 && nidle_all > 0 && spill_iters <= full_passes;
+    const int npass_main = spill ? full_passes : npass;
     // neighbour offsets of a class column: m+1 and m-1 wrapped, rows below/above wrapped
     const int offR1 = T_m_plus1_off(tid, G.hx), offL0 = T_m_minus1_off(tid, G.hx);
     const uint32_t hx4 = 4u * (uint32_t)G.hx;
@@ -211,7 +223,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
                 int wq = 0;  // warp-uniform
                 int y = T.ty;
 #pragma unroll 1
-                for (int pass = 0; pass < npass;
+                for (int pass = 0; pass < npass_main;
                      ++pass, y += rpp, aC += 4u * rstep, aO += 4u * rstep, aJ += rstep, i_orig += istep) {
                     const bool valid = T.active && y < G.Ly;
                     uint32_t own = 0, D = 0, acc = 0, m8 = 0;
@@ -256,6 +268,70 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
                             } while (D && j4 < 16u);
                         }
                         sts_u32(aC, own ^ acc);
+                    }
+                }
+                // leftover rows (Ly not a multiple of rpp): the warps that hold no class column
+                // take them, concurrently with the main passes, instead of a last partial pass
+                // of the column threads (C2: rows 96..99 on the 16th warp, 8 passes per warp
+                // instead of 9 for five warps)
+                if (SPILL && spill && warp >= idle_w0) {
+                    const int nidle = (nwarps - idle_w0) * 32, k0 = tid - idle_w0 * 32;
+#pragma unroll 1
+                    for (int it = 0; it < spill_iters; ++it) {
+                        const int sidx = it * nidle + k0;
+                        const bool valid = sidx < spill_sites;
+                        const int yy = main_rows + (valid ? sidx / hx : 0);
+                        const int mm = valid ? sidx - (sidx / hx) * hx : 0;
+                        const int pp = (c + yy) & 1;
+                        const uint32_t ll = (uint32_t)(yy * hx + mm);
+                        const uint32_t bC = sS + 4u * ((uint32_t)(c * G.half) + ll);
+                        const uint32_t bO = sS + 4u * ((uint32_t)((1 - c) * G.half) + ll);
+                        const uint32_t bJ = sJB + (uint32_t)(c * G.half) + ll;
+                        const int oR = pp ? (mm + 1 == hx ? 1 - hx : 1) : 0;
+                        const int oL = pp ? 0 : (mm == 0 ? hx - 1 : -1);
+                        const uint32_t io = (uint32_t)(2 * mm + pp + G.Lx * yy);
+                        uint32_t own = 0, D = 0, acc = 0, m8 = 0;
+                        if (valid) {
+                            own = lds_u32(bC);
+                            const uint32_t xr = lds_u32(bO + 4u * (uint32_t)oR);
+                            const uint32_t xl = lds_u32(bO + 4u * (uint32_t)oL);
+                            const uint32_t xd = lds_u32(bO + (yy + 1 == G.Ly ? wrapDb : hx4));
+                            const uint32_t xu = lds_u32(bO + (yy == 0 ? wrapUb : 0u - hx4));
+                            const uint32_t jw = lds_u8(bJ) * 0x10204080u;
+                            const uint32_t a0 = ~(own ^ xr ^ byte_sign_mask<0>(jw));
+                            const uint32_t a1 = ~(own ^ xl ^ byte_sign_mask<1>(jw));
+                            const uint32_t a2 = ~(own ^ xd ^ byte_sign_mask<2>(jw));
+                            const uint32_t a3 = ~(own ^ xu ^ byte_sign_mask<3>(jw));
+                            const uint32_t s01 = a0 ^ a1, c01 = a0 & a1;
+                            const uint32_t s23 = a2 ^ a3, c23 = a2 & a3;
+                            m8 = ~(s01 | c01 | s23 | c23);
+                            const uint32_t m4 = (s01 ^ s23) & ~(c01 | c23);
+                            D = m8 | m4;
+                            acc = ~D;
+                            if (D) {
+                                uint32_t sA, sB;
+                                plane_site(io, U, rkr, sA, sB);
+                                plane_call2(sA, sB, U, rkr, P, m8, D, acc);
+                            }
+                        }
+                        const bool need = D != 0u;
+                        const uint32_t pm = __ballot_sync(0xFFFFFFFFu, need);
+                        const int slot = wq + __popc(pm & lanemask_lt());
+                        wq += __popc(pm);
+                        if (need && slot < wcap) {
+                            Q4[wq0 + slot] = make_uint4(ll | (io << 16), D, acc, m8);
+                        } else if (valid) {
+                            if (need) {
+                                uint32_t sA, sB;
+                                plane_site(io, U, rkr, sA, sB);
+                                uint32_t j4 = 2;
+                                do {
+                                    plane_call(sA, sB, j4, U, rkr, P, m8, D, acc);
+                                    ++j4;
+                                } while (D && j4 < 16u);
+                            }
+                            sts_u32(bC, own ^ acc);
+                        }
                     }
                 }
 #ifdef ISING_GRID_TIMING
@@ -369,7 +445,14 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
 cudaError_t launch_grid_bits(const GridBitsParams &p, int32_t G, int32_t threads, size_t smem,
                              cudaStream_t st)
 {
-    cudaError_t e = cudaFuncSetAttribute(k_grid_bits, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    // the spilling instantiation only where the host-side geometry says rows are left over
+    // and the column-less warps can take them within the full passes (same rule as the kernel)
+    const int hx = p.hx, rpp = grid_rows_per_pass(threads, hx);
+    const int full = p.Ly / rpp, left = (p.Ly - full * rpp) * hx;
+    const int nidle = (threads / 32 - (rpp * hx + 31) / 32) * 32;
+    const bool spill = left > 0 && nidle > 0 && (left + nidle - 1) / nidle <= full;
+    auto kern = spill ? k_grid_bits<true> : k_grid_bits<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess)
         return e;
@@ -385,7 +468,7 @@ cudaError_t launch_grid_bits(const GridBitsParams &p, int32_t G, int32_t threads
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_grid_bits, p);
+    return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 }  // namespace ising

@@ -76,6 +76,7 @@ def bands(request, monkeypatch):
     (6, 4, 32, 3, 33, 7, 0),       # ragged: 12 sites per colour, odd copies, tail rounds
     (10, 8, 96, 2, 40, 5, 64),     # K = 96 (3 words per copy), small CTA
     (12, 20, 128, 1, 30, 10, 256),  # 4 words per copy
+    (48, 52, 32, 2, 30, 10, 320),   # 1 column-less warp takes the 4 leftover rows (as C2's 16th warp)
 ])
 def test_grid_bits_parity(Lx, Ly, K, C, sweeps, kex, threads, bands):
     inst = grid(Lx, Ly, 1000 + Lx * Ly)
