@@ -158,6 +158,10 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
     const int spill_iters = nidle_all > 0 ? (spill_sites + nidle_all - 1) / nidle_all : 0;
     const bool spill = SPILL && spill_sites > 0 && nidle_all > 0 && spill_iters <= full_passes;
     const int npass_main = spill ? full_passes : npass;
+    // per-warp stage-2 limit: about one 32-lane round of queued words per 8 passes (~11% of the
+    // words stay undecided after stage 1); beyond it a word is finished inline in stage 1, so a
+    // warp rarely pays a second, mostly empty stage-2 round after the others are done
+    const int wlim = min(wcap, 32 * max(1, (npass_main + 7) / 8));
     // neighbour offsets of a class column: m+1 and m-1 wrapped, rows below/above wrapped
     const int offR1 = T_m_plus1_off(tid, G.hx), offL0 = T_m_minus1_off(tid, G.hx);
     const uint32_t hx4 = 4u * (uint32_t)G.hx;
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
                     const uint32_t pm = __ballot_sync(0xFFFFFFFFu, need);
                     const int slot = wq + __popc(pm & lanemask_lt());
                     wq += __popc(pm);
-                    if (need && slot < wcap) {
+                    if (need && slot < wlim) {
                         const uint32_t l = (aC - sS) / 4u - (uint32_t)(c * G.half);
                         Q4[wq0 + slot] = make_uint4(l | (i_orig << 16), D, acc, m8);
                     } else if (valid) {
@@ -318,7 +322,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
                         const uint32_t pm = __ballot_sync(0xFFFFFFFFu, need);
                         const int slot = wq + __popc(pm & lanemask_lt());
                         wq += __popc(pm);
-                        if (need && slot < wcap) {
+                        if (need && slot < wlim) {
                             Q4[wq0 + slot] = make_uint4(ll | (io << 16), D, acc, m8);
                         } else if (valid) {
                             if (need) {
@@ -342,7 +346,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
 #endif
                 // stage 2 (own-queue variant): each warp finishes its own queued words right
                 // after its stage 1, no barrier in between
-                const int nown = min(wq, wcap);
+                const int nown = min(wq, wlim);
                 for (int qb = 0; qb < nown; qb += 32) {
                     const int q = qb + lane;
                     if (q >= nown)
