@@ -1279,7 +1279,15 @@ int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
     if (h->kernel == KER_GRID_BITS && h->K >= 2 && !h->fused_ok && h->xc_ok) {
         GridBitsParams p = grid_params(h, n_rounds, k_ex, true);
         p.xc = 1;
-        CK(launch_grid(h, p));
+        const cudaError_t le = launch_grid(h, p);
+        if (le == cudaErrorCooperativeLaunchTooLarge) {
+            // the copies' clusters no longer fit at once (e.g. another context holds SMs):
+            // per-round launches from now on, same results
+            cudaGetLastError();
+            h->xc_ok = false;
+            return ising_run(h, n_rounds, k_ex);
+        }
+        CK(le);
         h->cur ^= 1;
         CK(launch_merge_copy_best(h->d_copy_best, h->d_snap, h->C_local, h->n, h->d_best,
                                   h->d_best_spins, h->d_cbest, h->st));
