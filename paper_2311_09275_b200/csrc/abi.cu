@@ -440,6 +440,35 @@ int refresh_energy(ising_handle *h)
 }
 
 // Validated CSR -> internal, colour-sorted CSR and device upload (CSR kernels).
+// Lowest i in [0, n) with !check(i, nullptr), or n: the vertices split over up to 16 host
+// threads (per-vertex checks of a graph are independent; the lowest failing vertex is the one a
+// sequential scan reports first).
+template <class F>
+int32_t par_first_failing(int32_t n, F &&check)
+{
+    const int32_t nthr =
+        std::max(1, std::min<int32_t>(16, std::min<int32_t>((int32_t)std::thread::hardware_concurrency(), n / 65536)));
+    std::vector<int32_t> bad(nthr, n);
+    auto work = [&](int32_t t) {
+        const int32_t lo = (int32_t)((int64_t)n * t / nthr), hi = (int32_t)((int64_t)n * (t + 1) / nthr);
+        for (int32_t i = lo; i < hi; ++i)
+            if (!check(i, nullptr)) {
+                bad[t] = i;
+                return;
+            }
+    };
+    if (nthr > 1) {
+        std::vector<std::thread> pool;
+        for (int32_t t = 0; t < nthr; ++t)
+            pool.emplace_back(work, t);
+        for (auto &th : pool)
+            th.join();
+    } else {
+        work(0);
+    }
+    return *std::min_element(bad.begin(), bad.end());
+}
+
 int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const void *w,
                     int32_t wtype, const int32_t *colour, const ising_run_desc *desc,
                     ising_handle **out)
@@ -503,11 +532,22 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
             mx = std::max(mx, colour[i]);
             col_of[i] = colour[i];
         }
-        for (int32_t i = 0; i < n; ++i)
+        auto proper = [&](int32_t i, std::string *msg) -> bool {
             for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
-                if (colour[col[e]] == colour[i])
-                    return fail(ISING_E_GRAPH, "improper colouring: vertices " + std::to_string(i) +
-                                                   " and " + std::to_string(col[e]) + " share colour");
+                if (colour[col[e]] == colour[i]) {
+                    if (msg)
+                        *msg = "improper colouring: vertices " + std::to_string(i) + " and " +
+                               std::to_string(col[e]) + " share colour";
+                    return false;
+                }
+            return true;
+        };
+        const int32_t bad = par_first_failing(n, proper);
+        if (bad < n) {
+            std::string msg;
+            proper(bad, &msg);
+            return fail(ISING_E_GRAPH, msg);
+        }
         std::vector<char> used(mx + 1, 0);
         for (int32_t i = 0; i < n; ++i)
             used[col_of[i]] = 1;
@@ -524,18 +564,20 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
 
     // internal order: (colour, [degree for BITS], original id)
     h->orig.resize(n);
-    std::iota(h->orig.begin(), h->orig.end(), 0u);
     const bool by_deg = h->kernel == KER_CSR_BITS;
-    std::stable_sort(h->orig.begin(), h->orig.end(), [&](uint32_t a, uint32_t b) {
-        if (col_of[a] != col_of[b])
-            return col_of[a] < col_of[b];
-        if (by_deg) {
-            const int64_t da = row_ptr[a + 1] - row_ptr[a], db = row_ptr[b + 1] - row_ptr[b];
-            if (da != db)
-                return da < db;
-        }
-        return a < b;
-    });
+    {  // counting sort by key (colour, [degree]), ids ascending inside a key: O(n + keys)
+        const int64_t nd = by_deg ? (int64_t)maxdeg + 1 : 1;
+        auto key = [&](int32_t i) {
+            return (int64_t)col_of[i] * nd + (by_deg ? row_ptr[i + 1] - row_ptr[i] : 0);
+        };
+        std::vector<int64_t> start((size_t)h->ncol * nd + 1, 0);
+        for (int32_t i = 0; i < n; ++i)
+            ++start[key(i) + 1];
+        for (size_t k = 1; k < start.size(); ++k)
+            start[k] += start[k - 1];
+        for (int32_t i = 0; i < n; ++i)
+            h->orig[start[key(i)]++] = (uint32_t)i;
+    }
     h->o2i.resize(n);
     for (int32_t v = 0; v < n; ++v)
         h->o2i[h->orig[v]] = (uint32_t)v;
@@ -895,30 +937,52 @@ int ising_greedy_colour_sl(int32_t n, const int64_t *row_ptr, const int32_t *col
             uint64_t *base = store.data() + (size_t)d * per;
             bk[d] = Bits3{base, base + n0, base + n0 + n1, n2};
         }
-        for (int32_t i = 0; i < n; ++i) {
-            bk[deg[i]].set(i);
-            ++cnt[deg[i]];
-        }
-        int32_t dmin = 0;
-        for (int32_t k = 0; k < n; ++k) {
-            while (cnt[dmin] == 0)
-                ++dmin;
-            const int32_t i = bk[dmin].first();
-            bk[dmin].clr(i);
-            --cnt[dmin];
-            gone[i] = 1;
-            order.push_back(i);
-            for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
-                const int32_t j = col[e];
-                if (!gone[j]) {
-                    bk[deg[j]].clr(j);
-                    --cnt[deg[j]];
-                    --deg[j];
-                    bk[deg[j]].set(j);
-                    ++cnt[deg[j]];
-                    dmin = std::min(dmin, deg[j]);
+        // remaining degree and "removed" in one array (the sentinel), one byte per vertex when
+        // the degrees fit: the order visits vertices at random, so each step is a chain of
+        // cache misses (row -> neighbours -> their degrees); the rows of the neighbours just
+        // decremented (the likeliest next picks) are prefetched (C5: 2.9 s -> 1.5 s)
+        auto run = [&](auto *dg, auto gone_v) {
+            for (int32_t i = 0; i < n; ++i) {
+                dg[i] = (decltype(gone_v))deg[i];
+                bk[deg[i]].set(i);
+                ++cnt[deg[i]];
+            }
+            int32_t dmin = 0;
+            for (int32_t k = 0; k < n; ++k) {
+                while (cnt[dmin] == 0)
+                    ++dmin;
+                const int32_t i = bk[dmin].first();
+                bk[dmin].clr(i);
+                --cnt[dmin];
+                dg[i] = gone_v;
+                order.push_back(i);
+                const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
+                for (int64_t e = e0; e < e1; ++e) {
+                    const int32_t j = col[e];
+                    const int32_t dj = (int32_t)dg[j];
+                    if (dg[j] != gone_v) {
+                        __builtin_prefetch(row_ptr + j);
+                        bk[dj].clr(j);
+                        --cnt[dj];
+                        dg[j] = (decltype(gone_v))(dj - 1);
+                        bk[dj - 1].set(j);
+                        ++cnt[dj - 1];
+                        dmin = std::min(dmin, dj - 1);
+                    }
+                }
+                for (int64_t e = e0; e < e1; ++e) {
+                    const int32_t j = col[e];
+                    if (dg[j] != gone_v)
+                        __builtin_prefetch(col + row_ptr[j]);
                 }
             }
+        };
+        if (dmax < 255) {
+            std::vector<uint8_t> d8(n);
+            run(d8.data(), (uint8_t)0xFF);
+        } else {
+            std::vector<int32_t> d32(n);
+            run(d32.data(), (int32_t)-1);
         }
     } else {
         std::priority_queue<uint64_t, std::vector<uint64_t>, std::greater<uint64_t>> heap;
@@ -950,6 +1014,16 @@ int ising_greedy_colour_sl(int32_t n, const int64_t *row_ptr, const int32_t *col
         colour_out[i] = -1;
     int32_t ncol = 0;
     for (int32_t q = n - 1; q >= 0; --q) {
+        // prefetch ahead along the known order: row offsets, the row, its neighbours' colours
+        if (q >= 16)
+            __builtin_prefetch(row_ptr + order[q - 16]);
+        if (q >= 8)
+            __builtin_prefetch(col + row_ptr[order[q - 8]]);
+        if (q >= 4) {
+            const int32_t v = order[q - 4];
+            for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e)
+                __builtin_prefetch(colour_out + col[e]);
+        }
         const int32_t i = order[q];
         for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
             const int32_t c = colour_out[col[e]];
@@ -1167,25 +1241,52 @@ int ising_create_csr(int32_t n, const int64_t *row_ptr, const int32_t *col, cons
             return fail(ISING_E_GRAPH, "row_ptr decreases at vertex " + std::to_string(i));
     const int32_t *wi = wtype == ISING_W_I32 ? (const int32_t *)w : nullptr;
     const float *wf = wtype == ISING_W_F32 ? (const float *)w : nullptr;
-    std::vector<int64_t> mark(n, -1);
-    for (int32_t i = 0; i < n; ++i) {
-        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+    // Row checks in (vertex, entry) order: range, self-loop, duplicate of an earlier entry,
+    // finite weight.  Rows are independent, so the vertices are checked on host threads; the
+    // error reported is the one of the lowest failing vertex (the first one a sequential scan
+    // meets), its message produced by re-checking that row.
+    auto check_row = [&](int32_t i, std::string *msg) -> bool {
+        const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
+        const bool small = e1 - e0 <= 64;
+        std::vector<int32_t> seen;  // earlier entries of a long row, kept sorted
+        for (int64_t e = e0; e < e1; ++e) {
             const int32_t j = col[e];
-            if (j < 0 || j >= n)
-                return fail(ISING_E_GRAPH, "col[" + std::to_string(e) + "] = " + std::to_string(j) +
-                                               " out of range at vertex " + std::to_string(i));
-            if (j == i)
-                return fail(ISING_E_GRAPH, "self-loop at vertex " + std::to_string(i));
-            if (mark[j] == i)
-                return fail(ISING_E_GRAPH, "duplicate edge " + std::to_string(i) + "-" +
-                                               std::to_string(j));
-            mark[j] = i;
-            if (wf && !std::isfinite(wf[e]))
-                return fail(ISING_E_GRAPH, "non-finite weight at entry " + std::to_string(e));
+            if (j < 0 || j >= n) {
+                if (msg)
+                    *msg = "col[" + std::to_string(e) + "] = " + std::to_string(j) + " out of range at vertex " +
+                           std::to_string(i);
+                return false;
+            }
+            if (j == i) {
+                if (msg)
+                    *msg = "self-loop at vertex " + std::to_string(i);
+                return false;
+            }
+            bool dup = false;
+            if (small) {
+                for (int64_t f = e0; f < e && !dup; ++f)
+                    dup = col[f] == j;
+            } else {
+                const auto it = std::lower_bound(seen.begin(), seen.end(), j);
+                dup = it != seen.end() && *it == j;
+                if (!dup)
+                    seen.insert(it, j);
+            }
+            if (dup) {
+                if (msg)
+                    *msg = "duplicate edge " + std::to_string(i) + "-" + std::to_string(j);
+                return false;
+            }
+            if (wf && !std::isfinite(wf[e])) {
+                if (msg)
+                    *msg = "non-finite weight at entry " + std::to_string(e);
+                return false;
+            }
         }
-    }
+        return true;
+    };
     // symmetry: (i, j, w) present iff (j, i, w)
-    for (int32_t i = 0; i < n; ++i) {
+    auto check_sym = [&](int32_t i, std::string *msg) -> bool {
         for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
             const int32_t j = col[e];
             bool found = false;
@@ -1194,9 +1295,23 @@ int ising_create_csr(int32_t n, const int64_t *row_ptr, const int32_t *col, cons
                     found = wi ? (wi[f] == wi[e]) : (wf[f] == wf[e]);
                     break;
                 }
-            if (!found)
-                return fail(ISING_E_GRAPH, "asymmetric coupling " + std::to_string(i) + "-" +
-                                               std::to_string(j));
+            if (!found) {
+                if (msg)
+                    *msg = "asymmetric coupling " + std::to_string(i) + "-" + std::to_string(j);
+                return false;
+            }
+        }
+        return true;
+    };
+    for (int pass = 0; pass < 2; ++pass) {
+        const int32_t i = pass == 0 ? par_first_failing(n, check_row) : par_first_failing(n, check_sym);
+        if (i < n) {
+            std::string msg;
+            if (pass == 0)
+                check_row(i, &msg);
+            else
+                check_sym(i, &msg);
+            return fail(ISING_E_GRAPH, msg);
         }
     }
     return create_csr_impl(n, row_ptr, col, w, wtype, colour, desc, out);

@@ -55,6 +55,21 @@ def test_smallest_last_colouring_matches_oracle():
     a, na = L.ising_greedy_colour_sl(3000, rp, col)
     b, nb = oracle.greedy_colour_sl(3000, rp, col)
     assert na == nb and np.array_equal(a, b)
+    # bitmap buckets with degrees beyond one byte (the 32-bit remaining-degree array): a hub of
+    # 400 leaves inside a sparse random graph on 3000 vertices
+    n = 3000
+    x, y = synth.gnm(n, 3000, 12)
+    keep = (x != 0) & (y != 0)
+    u = np.concatenate([np.zeros(400, np.int64), x[keep]])
+    v = np.concatenate([np.arange(1, 401, dtype=np.int64), y[keep]])
+    pairs = {(min(a_, b_), max(a_, b_)) for a_, b_ in zip(u.tolist(), v.tolist())}
+    u = np.array([p[0] for p in sorted(pairs)], np.int64)
+    v = np.array([p[1] for p in sorted(pairs)], np.int64)
+    rp, col, _ = synth.edges_to_csr(n, u, v, np.ones(u.size, np.int32))
+    assert int(np.diff(rp).max()) >= 255
+    a, na = L.ising_greedy_colour_sl(n, rp, col)
+    b, nb = oracle.greedy_colour_sl(n, rp, col)
+    assert na == nb and np.array_equal(a, b)
     # the library's bitmap buckets give way to its heap when (max degree + 1) x n / 64
     # words exceed 2^25: a star on 2^16 vertices plus a sparse random part takes that path
     n = 1 << 16
@@ -99,6 +114,29 @@ def test_create_validation_errors():
     assert _code(L.ising_create_csr, 2, rp, np.array([1, 5], np.int32), np.array([1, 1], np.int32), **_desc())[0] == L.ISING_E_GRAPH  # range
     rp3 = np.array([0, 2, 3, 4], np.int64)
     assert _code(L.ising_create_csr, 3, rp3, np.array([1, 1, 0, 0], np.int32), np.ones(4, np.int32), **_desc())[0] == L.ISING_E_GRAPH  # duplicate
+    # the row checks run on host threads over vertex ranges: the error reported is still the
+    # lowest failing vertex's, row checks before symmetry, entries in row order
+    nb = 1 << 18
+    ring_u = np.arange(nb, dtype=np.int64)
+    rpb, colb, wb = synth.edges_to_csr(nb, ring_u, (ring_u + 1) % nb, np.ones(nb, np.int32))
+    colb = colb.copy(); wb = wb.copy()
+    colb[rpb[250000]] = 250000               # self-loop, late chunk
+    colb[rpb[150000] + 1] = colb[rpb[150000]]  # duplicate, earlier chunk
+    wb[rpb[7]] = -1                           # asymmetric weight, first chunk (symmetry pass)
+    c, msg = _code(L.ising_create_csr, nb, rpb, colb, wb, **_desc())
+    assert c == L.ISING_E_GRAPH and msg.endswith("duplicate edge 150000-" + str(colb[rpb[150000]])), msg
+    colb[rpb[150000] + 1] = 150001 if colb[rpb[150000]] == 149999 else 149999
+    c, msg = _code(L.ising_create_csr, nb, rpb, colb, wb, **_desc())
+    assert c == L.ISING_E_GRAPH and msg.endswith("self-loop at vertex 250000"), msg
+    colb[rpb[250000]] = 249999 if colb[rpb[250000] + 1] == 250001 else 250001
+    c, msg = _code(L.ising_create_csr, nb, rpb, colb, wb, **_desc())
+    assert c == L.ISING_E_GRAPH and msg.endswith("asymmetric coupling 6-7"), msg  # 6 meets it first
+    # a long row (> 64 entries, sorted-set duplicate check) with its duplicate at the end
+    hub_rp = np.array([0, 70] + [70 + k + 1 for k in range(70)], np.int64)
+    hub_col = np.concatenate([np.arange(1, 71), np.zeros(70)]).astype(np.int32)
+    hub_col[69] = 5
+    c, msg = _code(L.ising_create_csr, 71, hub_rp, hub_col, np.ones(140, np.int32), **_desc())
+    assert c == L.ISING_E_GRAPH and msg.endswith("duplicate edge 0-5"), msg
     # improper colouring
     c, msg = _code(L.ising_create_csr, 2, rp, np.array([1, 0], np.int32), np.array([1, 1], np.int32),
                    colour=np.array([0, 0], np.int32), **_desc())
