@@ -349,6 +349,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     total_ms, kernel_ms, nk, launches = 0.0, 0.0, 0, 0
+    step_ms = []  # this rank's per-step device times (the spread behind the mean)
     clocks.start()
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between timed steps (outside the timed events)
@@ -363,7 +364,8 @@ def run_ours(args):
         b.record(stream)
         torch.cuda.synchronize()
         launches += nl
-        total_ms += a.elapsed_time(b)
+        step_ms.append(a.elapsed_time(b))
+        total_ms += step_ms[-1]
         kernel_ms += sum(x.elapsed_time(y) for x, y in kev)
         nk += len(kev)
     clk = clocks.stop()
@@ -444,6 +446,7 @@ def run_ours(args):
         json_line({
             "metric": "spin-flip attempts/s", "value": value, "unit": "attempts/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "step_ms_rank0": {"median": float(np.median(step_ms)), "min": min(step_ms), "max": max(step_ms)},
             "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "u32" if cfg["layout"] == "bits" else ("f32" if cfg["kind"] == "regular" else "int32"),
             "data": "synthetic",
