@@ -5,16 +5,25 @@ Metric (BASELINE.json): spin-flip attempts/s (attempts = n x replicas x sweeps, 
 site of every replica counted once per sweep) at N GPUs, plus the
 fraction of the roofline of the dominant kernel.
 
-Workload at N=1 (BASELINE.json configs[1], the metric's config): 80x100 +-1 torus
-(G65 shape, Table I), 64 temperatures x 64 copies = 4096 replicas, beta
-0.1-3.0 geometric, 10,000 sweeps with a replica exchange every 10 sweeps, bit-packed
-spins.  One step = that whole schedule (1,000 rounds of 10 sweeps + best check +
-exchange) on inputs already resident on the GPU.  N>1: weak scaling -- every rank
-runs its own 64-copy shard (distinct global copy ids), local exchanges, and one NCCL
-all-gather of the per-rank best records per step.  C4 (--workload c4a|c4b) is strong
-scaling as BASELINE.json configs[3] states: 128 copies = 16,384 replicas in total, split
-over the N ranks (--copies overrides the copy count, e.g. --workload c4b --copies 16 runs
-one rank's share of the 8-GPU job on one GPU).
+Default workload (BASELINE.json configs[3], the config the metric "attempts/s at 1/2/4/8
+B200" is quoted on, and the largest single-GPU one): the 100x200 +-1 torus (G81 shape,
+PAPER.md:35 Table I), 128 temperatures x 128 copies = 16,384 replicas, beta 0.1-3.0
+geometric, 50,000 sweeps with a replica exchange every 10 sweeps, bit-packed spins.  One
+step = that whole schedule (5,000 rounds of 10 sweeps + best check + exchange) on inputs
+already resident on the GPU.  Strong scaling: the 128 copies are split over the N ranks
+(one process per GPU), exchanges are local to a copy, and one NCCL all-gather of the
+per-rank best records per step feeds the library's merge (ising_merge_best).
+
+The same JSON line carries:
+  * "c5": the HBM-bound stress config (BASELINE.json configs[4]: random 3-regular graph,
+    4e6 vertices, N(0,1) float32 couplings, 256 replicas per GPU, 1,000 sweeps) measured in
+    the same run (value, roofline against measured HBM, clocks, e2e);
+  * "scaling_projection" (N=1 only): one GPU's share of the N = 2/4/8 job (64/32/16 copies)
+    timed on this GPU, i.e. the strong-scaling efficiency the kernels allow;
+  * "roofline" of the dominant kernel against the MEASURED issue roof of its instruction mix
+    (tools/alu_peak.cu -> profiles/alu_peak.json) at the clock sampled in the timed region.
+Other workloads: --workload c1|c2|c3|c4a|c5 (c2/c3 weak scaling: a 64-copy shard per rank);
+--copies overrides the copy count (c4b --copies 16 = one rank's share of the 8-GPU job).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4a|c4b|c1|c5]
     python bench.py --impl reference ...   # the CPU oracle on the host cores
@@ -58,7 +67,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c4b", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sweeps", type=int, default=0, help="override sweeps per step")
     ap.add_argument("--no-e2e", action="store_true")
@@ -67,6 +76,9 @@ def parse():
                     help="copies override: per rank (weak-scaling workloads) or in total (c4a/c4b); "
                          "e.g. --workload c4b --copies 16 measures one rank's share at 8 GPUs")
     ap.add_argument("--threads", type=int, default=0, help="CTA size override")
+    ap.add_argument("--no-c5", action="store_true", help="skip the nested C5 (HBM-bound) record")
+    ap.add_argument("--no-projection", action="store_true",
+                    help="skip the one-GPU share runs of the strong-scaling workload (N = 2, 4, 8)")
     return ap.parse_args()
 
 
@@ -236,81 +248,115 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
-def roofline_entry(kernel_ms, attempts_per_launch, layout, clocks, workload="c2"):
-    """Roofline of the dominant kernel.  Bit-packed sweeps are issue (ALU) bound: achieved
-    = warp instructions per launch (ncu-measured per attempt, profiles/inst_per_attempt.json,
-    times the live attempts per launch) / live CUDA-event launch time; peak = 148 SMs x 4
-    schedulers x 1 warp-instruction/cycle x max SM clock."""
+ALU_PEAK_FILE = os.path.join(ROOT, "profiles", "alu_peak.json")
+
+
+def kernel_name(eng, inst, cfg, K, R, fused_one_launch):
+    if inst["kind"] == "grid" and cfg["layout"] == "bits":
+        if eng.info.fused_pt == 3:
+            return "k_grid_sched"
+        return "k_grid_bands" if eng.info.bands > 1 else "k_grid_bits"
+    if cfg["layout"] == "bits":
+        return "k_csr_bits"
+    if inst.get("w") is not None and inst["w"].dtype == np.float32 and R % 256 == 0:
+        return "k_csr_i8_ring"
+    if fused_one_launch:
+        return "k_i8_cluster" if K <= 64 else "k_i8_small"
+    return "k_csr_i8_phase"
+
+
+def roofline_entry(kernel_ms, attempts_per_launch, layout, clocks, ipa_key):
+    """Roofline of the dominant kernel.
+
+    int8 per-lane sweeps (C5) are HBM bound: achieved = algorithmic bytes per attempt (DESIGN.md
+    §5.4: 2 own + 3 neighbour + 0.11 CSR = 5.11 B) x attempts per launch / live CUDA-event launch
+    time, against MEASURED_PEAKS.json hbm_gbs.
+
+    Bit-packed sweeps (C2-C4) keep their state on chip and are issue (ALU) bound: achieved = warp
+    instructions per launch (ncu smsp__inst_executed.sum per attempt, profiles/inst_per_attempt.json,
+    times the live attempts per launch) / live launch time; peak = the MEASURED issue rate of the
+    PLANE instruction mix (tools/alu_peak.cu -> profiles/alu_peak.json, warp instructions per SM
+    cycle) x 148 SMs x the SM clock sampled during this run's timed region (SURVEY.md §8(d) "ALU
+    fraction ... at the same clock").  Falls back to the derived 4 issue/cycle/SM peak if the
+    microbenchmark has not been run."""
     peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
-    mhz = peaks.get("sm_max_mhz", 1965.0)
     ipa = None
     if os.path.exists(PROFILE_FILE):
-        ipa = json.load(open(PROFILE_FILE)).get(workload)
+        ipa = json.load(open(PROFILE_FILE)).get(ipa_key)
     if layout == "i8":
-        # int8 per-lane sweeps: HBM bound; algorithmic bytes per attempt stated in DESIGN.md
         bpa = ipa.get("alg_bytes_per_attempt", 5.11) if ipa else 5.11
         ach = attempts_per_launch * bpa / (kernel_ms * 1e-3) / 1e9
         peak = peaks.get("hbm_gbs", 6551.4)
         return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": (ipa or {}).get("dram_bytes_per_attempt") and
                 ipa["dram_bytes_per_attempt"] * attempts_per_launch,
+                "alg_bytes_per_attempt": bpa,
                 "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)"}
-    peak = 148 * 4 * mhz * 1e6 / 1e9  # Ginst/s (warp instructions)
+    mhz_max = peaks.get("sm_max_mhz", 1965.0)
+    mhz = (clocks or {}).get("sm_mhz") or mhz_max
+    alu = json.load(open(ALU_PEAK_FILE)) if os.path.exists(ALU_PEAK_FILE) else None
+    if alu:
+        peak = alu["warp_inst_per_sm_cycle"] * 148 * mhz * 1e6 / 1e9
+        src = (f"measured: tools/alu_peak.cu PLANE mix {alu['warp_inst_per_sm_cycle']:.3f} warp-inst per SM "
+               f"cycle (profiles/alu_peak.json) x 148 SMs x {mhz:.0f} MHz sampled in this timed region")
+    else:
+        peak = 148 * 4 * mhz * 1e6 / 1e9
+        src = f"derived: 148 SMs x 4 issue/cycle x {mhz:.0f} MHz (no alu_peak.json yet)"
     if not ipa:
         return {"bound": "alu", "achieved": None, "peak": peak, "unit": "Ginst/s", "frac": None,
-                "traffic": None, "note": "no ncu instruction count committed yet"}
+                "traffic": None, "peak_source": src, "note": "no ncu instruction count committed yet"}
     ach = attempts_per_launch * ipa["warp_inst_per_attempt"] / (kernel_ms * 1e-3) / 1e9
-    traffic = ipa.get("dram_bytes_per_attempt")
     if ipa.get("dram_bytes_per_launch") is not None:  # on-chip state: a fixed load/store per launch
         traffic_launch = ipa["dram_bytes_per_launch"]
     else:
-        traffic_launch = traffic * attempts_per_launch if traffic is not None else None
-    return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "Ginst/s", "frac": ach / peak,
-            "traffic": traffic_launch,
-            "peak_source": f"derived: 148 SMs x 4 issue/cycle x {mhz:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
-            "inst_per_attempt_source": ipa.get("source")}
+        t = ipa.get("dram_bytes_per_attempt")
+        traffic_launch = t * attempts_per_launch if t is not None else None
+    out = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "Ginst/s", "frac": ach / peak,
+           "traffic": traffic_launch, "peak_source": src,
+           "warp_inst_per_attempt": ipa["warp_inst_per_attempt"],
+           "inst_per_attempt_source": ipa.get("source"),
+           "frac_of_4_issue_per_cycle": ach / (148 * 4 * mhz * 1e-3)}
+    return out
 
 
-def run_ours(args):
+def measure(args, workload, world, rank, local, steps, warmup, e2e_steps, copies=0, sweeps=0,
+            cpu=True, quiet_cfg=False):
+    """Time `steps` steps of `workload` (one step = the whole schedule: all sweeps, exchanges and
+    best checks) after `warmup` untimed ones; returns this workload's JSON record (all ranks
+    compute it, rank 0 prints).  e2e_steps > 0 also times the public API from host arrays."""
     import torch
     import torch.distributed as dist
 
-    from paper_2311_09275_b200 import Engine
-    from paper_2311_09275_b200.driver import merge_best_over_ranks
+    from paper_2311_09275_b200.driver import Engine, merge_best_over_ranks
 
-    world, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = workload_params(args.workload, args.sweeps)
+    cfg = workload_params(workload, sweeps)
     inst = synth.make_instance(cfg)
     K, C = cfg["K"], cfg["C"]
-    if args.copies:
-        C = args.copies
+    if copies:
+        C = copies
     betas = synth.beta_ladder(K)
-    strong = args.workload in STRONG
+    strong = workload in STRONG
     if strong:  # BASELINE configs[3]: the 128 copies (16,384 replicas) are sharded over the ranks
         if C % world:
-            raise SystemExit(f"{args.workload}: {C} copies do not split over {world} ranks")
+            raise SystemExit(f"{workload}: {C} copies do not split over {world} ranks")
         Cg = C
         c_lo, c_hi = rank * C // world, (rank + 1) * C // world
     else:  # weak scaling: every rank runs a C-copy shard with distinct global ids
         Cg = C * world
         c_lo, c_hi = rank * C, (rank + 1) * C
-    stream = torch.cuda.current_stream()
-    eng = Engine(inst, K, Cg, betas, seed=synth.PHILOX_KEY, copy_begin=c_lo,
-                 copy_end=c_hi, layout=cfg["layout"], device=local,
-                 block_threads=args.threads, stream=stream.cuda_stream, colour=cfg.get("colouring"))
+    stream = torch.cuda.current_stream(local)
+    mk = dict(seed=synth.PHILOX_KEY, copy_begin=c_lo, copy_end=c_hi, layout=cfg["layout"], device=local,
+              block_threads=args.threads, stream=stream.cuda_stream, colour=cfg.get("colouring"))
+    eng = Engine(inst, K, Cg, betas, **mk)
     n, R = inst["n"], eng.R
-    sweeps, kex = cfg["sweeps"], cfg["k_ex"]
-    rounds = sweeps // kex if kex > 0 else 0
-    rem = sweeps - rounds * kex if kex > 0 else sweeps
-    attempts_step = n * R * sweeps  # this rank's attempts per step
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    sweeps_, kex = cfg["sweeps"], cfg["k_ex"]
+    rounds = sweeps_ // kex if kex > 0 else 0
+    rem = sweeps_ - rounds * kex if kex > 0 else sweeps_
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=torch.device("cuda", local))
 
-    # bit-packed kernels run all rounds in one launch (unless a band-split handle's clusters
-    # would not all be resident: then ising_run takes per-round launches, counted as such)
-    # (small int8 instances with integer weights, C1, also run all rounds in one launch)
+    # bit-packed kernels run all rounds in one launch (unless a band-split handle's clusters would
+    # not all be resident: then ising_run takes per-round launches, counted as such); small int8
+    # instances with integer weights (C1) also run all rounds in one launch
     fused = kex > 0 and (cfg["layout"] == "bits" or bool(eng.info.fused_pt))
     fused_one_launch = fused and bool(eng.info.fused_pt)
 
@@ -323,35 +369,39 @@ def run_ours(args):
         ev[1].record(stream)
         kev.append(ev)
 
-    def step(kev=None):
-        """One pass of the whole hot path over the workload; returns (our launches, best)."""
+    def schedule(e, kev=None):
+        """One pass of the whole hot path over the workload; returns our kernel launches."""
         launches = 0
         if fused:
-            # all rounds in ONE k_grid_bits launch (clusters exchange through DSMEM) + merge
-            timed(kev, eng.run, rounds, kex)
+            timed(kev, e.run, rounds, kex)
             launches += 2 if fused_one_launch else 3 * rounds
         else:
             for _ in range(rounds):
-                timed(kev, eng.sweep, kex)
-                eng.exchange()
-                launches += (1 if cfg["layout"] == "bits" else kex * eng.info.n_colours + 2) + 2
+                timed(kev, e.sweep, kex)
+                e.exchange()
+                launches += (1 if cfg["layout"] == "bits" else kex * e.info.n_colours + 2) + 2
         if rem:
-            timed(kev, eng.sweep, rem)
-            eng.check_best()
-            launches += (1 if cfg["layout"] == "bits" else rem * eng.info.n_colours + 2) + 1
+            timed(kev, e.sweep, rem)
+            e.check_best()
+            launches += (1 if cfg["layout"] == "bits" else rem * e.info.n_colours + 2) + 1
+        return launches
+
+    def step(kev=None):
+        launches = schedule(eng, kev)
         rec = eng.best(spins=False)
         if world > 1:
-            rec = merge_best_over_ranks(rec, None)
+            rec = merge_best_over_ranks(rec, None, engine=eng)
         return launches, rec
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     total_ms, kernel_ms, nk, launches = 0.0, 0.0, 0, 0
     step_ms = []  # this rank's per-step device times (the spread behind the mean)
+    rec = None
     clocks.start()
-    for _ in range(args.steps):
+    for _ in range(steps):
         flush.zero_()  # L2 flush between timed steps (outside the timed events)
         torch.cuda.synchronize()
         if world > 1:
@@ -369,104 +419,133 @@ def run_ours(args):
         kernel_ms += sum(x.elapsed_time(y) for x, y in kev)
         nk += len(kev)
     clk = clocks.stop()
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([total_ms], dtype=torch.float64, device=torch.device("cuda", local))
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    value = n * K * Cg * sweeps * args.steps / (total_ms * 1e-3)  # all ranks' attempts
-    ms_step = total_ms / args.steps
+    value = n * K * Cg * sweeps_ * steps / (total_ms * 1e-3)  # all ranks' attempts
     avg_launch_ms = kernel_ms / max(nk, 1)
-    per_launch_attempts = n * R * (rounds * kex if fused else (kex if kex > 0 else sweeps))
-    # instruction counts per attempt are kernel-specific: the band-split kernel has its own entry
-    ipa_key = args.workload + ("_bands" if eng.info.bands > 1 else "")
+    per_launch_attempts = n * R * (rounds * kex if fused else (kex if kex > 0 else sweeps_))
+    kname = kernel_name(eng, inst, cfg, K, R, fused_one_launch)
+    # instruction counts per attempt are kernel-specific
+    ipa_key = workload + {"k_grid_bands": "_bands", "k_grid_sched": "_sched"}.get(kname, "")
     roof = roofline_entry(avg_launch_ms, per_launch_attempts,
-                          "bits" if fused_one_launch else cfg["layout"], clk, ipa_key)
-    roof["kernel"] = ("k_grid_bands" if eng.info.bands > 1 else "k_grid_bits") \
-        if (inst["kind"] == "grid" and cfg["layout"] == "bits") else \
-        ("k_csr_bits" if cfg["layout"] == "bits" else
-         ("k_csr_i8_ring" if inst.get("w") is not None and inst["w"].dtype == np.float32 and R % 256 == 0
-          else (("k_i8_cluster" if K <= 64 else "k_i8_small") if fused_one_launch else "k_csr_i8_phase")))
-    if roof["kernel"] in ("k_i8_small", "k_i8_cluster"):
-        per = K // 8 if roof["kernel"] == "k_i8_cluster" else 1
+                          "bits" if cfg["layout"] == "bits" or fused_one_launch else cfg["layout"], clk, ipa_key)
+    roof["kernel"] = kname
+    if kname in ("k_i8_small", "k_i8_cluster"):
+        per = K // 8 if kname == "k_i8_cluster" else 1
         roof["note"] = (f"{per} CTA(s) per copy: {eng.R // K} copies use {per * (eng.R // K)} of the GPU's "
                         "SMs; frac is against the whole-GPU issue peak")
-    roof["kernel_share_of_step"] = kernel_ms / max(total_ms * (1 if world == 1 else 1), 1e-9)
+    roof["kernel_share_of_step"] = kernel_ms / max(sum(step_ms), 1e-9)
     roof["avg_launch_ms"] = avg_launch_ms
+    roof["attempts_per_launch"] = per_launch_attempts
 
     # ---- end to end through the public API with host buffers, every step
     e2e = None
-    if not args.no_e2e:
+    if e2e_steps > 0:
         e2e_ms = 0.0
-        h2d = d2h = 0
-        Jr = torch.from_numpy(inst["J_right"]).pin_memory() if inst["kind"] == "grid" else None
-        for s in range(args.warmup + args.steps):  # W untimed warm-up steps, then K timed
+        ew = min(warmup, 3)
+        for s in range(ew + e2e_steps):  # untimed warm-up steps, then timed ones
             torch.cuda.synchronize()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            e = Engine(inst, K, Cg, betas, seed=synth.PHILOX_KEY + s, copy_begin=c_lo,
-                       copy_end=c_hi, layout=cfg["layout"], device=local,
-                       block_threads=args.threads, stream=stream.cuda_stream,
-                       colour=cfg.get("colouring"))
-            if fused:
-                e.run(rounds, kex)
-            else:
-                for _ in range(rounds):
-                    e.sweep(kex)
-                    e.exchange()
-            if rem:
-                e.sweep(rem)
-                e.check_best()
-            rec = e.best(spins=True)
-            E = e.energies()
+            e = Engine(inst, K, Cg, betas, **{**mk, "seed": synth.PHILOX_KEY + s})
+            schedule(e)
+            e.best(spins=True)
+            e.energies()
             b.record(stream)
             torch.cuda.synchronize()
             e.close()
-            if s >= args.warmup:
+            if s >= ew:
                 e2e_ms += a.elapsed_time(b)
         if inst["kind"] == "grid":
             h2d = 2 * n + 8 * K
         else:
             h2d = 8 * (n + 1) + inst["col"].nbytes + inst["w"].nbytes + 8 * K
         d2h = 8 * R + n + 32
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=torch.device("cuda", local))
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = {"value": n * K * Cg * sweeps * args.steps / (float(t.item()) * 1e-3),
-               "unit": "attempts/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "includes": "create (validate, tables, upload, init) + full schedule + best/energy readback"}
+        ev = n * K * Cg * sweeps_ * e2e_steps / (float(t.item()) * 1e-3)
+        e2e = {"value": ev, "unit": "attempts/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "steps": e2e_steps, "frac_of_device_value": ev / value,
+               "includes": "create from host arrays (validate, colour, tables, upload, init) + full schedule "
+                           "+ best configuration / energies readback"}
+    eng.close()
+    del flush
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_oracle_sample(cfg)
+    cpu_rec = None
+    if rank == 0 and world == 1 and cpu:
+        cpu_rec = cpu_oracle_sample(cfg, target_s=12.0 if not quiet_cfg else 8.0)
 
+    peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
+    bpa = 0.25 if cfg["layout"] == "bits" else 5.11
+    return {
+        "metric": "spin-flip attempts/s", "value": value, "unit": "attempts/s",
+        "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": total_ms / steps,
+        "step_ms_rank0": {"median": float(np.median(step_ms)), "min": min(step_ms), "max": max(step_ms)},
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "u32" if cfg["layout"] == "bits" else ("f32" if cfg["kind"] == "regular" else "int32"),
+        "data": "synthetic",
+        "config": {"workload": workload, "description": WORKLOADS[workload],
+                   "n": n, "replicas_per_gpu": R, "sweeps_per_step": sweeps_, "exchange_every": kex,
+                   "copies_total": Cg, "copies_per_gpu": c_hi - c_lo,
+                   "parallelism": f"copies sharded over {world} GPU(s), "
+                                  + ("strong scaling (fixed total)" if strong else "weak scaling"),
+                   "l2": ("flushed between timed steps (256 MB write); the state is SMEM/L2-resident "
+                          "by design" if cfg["layout"] == "bits" or n * R < (64 << 20) else
+                          "flushed between timed steps (256 MB write); spins (%.2f GB) exceed L2"
+                          % (n * R / 1e9))},
+        "roofline": roof,
+        "hbm_frac": value / world * bpa / 1e9 / peaks.get("hbm_gbs", 6551.4),
+        "cpu_baseline": cpu_rec,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "best": {k: rec[k] for k in ("E", "slot", "sweep")} if rec else None,
+    }
+
+
+def scaling_projection(args, main_value, local):
+    """One GPU's share of the strong-scaling job at N = 2, 4, 8 (copies 64 / 32 / 16 of C4b's 128),
+    each timed on this GPU over 5,000 sweeps: projected N-GPU value = N x share rate, efficiency =
+    share rate / 1-GPU rate.  The N-GPU run adds one NCCL all-gather of 24-byte best records per
+    step (driver.merge_best_over_ranks), microseconds against seconds of sweeps."""
+    out = {}
+    cfg = workload_params(args.workload, 0)
+    for N in (2, 4, 8):
+        r = measure(args, args.workload, 1, 0, local, steps=2, warmup=1, e2e_steps=0,
+                    copies=cfg["C"] // N, sweeps=5000, cpu=False, quiet_cfg=True)
+        out[str(N)] = {"copies_per_gpu": cfg["C"] // N, "share_rate": r["value"],
+                       "projected_value": N * r["value"], "projected_efficiency": r["value"] / main_value,
+                       "kernel": r["roofline"]["kernel"], "sweeps": 5000}
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    e2e_steps = 0 if args.no_e2e else min(args.steps, 5)
+    line = measure(args, args.workload, world, rank, local, args.steps, args.warmup, e2e_steps,
+                   copies=args.copies, sweeps=args.sweeps, cpu=not args.no_cpu)
+    if args.workload in STRONG and world == 1 and not args.copies and not args.no_projection:
+        line["scaling_projection"] = scaling_projection(args, line["value"], local)
+    if args.workload != "c5" and not args.no_c5:
+        # the HBM-bound config (BASELINE.json configs[4], the north star's 60%-of-HBM target),
+        # measured in the same run: 256 replicas per GPU, weak scaling
+        c5 = measure(args, "c5", world, rank, local, min(args.steps, 5), min(args.warmup, 3),
+                     0 if args.no_e2e else min(args.steps, 3), cpu=not args.no_cpu, quiet_cfg=True)
+        line["c5"] = {k: c5[k] for k in ("value", "unit", "ms_per_step", "step_ms_rank0", "steps", "warmup",
+                                         "scaling", "dtype", "config", "roofline", "hbm_frac", "e2e",
+                                         "gpu_launches", "clocks", "cpu_baseline", "best")}
     if rank == 0:
-        peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
-        bpa = 0.25 if cfg["layout"] == "bits" else 5.11
-        json_line({
-            "metric": "spin-flip attempts/s", "value": value, "unit": "attempts/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "step_ms_rank0": {"median": float(np.median(step_ms)), "min": min(step_ms), "max": max(step_ms)},
-            "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
-            "dtype": "u32" if cfg["layout"] == "bits" else ("f32" if cfg["kind"] == "regular" else "int32"),
-            "data": "synthetic",
-            "config": {"workload": args.workload, "description": WORKLOADS[args.workload],
-                       "n": n, "replicas_per_gpu": R, "sweeps_per_step": sweeps, "exchange_every": kex,
-                       "copies_total": Cg, "copies_per_gpu": c_hi - c_lo,
-                       "parallelism": f"copies sharded over {world} GPU(s), "
-                                      + ("strong scaling (fixed total)" if strong else "weak scaling"),
-                       "l2": ("flushed between timed steps (256 MB write); the state is SMEM/L2-resident "
-                              "by design" if cfg["layout"] == "bits" or n * R < (64 << 20) else
-                              "flushed between timed steps (256 MB write); spins (%.2f GB) exceed L2"
-                              % (n * R / 1e9))},
-            "roofline": roof,
-            "hbm_frac": value / world * bpa / 1e9 / peaks.get("hbm_gbs", 6551.4),
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches,
-            "clocks": clk,
-            "best": {k: rec[k] for k in ("E", "slot", "sweep")},
-        })
+        json_line(line)
     if world > 1:
         dist.destroy_process_group()
 

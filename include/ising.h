@@ -100,6 +100,15 @@ typedef struct {
     int64_t slot;
 } ising_record;
 
+/* Best record of one rank for ising_merge_best (24 bytes): energy (int64, or the bits of a
+ * double for float weights), the sweep t at which it was reached, its GLOBAL slot (< 0: the
+ * rank has no record yet). */
+typedef struct {
+    int64_t energy;
+    int64_t sweep;
+    int64_t slot;
+} ising_best_record;
+
 typedef struct {
     int32_t n;            /* vertices */
     int32_t n_colours;    /* colour classes swept per sweep */
@@ -114,7 +123,9 @@ typedef struct {
     double W_f64;         /* sum of weights (float weights, float64 sum in edge order) */
     int32_t bands;        /* grid BITS: rows of a word group split over this many CTAs (1 or 2) */
     int32_t fused_pt;     /* 1 if ising_run runs all rounds in one launch; 2: one cooperative launch
-                             whose copies span K/32 clusters (band split); 0: per-round launches */
+                             whose copies span K/32 clusters (band split); 3: one persistent
+                             ticket-scheduled launch (grid BITS with more word groups than
+                             resident CTAs); 0: per-round launches */
 } ising_info_t;
 
 /* Create from a periodic Lx x Ly grid (torus).  Site i = x + Lx*y; J_right[i]
@@ -206,6 +217,16 @@ ISING_API int ising_exchange_end(ising_handle *h, const void *dev_recv, int64_t 
  * local slots.  Used at the end of a run whose length is not a multiple of the
  * exchange interval. */
 ISING_API int ising_check_best(ising_handle *h, const void *dev_recv, int64_t n_records);
+
+/* Global best over per-rank best records (syncs): multi-process runs whose ranks keep local
+ * best-so-far records gather every rank's ising_best into DEVICE memory (e.g. one NCCL
+ * all-gather of n ising_best_record) and merge them here: the lexicographic minimum of
+ * (energy, sweep, slot) -- the lowest energy, first reached, then the lowest slot --
+ * computed by one kernel on the handle's stream.  best_E: int64* or double* (per the handle's
+ * weights); slot, sweep: the winner's.  Errors: ISING_E_ARG (NULL, n < 1), ISING_E_STATE (no
+ * record has a slot). */
+ISING_API int ising_merge_best(ising_handle *h, const void *dev_recs, int64_t n, void *best_E, int64_t *slot,
+                               int64_t *sweep);
 
 /* Best record (syncs).  best_E: int64* or double*; slot: global slot; sweep: the t
  * at which it was first reached (strict <).  spins_out (n int8, original ids,

@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -26,13 +27,31 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def _deps():
+    return sorted(sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  [os.path.join(HERE, "..", "include", "ising.h")])
+
+
+def source_hash() -> str:
+    """sha256 over the library's sources (content, not mtimes: snapshots may not keep them)
+    and the compiler flags."""
+    h = hashlib.sha256(" ".join(FLAGS).encode())
+    for d in _deps():
+        h.update(os.path.basename(d).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
+HASH = LIB + ".srchash"
+
+
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    """True if libising.so is missing or was built from other sources than the tree's."""
+    if not os.path.exists(LIB) or not os.path.exists(HASH):
         return True
-    t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
-    deps.append(os.path.join(HERE, "..", "include", "ising.h"))
-    return any(os.path.getmtime(d) > t for d in deps)
+    with open(HASH) as f:
+        return f.read().strip() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -50,6 +69,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         print(res.stdout + res.stderr)
     os.replace(tmp, LIB)
+    with open(HASH, "w") as f:
+        f.write(source_hash())
     return LIB
 
 

@@ -110,6 +110,10 @@ struct ising_handle {
     int32_t bands = 1;    // grid BITS: row bands per word group (CTA pairs with DSMEM halos)
     bool fused_ok = true; // grid BITS: the fused PT launch's clusters (K/32 x bands CTAs per copy) fit one wave
     bool xc_ok = false;   // grid BITS, 2 bands: cooperative fused launch with copies over K/32 clusters
+    bool sched_ok = false;     // grid BITS, 1 band: persistent ticket-scheduled fused launch (k_grid_sched)
+    int32_t sched_ctas = 0;    // its resident CTAs
+    uint32_t *d_xs_ctl = nullptr, *d_xs_B = nullptr, *d_xs_M = nullptr;
+    int64_t *d_xs_E = nullptr;
     int64_t *d_xc_E = nullptr;
     uint32_t *d_xc_B = nullptr, *d_xc_bar = nullptr;
     std::vector<int32_t> class_off;
@@ -137,6 +141,7 @@ struct ising_handle {
     int64_t *d_cbest = nullptr;      // persistent per-copy best-so-far (E, slot, sweep)
     int8_t *d_snap = nullptr;        // fused PT launches: per-copy best configuration
     int8_t *d_best_spins = nullptr, *d_tmp = nullptr;
+    int64_t *d_merge = nullptr;      // ising_merge_best result (E, sweep, slot)
     void *d_scratch = nullptr;
     size_t scratch_bytes = 0;
     std::vector<void *> allocs;
@@ -205,6 +210,16 @@ int validate_desc(const ising_run_desc *d)
         return fail(ISING_E_ARG, "I8 layout requires n_temps % 8 == 0");
     if ((int64_t)d->n_copies * d->n_temps >= (int64_t)1 << 33)
         return fail(ISING_E_ARG, "too many replicas");
+    // the int8 kernels index local replicas with int32 (R and R/8 threads per vertex)
+    if (d->layout == ISING_SPINS_I8 && (int64_t)(d->copy_end - d->copy_begin) * d->n_temps >= (int64_t)1 << 31)
+        return fail(ISING_E_UNSUPPORTED, "I8 layout: local replicas must be < 2^31");
+    if (d->stream) {  // a stream of another device would run the handle's work on the wrong GPU
+        int sdev = -1;
+        if (cudaStreamGetDevice((cudaStream_t)d->stream, &sdev) == cudaSuccess && sdev != d->device)
+            return fail(ISING_E_ARG, "stream belongs to device " + std::to_string(sdev) + ", desc->device is " +
+                                         std::to_string(d->device));
+        cudaGetLastError();
+    }
     if (d->block_threads != 0 && (d->block_threads < 32 || d->block_threads > 1024 ||
                                   d->block_threads % 32 != 0))
         return fail(ISING_E_ARG, "block_threads must be 0 or a multiple of 32 in [32, 1024]");
@@ -296,6 +311,7 @@ int build_common_device(ising_handle *h, int64_t sum_abs_w)
         CK(cudaStreamSynchronize(h->st));
     }
     CK(h->alloc(&h->d_best_spins, h->n));
+    CK(h->alloc(&h->d_merge, 3));
     CK(h->alloc(&h->d_tmp, h->n));
     std::vector<int64_t> walker(h->R);
     std::iota(walker.begin(), walker.end(), h->slot0);
@@ -380,6 +396,11 @@ GridBitsParams grid_params(ising_handle *h, int32_t n_rounds, int32_t k_ex, bool
     p.xc_E = h->d_xc_E;
     p.xc_B = h->d_xc_B;
     p.xc_bar = h->d_xc_bar;
+    p.n_groups = h->G;
+    p.xs_ctl = h->d_xs_ctl;
+    p.xs_E = h->d_xs_E;
+    p.xs_B = h->d_xs_B;
+    p.xs_M = h->d_xs_M;
     return p;
 }
 
@@ -1168,6 +1189,32 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
             h->xc_ok = true;
         }
     }
+    // more word groups than resident CTAs (C4 on 1-2 GPUs): the fused PT launch as a persistent
+    // ticket-scheduled kernel (k_grid_sched) instead of waves of clusters.
+    // ISING_GRID_SCHED=0|1 overrides the choice (tests, measurements).
+    if (h->bands == 1 && h->K >= 2) {
+        CK(cudaSetDevice(h->device));
+        const int32_t full = Ly / rpp, left = (Ly - full * rpp) * hx;
+        const int32_t nidle = (h->threads / 32 - (rpp * hx + 31) / 32) * 32;
+        const bool spill = left > 0 && nidle > 0 && (left + nidle - 1) / nidle <= full;
+        const int32_t ctas = grid_sched_ctas(h->threads, h->smem, spill);
+        bool want = ctas > 0 && h->G > ctas;
+        if (const char *env = std::getenv("ISING_GRID_SCHED")) {
+            const int v = std::atoi(env);
+            if (v != 0 && v != 1)
+                return fail(ISING_E_ARG, "ISING_GRID_SCHED must be 0 or 1");
+            want = v == 1 && ctas > 0;
+        }
+        if (want) {
+            const size_t nbw = ((size_t)n + 31) / 32;
+            CK(h->alloc(&h->d_xs_ctl, 1 + 2 * (size_t)h->C_local));
+            CK(h->alloc(&h->d_xs_E, (size_t)h->G * 32));
+            CK(h->alloc(&h->d_xs_B, (size_t)2 * h->G * 2 * nbw));
+            CK(h->alloc(&h->d_xs_M, (size_t)h->C_local * h->wpc));
+            h->sched_ok = true;
+            h->sched_ctas = std::min(ctas, h->G);
+        }
+    }
     // J bytes in colour-separated order: bit 0..3 = (right, left, down, up) bond has J = -1
     std::vector<uint8_t> jb(n);
     for (int32_t c = 0; c < 2; ++c)
@@ -1391,6 +1438,29 @@ int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
         h->e += (uint32_t)n_rounds;
         return ISING_OK;
     }
+    if (h->kernel == KER_GRID_BITS && h->K >= 2 && h->sched_ok) {
+        // persistent ticket-scheduled launches; tasks (group, round) are counted in int32
+        const int32_t max_rounds = (int32_t)std::max<int64_t>(1, (((int64_t)1 << 31) - 1) / h->G);
+        for (int32_t r0 = 0; r0 < n_rounds; r0 += max_rounds) {
+            const int32_t nr = std::min(max_rounds, n_rounds - r0);
+            GridBitsParams p = grid_params(h, nr, k_ex, true);
+            const cudaError_t le = launch_grid_sched(p, h->sched_ctas, h->threads, h->smem, h->st);
+            if (le == cudaErrorCooperativeLaunchTooLarge) {
+                // fewer SMs available than at create (e.g. another context): the cluster launch
+                // from now on, same results
+                cudaGetLastError();
+                h->sched_ok = false;
+                return ising_run(h, n_rounds - r0, k_ex);
+            }
+            CK(le);
+            h->cur ^= 1;
+            CK(launch_merge_copy_best(h->d_copy_best, h->d_snap, h->C_local, h->n, h->d_best,
+                                      h->d_best_spins, h->d_cbest, h->st));
+            h->t += (uint32_t)(nr * k_ex);
+            h->e += (uint32_t)nr;
+        }
+        return ISING_OK;
+    }
     if (h->kernel == KER_GRID_BITS && h->K >= 2 && !h->fused_ok && h->xc_ok) {
         GridBitsParams p = grid_params(h, n_rounds, k_ex, true);
         p.xc = 1;
@@ -1450,69 +1520,81 @@ int ising_anneal(ising_handle *h, int32_t n_sweeps, const double *sched)
             return fail(ISING_E_ARG, "schedule entry " + std::to_string(x) + " must be finite and > 0");
     if (n_sweeps == 0)
         return ISING_OK;
-    // per-sweep tables, same formulas as the fixed ladder
-    std::vector<uint8_t> host;
+    // per-sweep tables, same formulas as the fixed ladder, built and
+    // uploaded in chunks of sweeps so the table never exceeds kAnnealChunkBytes on the host or
+    // the device (a chunk's launches equal the same sweeps in one launch: every random number is
+    // keyed by the sweep counter t)
+    size_t per_sweep = 0;
+    std::vector<int32_t> qs;
     if (h->layout == ISING_SPINS_BITS) {
-        std::vector<int32_t> qs;
         if (h->kernel == KER_GRID_BITS)
             qs = {2, 4};
         else
             for (int32_t q = 1; q <= h->qmax; ++q)
                 qs.push_back(q);
-        std::vector<uint32_t> all, planes;
-        for (int32_t s = 0; s < n_sweeps; ++s) {
-            std::vector<double> row(sched + (size_t)s * h->K, sched + (size_t)(s + 1) * h->K);
-            plane_table(row, qs, planes);
-            all.insert(all.end(), planes.begin(), planes.end());
-        }
-        host.resize(all.size() * 4);
-        std::memcpy(host.data(), all.data(), host.size());
+        per_sweep = (size_t)h->wpc * qs.size() * 64 * 4;
     } else if (h->wtype == ISING_W_I32) {
-        const size_t per = (size_t)h->R * (h->qmax + 1);
-        std::vector<uint64_t> all(per * n_sweeps);
-        for (int32_t s = 0; s < n_sweeps; ++s)
-            for (int64_t r = 0; r < h->R; ++r) {
-                const double beta = sched[(size_t)s * h->K + (h->slot0 + r) % h->K];
-                all[s * per + r * (h->qmax + 1)] = std::numeric_limits<uint64_t>::max();
-                for (int32_t q = 1; q <= h->qmax; ++q)
-                    all[s * per + r * (h->qmax + 1) + q] = metropolis_threshold(beta, 2 * (int64_t)q);
+        per_sweep = (size_t)h->R * (h->qmax + 1) * 8;
+    } else {
+        per_sweep = (size_t)h->R * 4;
+    }
+    constexpr size_t kAnnealChunkBytes = 64u << 20;
+    const int32_t chunk = (int32_t)std::max<size_t>(1, std::min<size_t>(n_sweeps, kAnnealChunkBytes / per_sweep));
+    std::vector<uint8_t> host;
+    for (int32_t s0 = 0; s0 < n_sweeps; s0 += chunk) {
+        const int32_t ns = std::min(chunk, n_sweeps - s0);
+        const double *sc = sched + (size_t)s0 * h->K;
+        host.resize(per_sweep * ns);
+        if (h->layout == ISING_SPINS_BITS) {
+            std::vector<uint32_t> planes;
+            for (int32_t s = 0; s < ns; ++s) {
+                std::vector<double> row(sc + (size_t)s * h->K, sc + (size_t)(s + 1) * h->K);
+                plane_table(row, qs, planes);
+                std::memcpy(host.data() + s * per_sweep, planes.data(), per_sweep);
             }
-        host.resize(all.size() * 8);
-        std::memcpy(host.data(), all.data(), host.size());
-    } else {
-        std::vector<float> all((size_t)h->R * n_sweeps);
-        for (int32_t s = 0; s < n_sweeps; ++s)
-            for (int64_t r = 0; r < h->R; ++r)
-                all[(size_t)s * h->R + r] = 2.0f * (float)sched[(size_t)s * h->K + (h->slot0 + r) % h->K];
-        host.resize(all.size() * 4);
-        std::memcpy(host.data(), all.data(), host.size());
-    }
-    CK(cudaStreamSynchronize(h->st));  // the previous schedule buffer may still be in use
-    if (host.size() > h->sched_bytes) {
-        if (h->d_sched)
-            cudaFree(h->d_sched);
-        h->d_sched = nullptr;
-        h->sched_bytes = 0;
-        CK(cudaMalloc(&h->d_sched, host.size()));
-        h->sched_bytes = host.size();
-    }
-    CK(cudaMemcpyAsync(h->d_sched, host.data(), host.size(), cudaMemcpyHostToDevice, h->st));
-    if (h->kernel == KER_GRID_BITS) {
-        GridBitsParams p = grid_params(h, 1, n_sweeps, false);
-        p.planes_sched = (const uint32_t *)h->d_sched;
-        CK(launch_grid(h, p));
-        h->cur ^= 1;
-        h->t += (uint32_t)n_sweeps;
-    } else if (h->kernel == KER_CSR_BITS) {
-        CsrBitsParams p = csr_params(h, 1, n_sweeps, false);
-        p.planes_sched = (const uint32_t *)h->d_sched;
-        CK(launch_csr_bits(p, h->G, h->threads, h->smem, h->st));
-        h->cur ^= 1;
-        h->t += (uint32_t)n_sweeps;
-    } else {
-        rc = launch_sweeps_i8(h, n_sweeps, h->d_sched);
-        if (rc)
-            return rc;
+        } else if (h->wtype == ISING_W_I32) {
+            uint64_t *all = (uint64_t *)host.data();
+            const size_t per = (size_t)h->R * (h->qmax + 1);
+            for (int32_t s = 0; s < ns; ++s)
+                for (int64_t r = 0; r < h->R; ++r) {
+                    const double beta = sc[(size_t)s * h->K + (h->slot0 + r) % h->K];
+                    all[s * per + r * (h->qmax + 1)] = std::numeric_limits<uint64_t>::max();
+                    for (int32_t q = 1; q <= h->qmax; ++q)
+                        all[s * per + r * (h->qmax + 1) + q] = metropolis_threshold(beta, 2 * (int64_t)q);
+                }
+        } else {
+            float *all = (float *)host.data();
+            for (int32_t s = 0; s < ns; ++s)
+                for (int64_t r = 0; r < h->R; ++r)
+                    all[(size_t)s * h->R + r] = 2.0f * (float)sc[(size_t)s * h->K + (h->slot0 + r) % h->K];
+        }
+        CK(cudaStreamSynchronize(h->st));  // the previous chunk's table may still be in use
+        if (host.size() > h->sched_bytes) {
+            if (h->d_sched)
+                cudaFree(h->d_sched);
+            h->d_sched = nullptr;
+            h->sched_bytes = 0;
+            CK(cudaMalloc(&h->d_sched, host.size()));
+            h->sched_bytes = host.size();
+        }
+        CK(cudaMemcpyAsync(h->d_sched, host.data(), host.size(), cudaMemcpyHostToDevice, h->st));
+        if (h->kernel == KER_GRID_BITS) {
+            GridBitsParams p = grid_params(h, 1, ns, false);
+            p.planes_sched = (const uint32_t *)h->d_sched;
+            CK(launch_grid(h, p));
+            h->cur ^= 1;
+            h->t += (uint32_t)ns;
+        } else if (h->kernel == KER_CSR_BITS) {
+            CsrBitsParams p = csr_params(h, 1, ns, false);
+            p.planes_sched = (const uint32_t *)h->d_sched;
+            CK(launch_csr_bits(p, h->G, h->threads, h->smem, h->st));
+            h->cur ^= 1;
+            h->t += (uint32_t)ns;
+        } else {
+            rc = launch_sweeps_i8(h, ns, h->d_sched);
+            if (rc)
+                return rc;
+        }
     }
     CK(cudaStreamSynchronize(h->st));  // host table buffer goes out of scope
     return do_exchange(h, nullptr, 0, false);  // best-so-far check after the anneal
@@ -1595,6 +1677,26 @@ int ising_check_best(ising_handle *h, const void *dev_recv, int64_t n_records)
     if (dev_recv && n_records < 1)
         return fail(ISING_E_ARG, "n_records < 1");
     return do_exchange(h, dev_recv, dev_recv ? n_records : 0, false);
+}
+
+int ising_merge_best(ising_handle *h, const void *dev_recs, int64_t n, void *best_E, int64_t *slot,
+                     int64_t *sweep)
+{
+    int rc = check_handle(h);
+    if (rc)
+        return rc;
+    if (!dev_recs || n < 1 || !best_E || !slot || !sweep)
+        return fail(ISING_E_ARG, "NULL argument or n < 1");
+    CK(launch_merge_best((const int64_t *)dev_recs, n, h->wtype == ISING_W_F32 ? 1 : 0, h->d_merge, h->st));
+    int64_t out[3];
+    CK(cudaMemcpyAsync(out, h->d_merge, sizeof(out), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (out[2] < 0)
+        return fail(ISING_E_STATE, "no record holds a slot");
+    std::memcpy(best_E, &out[0], 8);
+    *sweep = out[1];
+    *slot = out[2];
+    return ISING_OK;
 }
 
 int ising_best(ising_handle *h, void *best_E, int64_t *slot, int64_t *sweep, int8_t *spins_out)
@@ -1736,6 +1838,8 @@ int ising_info(const ising_handle *h, ising_info_t *out)
                     small_i8(h);
     if (h->kernel == KER_GRID_BITS && h->K >= 2 && !h->fused_ok && h->xc_ok)
         out->fused_pt = 2;  // one cooperative launch; each copy spans K/32 clusters
+    if (h->kernel == KER_GRID_BITS && h->K >= 2 && h->sched_ok)
+        out->fused_pt = 3;  // one persistent ticket-scheduled launch (k_grid_sched)
     return ISING_OK;
 }
 

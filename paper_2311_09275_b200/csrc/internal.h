@@ -81,6 +81,12 @@ struct GridBitsParams {
     int64_t *xc_E;             // [C_local][2][K] word types' energies, by round parity
     uint32_t *xc_B;            // [C_local][2][K/32][2 bands][2 planes][nbw], by round parity
     uint32_t *xc_bar;          // [C_local] copy barrier counters (zero at launch)
+    // persistent ticket-scheduled launch (k_grid_sched): tasks = (local word group, round)
+    int32_t n_groups;          // local word groups G
+    uint32_t *xs_ctl;          // [1 + 2 C_local]: ticket, per-copy finished tasks, published rounds
+    int64_t *xs_E;             // [G][32] energies of the group's last round
+    uint32_t *xs_B;            // [2][G][2][nbw] bit 0 / bit 31 planes of each site, by round parity
+    uint32_t *xs_M;            // [C_local][K/32] swap mask of the copy's last exchange
 };
 
 struct CsrBitsParams {
@@ -213,6 +219,10 @@ size_t grid_bits_smem(int32_t n);
 cudaError_t launch_grid_bands(const GridBitsParams &p, int32_t G, int32_t threads, size_t smem,
                               cudaStream_t st);
 int32_t grid_bands_max_clusters(int32_t cluster, int32_t threads, size_t smem);
+// persistent ticket-scheduled fused PT launch (k_grid_sched.cu): `ctas` resident CTAs
+cudaError_t launch_grid_sched(const GridBitsParams &p, int32_t ctas, int32_t threads, size_t smem,
+                              cudaStream_t st);
+int32_t grid_sched_ctas(int32_t threads, size_t smem, bool spill);
 int32_t grid_bits_qcap(int32_t n);
 cudaError_t launch_csr_bits(const CsrBitsParams &p, int32_t G, int32_t threads, size_t smem,
                             cudaStream_t st);
@@ -235,6 +245,8 @@ cudaError_t launch_swap_i8(int8_t *s, const uint32_t *swapmask, int32_t n, int32
                            cudaStream_t st);
 cudaError_t launch_records(const int64_t *E, ising_record *out, int64_t R, int64_t slot0,
                            cudaStream_t st);
+cudaError_t launch_merge_best(const int64_t *recs, int64_t n, int32_t is_float, int64_t *out,
+                              cudaStream_t st);
 cudaError_t launch_extract_bits(const uint32_t *state, int32_t n, int32_t gl, int32_t bit,
                                 const uint32_t *perm_o2i, int8_t *out, cudaStream_t st);
 cudaError_t launch_insert_bits(uint32_t *state, int32_t n, int32_t gl, int32_t bit,

@@ -373,6 +373,61 @@ cudaError_t launch_records(const int64_t *E, ising_record *out, int64_t R, int64
     return cudaGetLastError();
 }
 
+// Global best over per-rank best records {E, sweep, slot} (slot < 0: none): the
+// lexicographic minimum of (E, sweep, slot) -- lowest energy, then first reached, then lowest
+// slot -- as multi-process runs merge their ranks' ising_best records
+// (ising_merge_best).  E is an int64 or the bits of a double.  One CTA; out[3] = the winner
+// (slot -1 if no record has one).
+__device__ __forceinline__ bool best_less(const int64_t *a, const int64_t *b, int32_t is_float)
+{
+    if (b[2] < 0)
+        return a[2] >= 0;
+    if (a[2] < 0)
+        return false;
+    if (is_float) {
+        const double ea = __longlong_as_double(a[0]), eb = __longlong_as_double(b[0]);
+        if (ea != eb)
+            return ea < eb;
+    } else if (a[0] != b[0]) {
+        return a[0] < b[0];
+    }
+    return a[1] != b[1] ? a[1] < b[1] : a[2] < b[2];
+}
+
+__global__ void k_merge_best(const int64_t *recs, int64_t n, int32_t is_float, int64_t *out)
+{
+    __shared__ int64_t sk[1024][3];
+    int64_t k[3] = {0, -1, -1};
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int64_t c[3] = {recs[3 * i], recs[3 * i + 1], recs[3 * i + 2]};
+        if (best_less(c, k, is_float)) {
+            k[0] = c[0];
+            k[1] = c[1];
+            k[2] = c[2];
+        }
+    }
+    sk[threadIdx.x][0] = k[0];
+    sk[threadIdx.x][1] = k[1];
+    sk[threadIdx.x][2] = k[2];
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s && best_less(sk[threadIdx.x + s], sk[threadIdx.x], is_float)) {
+            sk[threadIdx.x][0] = sk[threadIdx.x + s][0];
+            sk[threadIdx.x][1] = sk[threadIdx.x + s][1];
+            sk[threadIdx.x][2] = sk[threadIdx.x + s][2];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < 3)
+        out[threadIdx.x] = sk[0][threadIdx.x];
+}
+
+cudaError_t launch_merge_best(const int64_t *recs, int64_t n, int32_t is_float, int64_t *out, cudaStream_t st)
+{
+    k_merge_best<<<1, 1024, 0, st>>>(recs, n, is_float, out);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ a9: readback
 __global__ void k_extract_bits(const uint32_t *state, int32_t n, int32_t gl, int32_t bit,
                                const uint32_t *perm_o2i, int8_t *out)

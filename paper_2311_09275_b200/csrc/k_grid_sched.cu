@@ -1,0 +1,336 @@
+// k_grid_sched.cu -- persistent, ticket-scheduled variant of the fused torus PT launch
+// (sm_100a), for handles with more 32-replica word groups than SMs (C4 on one or two GPUs:
+// 512 / 256 groups on 148 SMs).  DESIGN.md §5.2b.
+//
+// Why: the fused launch of k_grid_bits keeps each word group resident in one CTA for the
+// whole schedule and runs each copy as a cluster of K/32 CTAs.  With 512 groups in clusters
+// of 4, only 33 clusters (132 CTAs) fit on a B200 at once (GPC sizes), so 128 copies take 4
+// waves on 132 SMs: 86% of the GPU's SM-time.  Here one CTA per SM (a cooperative launch)
+// loops over TASKS = (word group, round): load the group's state from global memory (L2:
+// the whole C4b state is 41 MB), run the round's k_ex sweeps and the bond count in shared
+// memory exactly as k_grid_bits does (grid_core.cuh), store it, and publish the 32 energies.
+// Tasks are handed out by one atomic ticket in round-major order, so every SM stays busy
+// until the last round and the state round trip (~160 KB of L2 traffic per task of ~0.3 ms)
+// costs ~1%.
+//
+// The PT step of a copy (best-so-far check, exchange decisions, walker and energy swaps;
+// same rule and RNG counters as bits::pt_step / k_exchange) is run by the
+// CTA that completes the copy's LAST task of the round (an atomic counter per copy).  It does
+// not touch the configurations: it publishes the copy's swap mask, and each group applies it
+// when it loads its state for the next round -- pairs inside a word by a delta swap, the pair
+// that crosses two words from the neighbouring group's boundary bit plane (bit 0 / bit 31 of
+// every site) saved at the end of the round (double-buffered by round parity).  After the
+// last round the PT step applies the swaps to the stored states itself.  A task of round r
+// waits (acquire spin) until its copy's exchange r-1 is published; tickets are handed out in
+// order and every CTA is resident, so a wait is always on an earlier ticket that a running
+// CTA holds: no deadlock, and in practice no waiting (the previous round's tasks of a copy
+// were handed out one round of tickets, >= 1.7 task durations, earlier).
+//
+// Results are bit-identical to k_grid_bits' fused launch (tests: test_sched_*).
+#include "grid_core.cuh"
+
+namespace ising {
+
+using namespace bits;
+
+namespace {
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *a)
+{
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(uint32_t *a, uint32_t v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+
+// The PT step of copy c_local after round `round` (all its K/32 groups stored).  Run by
+// every thread of the CTA that completed the copy's last task of the round.
+__device__ void copy_pt_step(PtShared &ps, const GridBitsParams &p, int round, int c_local, int Gl)
+{
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int KW = p.words_per_copy, K = 32 * KW, n = p.n;
+    const uint32_t c_global = p.g0 / (uint32_t)KW + (uint32_t)c_local;
+    const uint32_t t_now = p.t0 + (uint32_t)((round + 1) * p.k_ex), e_now = p.e0 + (uint32_t)round;
+    const int64_t *Eg = p.xs_E + (size_t)c_local * K;
+    int64_t *Wg = p.walker + (size_t)c_local * K;
+    for (int k = tid; k < K; k += nt) {
+        ps.Ecopy[k] = __ldcg(Eg + k);
+        ps.Wcopy[k] = __ldcg(Wg + k);
+    }
+    for (int q = tid; q < KW; q += nt)
+        ps.Mswap[q] = 0u;
+    __syncthreads();
+    int64_t *cb = p.copy_best + 3 * (size_t)c_local;
+    if (warp == 0) {  // best-so-far of the copy: argmin, ties -> lowest slot; strict improvement
+        int64_t bE = INT64_MAX;
+        int bk = -1;
+        for (int k = lane; k < K; k += 32)
+            if (bk < 0 || ps.Ecopy[k] < bE) {
+                bE = ps.Ecopy[k];
+                bk = k;
+            }
+        for (int o = 16; o > 0; o >>= 1) {
+            const int64_t oE = __shfl_down_sync(0xFFFFFFFFu, bE, o);
+            const int ok = __shfl_down_sync(0xFFFFFFFFu, bk, o);
+            if (ok >= 0 && (bk < 0 || oE < bE || (oE == bE && ok < bk))) {
+                bE = oE;
+                bk = ok;
+            }
+        }
+        if (lane == 0) {
+            const int64_t oldE = __ldcg(cb), oldSlot = __ldcg(cb + 1);
+            const bool imp = oldSlot < 0 || bE < oldE;
+            ps.improve = imp;
+            ps.kmin = bk;
+            if (imp) {
+                cb[0] = bE;
+                cb[1] = (int64_t)c_global * K + bk;
+                cb[2] = t_now;
+            }
+        }
+    }
+    __syncthreads();
+    if (ps.improve) {  // snapshot of the configuration (stored this round, before the swap)
+        const uint32_t *src = p.state_out + (size_t)(c_local * KW + (ps.kmin >> 5)) * n;
+        const int bit = ps.kmin & 31;
+        int8_t *dst = p.snap + (size_t)c_local * n;
+        for (int i = tid; i < n; i += nt)
+            dst[i] = ((__ldcg(src + i) >> bit) & 1u) ? -1 : 1;
+    }
+    const int par = (int)(e_now & 1u);
+    const int npairs = (K - par) / 2;
+    for (int pi = tid; pi < npairs; pi += nt) {
+        const int k = par + 2 * pi;
+        const int64_t d = ps.Ecopy[k + 1] - ps.Ecopy[k];
+        bool accept = d >= 0;
+        if (!accept) {
+            const int64_t j = -d - 1;
+            if (j < p.Tx_len[k]) {
+                const uint4 w = philox((uint32_t)k, e_now, c_global, ST_EXCH << 24, p.rk);
+                const uint64_t Ux = ((uint64_t)w.x << 32) | (uint64_t)w.y;
+                accept = Ux < p.Tx[p.Tx_off[k] + j];
+            }
+        }
+        if (accept) {
+            atomicOr(&ps.Mswap[k >> 5], 1u << (k & 31));
+            const int64_t te = ps.Ecopy[k];
+            ps.Ecopy[k] = ps.Ecopy[k + 1];
+            ps.Ecopy[k + 1] = te;
+            const int64_t tw = ps.Wcopy[k];
+            ps.Wcopy[k] = ps.Wcopy[k + 1];
+            ps.Wcopy[k + 1] = tw;
+        }
+    }
+    __syncthreads();
+    for (int k = tid; k < K; k += nt) {
+        p.E_out[(size_t)c_local * K + k] = ps.Ecopy[k];
+        Wg[k] = ps.Wcopy[k];
+    }
+    for (int q = tid; q < KW; q += nt)
+        p.xs_M[(size_t)c_local * KW + q] = ps.Mswap[q];
+    if (round + 1 == p.n_rounds) {  // no later load applies the swaps: apply them to the states
+        bool any = false;
+        for (int q = 0; q < KW; ++q)
+            any |= ps.Mswap[q] != 0u;
+        if (any) {
+            uint32_t *base = p.state_out + (size_t)c_local * KW * n;
+            for (int i = tid; i < n; i += nt) {
+                uint32_t prev = 0u, cur = __ldcg(base + i);
+                for (int q = 0; q < KW; ++q) {
+                    const uint32_t next = q + 1 < KW ? __ldcg(base + (size_t)(q + 1) * n + i) : 0u;
+                    const uint32_t M = ps.Mswap[q];
+                    uint32_t w = cur;
+                    const uint32_t tt = (w ^ (w >> 1)) & M & 0x7FFFFFFFu;
+                    w ^= tt ^ (tt << 1);
+                    if (q > 0 && ((ps.Mswap[q - 1] >> 31) & 1u))
+                        w = (w & ~1u) | (prev >> 31);
+                    if (q + 1 < KW && ((M >> 31) & 1u))
+                        w = (w & 0x7FFFFFFFu) | (next << 31);
+                    base[(size_t)q * n + i] = w;
+                    prev = cur;
+                    cur = next;
+                }
+            }
+        }
+    }
+}
+
+}  // namespace
+
+template <bool SPILL>
+__global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_sched(const GridBitsParams p)
+{
+    extern __shared__ __align__(16) uint32_t sm[];
+    __shared__ int32_t Ucnt[32];
+    __shared__ PtShared ps;
+    __shared__ int32_t s_task, s_last;
+    const int n = p.n;
+    const GridGeom G{p.Lx, p.Ly, p.hx, p.half, p.ymagic};
+    uint32_t *S = sm;
+    uint8_t *JB = reinterpret_cast<uint8_t *>(sm + n);
+    uint32_t *P = reinterpret_cast<uint32_t *>(JB + ((n + 15) & ~15));  // P[0..63] dE=4, P[64..127] dE=8
+    uint4 *Q4 = reinterpret_cast<uint4 *>(P + 128);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int KW = p.words_per_copy;
+    const int Gl = p.n_groups;
+    const int C_local = Gl / KW;
+    const int32_t ntask = Gl * p.n_rounds;  // host guarantees < 2^31
+    const int nbw = (n + 31) / 32;
+    uint32_t *ticket = p.xs_ctl, *cnt = p.xs_ctl + 1, *ready = p.xs_ctl + 1 + C_local;
+
+    RoundKeys rkr;
+#pragma unroll
+    for (int r = 0; r < 20; ++r)
+        rkr.k[r] = p.rk.k[r];
+    const grid::Ctx X = grid::make_ctx(G, n, p.qcap, S, JB, SPILL);
+    for (int l = tid; l < n; l += nt)  // the couplings are the same for every task
+        JB[l] = p.jbyte[l];
+
+    for (;;) {
+        if (tid == 0)
+            s_task = (int32_t)atomicAdd(ticket, 1u);
+        __syncthreads();
+        const int32_t task = s_task;
+        if (task >= ntask)
+            break;
+        const int round = task / Gl, gl = task - round * Gl;
+        const uint32_t g = p.g0 + (uint32_t)gl;
+        const int wt = (int)(g % (uint32_t)KW);
+        const int c_local = gl / KW;
+        if (round > 0) {  // the copy's exchange of the previous round must be published
+            if (tid == 0)
+                while (ld_acquire(ready + c_local) < (uint32_t)round)
+                    __nanosleep(256);
+            __syncthreads();
+        }
+        // ---- load (original order -> colour-separated), applying the copy's pending swaps
+        const uint32_t *src = (round == 0 ? p.state_in : p.state_out) + (size_t)gl * n;
+        uint32_t Min = 0u;
+        bool clo = false, chi = false;
+        const uint32_t *nB31 = nullptr, *nB0 = nullptr;
+        if (round > 0) {
+            const uint32_t *M = p.xs_M + (size_t)c_local * KW;
+            const uint32_t Mw = __ldcg(M + wt);
+            Min = Mw & 0x7FFFFFFFu;
+            clo = wt > 0 && ((__ldcg(M + wt - 1) >> 31) & 1u);
+            chi = wt + 1 < KW && ((Mw >> 31) & 1u);
+            const uint32_t *Bp = p.xs_B + (size_t)((round - 1) & 1) * Gl * 2 * nbw;
+            nB31 = Bp + ((size_t)(gl - 1) * 2 + 1) * nbw;  // used only if clo (wt > 0)
+            nB0 = Bp + (size_t)(gl + 1) * 2 * nbw;         // used only if chi (wt < KW - 1)
+        }
+        for (int i = tid; i < n; i += nt) {
+            uint32_t w = __ldcg(src + i);
+            const uint32_t tt = (w ^ (w >> 1)) & Min;
+            w ^= tt ^ (tt << 1);
+            if (clo)
+                w = (w & ~1u) | ((__ldcg(nB31 + (i >> 5)) >> (i & 31)) & 1u);
+            if (chi)
+                w = (w & 0x7FFFFFFFu) | (((__ldcg(nB0 + (i >> 5)) >> (i & 31)) & 1u) << 31);
+            S[grid::colsep(G, i)] = w;
+        }
+        for (int j = tid; j < 128; j += nt)
+            P[j] = __ldg(p.planes + wt * 128 + j);
+        if (tid < 32)
+            Ucnt[tid] = 0;
+        __syncthreads();
+        // ---- the round's k_ex sweeps (grid_core.cuh, as k_grid_bits)
+        for (int s = 0; s < p.k_ex; ++s) {
+            const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + s);
+            const PlaneUniform U = plane_uniform(g, t, rkr);
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c)
+                grid::colour_phase<SPILL>(X, c, U, rkr, P, Q4);
+        }
+        atomicAdd(&Ucnt[X.lane], grid::unsat_counts(X, S, JB));
+        // ---- store + this round's boundary bit planes (parity round & 1)
+        uint32_t *dst = p.state_out + (size_t)gl * n;
+        uint32_t *Bo = p.xs_B + ((size_t)(round & 1) * Gl + gl) * 2 * nbw;
+        for (int b = X.warp * 32; b < nbw * 32; b += nt) {
+            const int i = b + X.lane;
+            const uint32_t w = i < n ? S[grid::colsep(G, i)] : 0u;
+            if (i < n)
+                dst[i] = w;
+            const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, w & 1u);
+            const uint32_t b31 = __ballot_sync(0xFFFFFFFFu, w >> 31);
+            if (X.lane == 0) {
+                Bo[b >> 5] = b0;
+                Bo[nbw + (b >> 5)] = b31;
+            }
+        }
+        __syncthreads();  // Ucnt complete
+        if (tid < 32)
+            p.xs_E[(size_t)gl * 32 + tid] = 2 * (int64_t)Ucnt[tid] - 2 * (int64_t)n;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) {
+            const uint32_t done = atomicAdd(cnt + c_local, 1u) + 1u;
+            s_last = done == (uint32_t)KW * (uint32_t)(round + 1);
+        }
+        __syncthreads();
+        if (s_last) {  // this CTA completed the copy's round: its PT step
+            __threadfence();
+            copy_pt_step(ps, p, round, c_local, Gl);
+            __threadfence();
+            __syncthreads();
+            if (tid == 0)
+                st_release(ready + c_local, (uint32_t)(round + 1));
+        }
+    }
+}
+
+// Resident CTAs of the persistent launch (one per SM at this shared-memory size), 0 if the
+// kernel cannot be launched.
+int32_t grid_sched_ctas(int32_t threads, size_t smem, bool spill)
+{
+    auto kern = spill ? k_grid_sched<true> : k_grid_sched<false>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int per_sm = 0, dev = 0, nsm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess ||
+        cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return per_sm * nsm;
+}
+
+cudaError_t launch_grid_sched(const GridBitsParams &p, int32_t ctas, int32_t threads, size_t smem,
+                              cudaStream_t st)
+{
+    const int hx = p.hx, rpp = grid_rows_per_pass(threads, hx);
+    const int full = p.Ly / rpp, left = (p.Ly - full * rpp) * hx;
+    const int nidle = (threads / 32 - (rpp * hx + 31) / 32) * 32;
+    const bool spill = left > 0 && nidle > 0 && (left + nidle - 1) / nidle <= full;
+    auto kern = spill ? k_grid_sched<true> : k_grid_sched<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return e;
+    // control words: ticket, per-copy task counters and published exchange rounds
+    e = cudaMemsetAsync(p.xs_ctl, 0, sizeof(uint32_t) * (1 + 2 * (size_t)(p.n_groups / p.words_per_copy)), st);
+    if (e != cudaSuccess)
+        return e;
+    // per-copy best of this launch: slot -1 = none yet (all bytes 0xFF)
+    e = cudaMemsetAsync(p.copy_best, 0xFF, sizeof(int64_t) * 3 * (size_t)(p.n_groups / p.words_per_copy), st);
+    if (e != cudaSuccess)
+        return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ctas);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: the spin waits cannot deadlock
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+}  // namespace ising

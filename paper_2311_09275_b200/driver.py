@@ -103,6 +103,14 @@ class Engine:
                 return L.ising_best(self.h, spins=False)
             raise
 
+    def merge_best(self, recs):
+        """Global best over gathered ising_best_record rows (int64 tensor [n, 3]: energy bits,
+        sweep, slot) by the library's device merge."""
+        import torch
+        d = recs.to(torch.device("cuda", self.device)).contiguous()
+        r = L.ising_merge_best(self.h, d.data_ptr(), d.shape[0])
+        return r
+
     def copy_best(self):
         """Per-copy best-so-far (E[C_local], slot[C_local], sweep[C_local])."""
         return L.ising_copy_best(self.h)
@@ -219,24 +227,22 @@ def run_pt(engine, sweeps: int, k_ex: int, group=None, gather: bool = True, fuse
             engine.check_best()
     rec = engine.best(spins=False)
     if multi and not gather:
-        rec = merge_best_over_ranks(rec, group)
+        rec = merge_best_over_ranks(rec, group, engine)
     return {k: rec[k] for k in ("E", "slot", "sweep")}
 
 
-def merge_best_over_ranks(rec, group):
-    """All-gather the per-rank best records and keep the lexicographic min (E, sweep, slot)."""
+def merge_best_over_ranks(rec, group, engine):
+    """Global best over the ranks' local best records: one all-gather of a 24-byte
+    ising_best_record per rank (energy, sweep, slot), merged by the library on the device
+    (ising_merge_best: lexicographic (E, sweep, slot), S:327 first reached)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
     backend = dist.get_backend(group)
-    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    dev = torch.device("cuda", engine.device) if backend == "nccl" else torch.device("cpu")
     E = rec["E"]
-    is_float = isinstance(E, float)
-    mine = torch.tensor([[float(E) if is_float else int(E), rec["sweep"], rec["slot"]]],
-                        dtype=torch.float64 if is_float else torch.int64, device=dev)
-    allr = torch.empty((world, 3), dtype=mine.dtype, device=dev)
+    e_bits = int(np.array([E], np.float64).view(np.int64)[0]) if isinstance(E, float) else int(E)
+    mine = torch.tensor([[e_bits, rec["sweep"], rec["slot"]]], dtype=torch.int64, device=dev)
+    allr = torch.empty((world, 3), dtype=torch.int64, device=dev)
     all_gather(allr, mine, group)
-    rows = allr.cpu().numpy()
-    order = np.lexsort((rows[:, 2], rows[:, 1], rows[:, 0]))
-    r = rows[order[0]]
-    return dict(E=float(r[0]) if is_float else int(r[0]), sweep=int(r[1]), slot=int(r[2]))
+    return engine.merge_best(allr)

@@ -19,16 +19,35 @@ import numpy as np
 
 
 def parse_gset(text: str):
-    """-> (n, u, v, w) with 0-based endpoints and int32 weights."""
+    """-> (n, u, v, w) with 0-based endpoints and int32 weights.  Rejects (ValueError, naming
+    the edge line -- line 1 is the header) a header that is not two integers, a token count
+    other than 2 + 3m (truncated or trailing data), ids out of range, self-loops and
+    duplicate undirected edges (S:43-60, S:29-35 instance invariants)."""
     toks = text.split()
+    if len(toks) < 2:
+        raise ValueError("Gset header 'n m' missing")
     n, m = int(toks[0]), int(toks[1])
-    a = np.array(toks[2:2 + 3 * m], dtype=np.int64).reshape(m, 3)
-    if a.shape[0] != m:
-        raise ValueError("truncated Gset file")
-    u, v, w = a[:, 0] - 1, a[:, 1] - 1, a[:, 2].astype(np.int32)
-    if np.any((u < 0) | (u >= n) | (v < 0) | (v >= n)):
-        raise ValueError("vertex id out of range")
-    return n, u, v, w
+    if n < 1 or m < 0:
+        raise ValueError(f"bad Gset header: n={n} m={m}")
+    if len(toks) != 2 + 3 * m:
+        raise ValueError(f"Gset file has {len(toks) - 2} edge tokens, expected 3*m = {3 * m} "
+                         f"({'truncated' if len(toks) < 2 + 3 * m else 'trailing data'})")
+    a = np.array(toks[2:], dtype=np.int64).reshape(m, 3)
+    u, v, w = a[:, 0] - 1, a[:, 1] - 1, a[:, 2]
+    bad = np.flatnonzero((u < 0) | (u >= n) | (v < 0) | (v >= n))
+    if bad.size:
+        raise ValueError(f"vertex id out of range on line {bad[0] + 2}")
+    loop = np.flatnonzero(u == v)
+    if loop.size:
+        raise ValueError(f"self-loop on line {loop[0] + 2}")
+    key = np.minimum(u, v) * n + np.maximum(u, v)
+    order = np.argsort(key, kind="stable")
+    dup = np.flatnonzero(key[order][1:] == key[order][:-1])
+    if dup.size:
+        raise ValueError(f"duplicate edge on line {int(np.min(order[dup + 1])) + 2}")
+    if np.any(np.abs(w) >= 2**31):
+        raise ValueError("weight outside int32")
+    return n, u, v, w.astype(np.int32)
 
 
 def write_gset(n: int, u, v, w) -> str:

@@ -24,7 +24,7 @@ LAYOUTS = {"bits": ISING_SPINS_BITS, "i8": ISING_SPINS_I8}
 EXPORTED = [
     "ising_create_grid", "ising_create_csr", "ising_sweep", "ising_run", "ising_anneal", "ising_energy", "ising_cut",
     "ising_exchange", "ising_icm", "ising_exchange_begin", "ising_exchange_end", "ising_check_best",
-    "ising_best", "ising_copy_best", "ising_get_spins", "ising_set_spins", "ising_get_walkers", "ising_info",
+    "ising_best", "ising_merge_best", "ising_copy_best", "ising_get_spins", "ising_set_spins", "ising_get_walkers", "ising_info",
     "ising_sync", "ising_last_error", "ising_destroy", "ising_greedy_colour", "ising_greedy_colour_sl", "ising_threshold",
     "ising_version", "ising_debug_philox", "ising_debug_exp_bound",
     "ising_state_size", "ising_state_save", "ising_state_load",
@@ -66,9 +66,9 @@ def lib(build_if_missing: bool = True):
     if _lib is not None:
         return _lib
     path = _build.LIB
-    if not os.path.exists(path):
+    if _build.needs_build():  # missing, or older than a source file: never load a stale binary
         if not build_if_missing:
-            raise ImportError(f"libising.so not built: {path}")
+            raise ImportError(f"libising.so missing or older than its sources: {path}")
         _build.build()
     L = C.CDLL(path)
     vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
@@ -86,6 +86,7 @@ def lib(build_if_missing: bool = True):
         "ising_exchange_end": ([vp, vp, i64], C.c_int),
         "ising_check_best": ([vp, vp, i64], C.c_int),
         "ising_best": ([vp, vp, C.POINTER(i64), C.POINTER(i64), vp], C.c_int),
+        "ising_merge_best": ([vp, vp, i64, vp, C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "ising_get_spins": ([vp, i64, vp], C.c_int),
         "ising_copy_best": ([vp, vp, vp, vp], C.c_int),
         "ising_set_spins": ([vp, i64, vp], C.c_int),
@@ -121,13 +122,15 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(C.c_void_p)
 
 
-def _current_stream(stream):
+def _current_stream(stream, device=0):
+    """The caller's stream, else torch's current stream OF THE HANDLE'S DEVICE (not of torch's
+    current device: a handle on device d must enqueue on a stream of d)."""
     if stream is not None:
         return stream
     try:
         import torch
         if torch.cuda.is_available():
-            return torch.cuda.current_stream().cuda_stream
+            return torch.cuda.current_stream(device).cuda_stream
     except Exception:  # pragma: no cover - torch absent
         pass
     return None
@@ -141,7 +144,7 @@ def _desc(seed, n_temps, n_copies, betas, copy_begin=0, copy_end=None, layout="b
                 copy_begin=copy_begin, copy_end=n_copies if copy_end is None else copy_end,
                 betas=betas.ctypes.data, layout=lay,
                 rng=ISING_RNG_PLANE if lay == ISING_SPINS_BITS else ISING_RNG_WORD,
-                device=device, block_threads=block_threads, stream=_current_stream(stream))
+                device=device, block_threads=block_threads, stream=_current_stream(stream, device))
     return d, betas
 
 
@@ -237,6 +240,15 @@ def ising_best(h, spins: bool = True):
     _check(lib().ising_best(h, _ptr(e), C.byref(slot), C.byref(sweep),
                             _ptr(sp) if sp is not None else None))
     return dict(E=e[0].item(), slot=slot.value, sweep=sweep.value, spins=sp)
+
+
+def ising_merge_best(h, dev_recs_ptr: int, n: int):
+    """Global best over n gathered ising_best_record (device memory, 24 bytes each)."""
+    info = ising_info(h)
+    e = np.zeros(1, np.float64 if info.wtype == ISING_W_F32 else np.int64)
+    slot, sweep = C.c_int64(), C.c_int64()
+    _check(lib().ising_merge_best(h, C.c_void_p(dev_recs_ptr), int(n), _ptr(e), C.byref(slot), C.byref(sweep)))
+    return dict(E=e[0].item(), slot=slot.value, sweep=sweep.value)
 
 
 def ising_copy_best(h):

@@ -96,7 +96,7 @@ def _nccl_worker(rank, world, port, out):
     np.save(os.path.join(out, "E.npy"), eng.energies())
     np.save(os.path.join(out, "W.npy"), eng.walkers())
     from paper_2311_09275_b200.driver import merge_best_over_ranks
-    b = merge_best_over_ranks(eng.best(spins=False), None)  # the bench's per-step NCCL merge
+    b = merge_best_over_ranks(eng.best(spins=False), None, eng)  # the bench's per-step NCCL merge
     np.save(os.path.join(out, "rec.npy"), np.array([b["E"], b["slot"], b["sweep"]]))
     dist.destroy_process_group()
 
@@ -114,3 +114,40 @@ def test_nccl_record_gather_single_rank():
     assert np.array_equal(E, ref.energies())
     assert np.array_equal(W, ref.walker)
     assert (rec[0], rec[1], rec[2]) == (ref.best.E, ref.best.slot, ref.best.sweep)
+
+
+def _nccl2_worker(rank, world, port, out, gather, workload_kind):
+    """One process per GPU (cuda:rank), NCCL, each rank a contiguous copy shard."""
+    from paper_2311_09275_b200 import Engine
+    from paper_2311_09275_b200.driver import run_pt, shard
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    a, b = shard(C, world, rank)
+    eng = Engine(_inst(workload_kind), K, C, synth.beta_ladder(K), seed=KEY, copy_begin=a, copy_end=b,
+                 layout="bits", device=rank)
+    rec = run_pt(eng, 35, 10, group=None, gather=gather)
+    np.save(os.path.join(out, f"E{rank}.npy"), eng.energies())
+    np.save(os.path.join(out, f"W{rank}.npy"), eng.walkers())
+    np.save(os.path.join(out, f"rec{rank}.npy"), np.array([rec["E"], rec["slot"], rec["sweep"]]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs (one process per GPU over NCCL)")
+@pytest.mark.parametrize("gather", [True, False])
+@pytest.mark.parametrize("kind", ["grid", "csr"])
+def test_two_gpus_nccl_equal_oracle(gather, kind):
+    """The N>1 path on hardware: 2 ranks on 2 GPUs over NCCL (record all-gather per exchange,
+    or local bests merged by ising_merge_best), equal to the single-process oracle run."""
+    world = 2
+    with tempfile.TemporaryDirectory() as out:
+        mp.spawn(_nccl2_worker, args=(world, _free_port(), out, gather, kind), nprocs=world, join=True)
+        E = np.concatenate([np.load(os.path.join(out, f"E{r}.npy")) for r in range(world)])
+        W = np.concatenate([np.load(os.path.join(out, f"W{r}.npy")) for r in range(world)])
+        recs = [np.load(os.path.join(out, f"rec{r}.npy")) for r in range(world)]
+    ref = oracle.Oracle(_inst(kind), K, synth.beta_ladder(K), KEY, 0, C, rng=oracle.RNG_PLANE).run(35, 10)
+    assert np.array_equal(E, ref.energies())
+    assert np.array_equal(W, ref.walker)
+    for r in recs:
+        assert (r[0], r[1], r[2]) == (ref.best.E, ref.best.slot, ref.best.sweep)

@@ -49,3 +49,23 @@ def test_gset_round_trip_and_host_cut():
     s[0] = -1
     nb = (u == 0) | (v == 0)
     assert gset.cut_of(u, v, w, s) == int(w[nb].sum())
+
+
+def test_parse_gset_rejects_malformed_files():
+    """S:43-60 / S:29-35: truncated files, trailing tokens, self-loops and duplicate edges are
+    errors naming the line (line 1 = header)."""
+    import pytest
+    from paper_2311_09275_b200.gset import parse_gset
+    good = "3 2\n1 2 1\n2 3 -1\n"
+    n, u, v, w = parse_gset(good)
+    assert n == 3 and list(u) == [0, 1] and list(v) == [1, 2] and list(w) == [1, -1]
+    with pytest.raises(ValueError, match="truncated"):
+        parse_gset("3 2\n1 2 1\n2 3\n")
+    with pytest.raises(ValueError, match="trailing"):
+        parse_gset("3 2\n1 2 1\n2 3 -1\n7\n")
+    with pytest.raises(ValueError, match="self-loop on line 3"):
+        parse_gset("3 2\n1 2 1\n3 3 1\n")
+    with pytest.raises(ValueError, match="duplicate edge on line 3"):
+        parse_gset("3 2\n1 2 1\n2 1 1\n")
+    with pytest.raises(ValueError, match="out of range on line 2"):
+        parse_gset("3 1\n1 4 1\n")

@@ -59,6 +59,13 @@ class OracleEngine:
         else:
             self._global_best(recv)
 
+    def merge_best(self, recs):
+        """ising_merge_best's rule on the host: lexicographic (E, sweep, slot) over the ranks'
+        records (test-side; the product Engine merges on the device)."""
+        rows = [tuple(int(x) for x in r) for r in recs.numpy() if r[2] >= 0]
+        E, sweep, slot = min(rows)
+        return dict(E=E, slot=slot, sweep=sweep)
+
     def best(self, spins=True):
         if self.gbest is not None:
             return dict(self.gbest)
