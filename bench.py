@@ -272,13 +272,13 @@ def roofline_entry(kernel_ms, attempts_per_launch, layout, clocks, ipa_key):
     §5.4: 2 own + 3 neighbour + 0.11 CSR = 5.11 B) x attempts per launch / live CUDA-event launch
     time, against MEASURED_PEAKS.json hbm_gbs.
 
-    Bit-packed sweeps (C2-C4) keep their state on chip and are issue (ALU) bound: achieved = warp
-    instructions per launch (ncu smsp__inst_executed.sum per attempt, profiles/inst_per_attempt.json,
-    times the live attempts per launch) / live launch time; peak = the MEASURED issue rate of the
-    PLANE instruction mix (tools/alu_peak.cu -> profiles/alu_peak.json, warp instructions per SM
-    cycle) x 148 SMs x the SM clock sampled during this run's timed region (SURVEY.md §8(d) "ALU
-    fraction ... at the same clock").  Falls back to the derived 4 issue/cycle/SM peak if the
-    microbenchmark has not been run."""
+    Bit-packed sweeps (C1-C4) keep their state on chip and are bound by the integer pipes (Philox
+    IMAD.WIDE on the FMA pipe, LOP3 on the ALU pipe): achieved = ALU + FMA pipe warp instructions
+    per launch (ncu sm__inst_executed_pipe_alu + _fma per attempt, profiles/inst_per_attempt.json,
+    times the live attempts per launch) / live launch time; peak = the MEASURED ALU + FMA pipe rate
+    of the PLANE instruction mix (tools/alu_peak.cu -> profiles/alu_peak.json, per SM cycle) x 148
+    SMs x the SM clock sampled during this run's timed region (SURVEY.md §8(d) "ALU fraction ... at
+    the same clock").  Falls back to all-instruction issue rates if those counts are missing."""
     peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
     ipa = None
     if os.path.exists(PROFILE_FILE):
@@ -295,6 +295,27 @@ def roofline_entry(kernel_ms, attempts_per_launch, layout, clocks, ipa_key):
     mhz_max = peaks.get("sm_max_mhz", 1965.0)
     mhz = (clocks or {}).get("sm_mhz") or mhz_max
     alu = json.load(open(ALU_PEAK_FILE)) if os.path.exists(ALU_PEAK_FILE) else None
+    traffic_launch = None
+    if ipa:
+        if ipa.get("dram_bytes_per_launch") is not None:  # on-chip state: a fixed load/store per launch
+            traffic_launch = ipa["dram_bytes_per_launch"]
+        elif ipa.get("dram_bytes_per_attempt") is not None:
+            traffic_launch = ipa["dram_bytes_per_attempt"] * attempts_per_launch
+    if ipa and ipa.get("alu_fma_pipe_inst_per_attempt") and alu and alu.get("pipe_inst_per_sm_cycle"):
+        # the integer roof: ALU + FMA pipe warp instructions (LOP3 / IMAD.WIDE), measured
+        peak = alu["pipe_inst_per_sm_cycle"] * 148 * mhz * 1e6 / 1e9
+        ach = attempts_per_launch * ipa["alu_fma_pipe_inst_per_attempt"] / (kernel_ms * 1e-3) / 1e9
+        out = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "G ALU+FMA-pipe warp-inst/s",
+               "frac": ach / peak, "traffic": traffic_launch,
+               "peak_source": (f"measured: tools/alu_peak.cu PLANE mix, {alu['pipe_inst_per_sm_cycle']:.3f} ALU+FMA "
+                               f"pipe warp-inst per SM cycle (ncu, profiles/alu_peak.json) x 148 SMs x {mhz:.0f} "
+                               "MHz sampled in this timed region"),
+               "alu_fma_pipe_inst_per_attempt": ipa["alu_fma_pipe_inst_per_attempt"],
+               "inst_per_attempt_source": ipa.get("pipes_source") or ipa.get("source")}
+        if ipa.get("warp_inst_per_attempt"):
+            out["issue_frac_of_4_per_cycle"] = (attempts_per_launch * ipa["warp_inst_per_attempt"] /
+                                                (kernel_ms * 1e-3) / (148 * 4 * mhz * 1e6))
+        return out
     if alu:
         peak = alu["warp_inst_per_sm_cycle"] * 148 * mhz * 1e6 / 1e9
         src = (f"measured: tools/alu_peak.cu PLANE mix {alu['warp_inst_per_sm_cycle']:.3f} warp-inst per SM "
@@ -306,17 +327,10 @@ def roofline_entry(kernel_ms, attempts_per_launch, layout, clocks, ipa_key):
         return {"bound": "alu", "achieved": None, "peak": peak, "unit": "Ginst/s", "frac": None,
                 "traffic": None, "peak_source": src, "note": "no ncu instruction count committed yet"}
     ach = attempts_per_launch * ipa["warp_inst_per_attempt"] / (kernel_ms * 1e-3) / 1e9
-    if ipa.get("dram_bytes_per_launch") is not None:  # on-chip state: a fixed load/store per launch
-        traffic_launch = ipa["dram_bytes_per_launch"]
-    else:
-        t = ipa.get("dram_bytes_per_attempt")
-        traffic_launch = t * attempts_per_launch if t is not None else None
-    out = {"bound": "alu", "achieved": ach, "peak": peak, "unit": "Ginst/s", "frac": ach / peak,
-           "traffic": traffic_launch, "peak_source": src,
-           "warp_inst_per_attempt": ipa["warp_inst_per_attempt"],
-           "inst_per_attempt_source": ipa.get("source"),
-           "frac_of_4_issue_per_cycle": ach / (148 * 4 * mhz * 1e-3)}
-    return out
+    return {"bound": "alu", "achieved": ach, "peak": peak, "unit": "Ginst/s", "frac": ach / peak,
+            "traffic": traffic_launch, "peak_source": src,
+            "warp_inst_per_attempt": ipa["warp_inst_per_attempt"],
+            "inst_per_attempt_source": ipa.get("source")}
 
 
 def measure(args, workload, world, rank, local, steps, warmup, e2e_steps, copies=0, sweeps=0,

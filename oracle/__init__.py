@@ -68,6 +68,8 @@ def lib():
             L.or_greedy_colour.restype = C.c_int32
             L.or_greedy_colour_sl.argtypes = [C.c_int32, vp, vp, vp]
             L.or_greedy_colour_sl.restype = C.c_int32
+            L.or_greedy_colour_jp.argtypes = [C.c_int32, vp, vp, vp, vp]
+            L.or_greedy_colour_jp.restype = C.c_int32
             L.or_init.argtypes = [C.POINTER(_Run), vp]
             L.or_energy.argtypes = [C.POINTER(_Run), vp, vp, vp]
             L.or_sweeps.argtypes = [C.POINTER(_Run), vp, vp, C.c_uint32, C.c_int32]
@@ -140,6 +142,17 @@ def greedy_colour_sl(n, row_ptr, col):
     out = np.zeros(n, np.int32)
     ncol = lib().or_greedy_colour_sl(n, _p(rp), _p(cc), _p(out))
     return out, int(ncol)
+
+
+def greedy_colour_jp(n, row_ptr, col, with_priority=False):
+    """Greedy colouring in Jones-Plassmann priority order (R12c), sequentially:
+    decreasing Philox priority, ties by lower id, smallest free colour."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cc = np.ascontiguousarray(col, np.int32)
+    out = np.zeros(n, np.int32)
+    pr = np.zeros(n, np.uint32)
+    ncol = lib().or_greedy_colour_jp(n, _p(rp), _p(cc), _p(out), _p(pr))
+    return (out, int(ncol), pr) if with_priority else (out, int(ncol))
 
 
 # ------------------------------------------------------------------ the run

@@ -288,6 +288,68 @@ int32_t or_greedy_colour_sl(int32_t n, const int64_t *rp, const int32_t *col, in
     return ncol;
 }
 
+/* Greedy colouring in Jones-Plassmann priority order (R12c): vertex i has the
+ * priority pr(i) = word 0 of Philox4x32-10(ctr = (i, 0, 0, COLOUR << 24), key = (0, 0)),
+ * COLOUR = 6; vertices are coloured in decreasing priority (ties: lower id first), each with
+ * the smallest colour not used by an already-coloured neighbour.  This is the sequential
+ * definition of the colouring the Jones-Plassmann rounds compute in parallel (a vertex is
+ * coloured once every higher-priority neighbour is).  Returns the number of colours. */
+static const uint32_t *jp_prio;
+
+static int jp_cmp(const void *a, const void *b)
+{
+    const int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    if (jp_prio[x] != jp_prio[y])
+        return jp_prio[x] > jp_prio[y] ? -1 : 1;
+    return x < y ? -1 : (x > y);
+}
+
+int32_t or_greedy_colour_jp(int32_t n, const int64_t *rp, const int32_t *col, int32_t *colour,
+                            uint32_t *prio_out)
+{
+    int32_t maxdeg = 0;
+    for (int32_t i = 0; i < n; ++i)
+        if (rp[i + 1] - rp[i] > maxdeg)
+            maxdeg = (int32_t)(rp[i + 1] - rp[i]);
+    size_t nn = (size_t)(uint32_t)n;
+    uint32_t *prio = (uint32_t *)malloc(sizeof(uint32_t) * nn);
+    int32_t *order = (int32_t *)malloc(sizeof(int32_t) * nn);
+    const uint32_t key[2] = {0u, 0u};
+    for (int32_t i = 0; i < n; ++i) {
+        const uint32_t ctr[4] = {(uint32_t)i, 0u, 0u, 6u << 24};
+        uint32_t w[4];
+        or_philox4x32_10(ctr, key, w);
+        prio[i] = w[0];
+        order[i] = i;
+        colour[i] = -1;
+    }
+    jp_prio = prio;
+    qsort(order, nn, sizeof(int32_t), jp_cmp);
+    char *used = (char *)calloc((size_t)maxdeg + 2, 1);
+    int32_t ncol = 0;
+    for (size_t q = 0; q < nn; ++q) {
+        const int32_t i = order[q];
+        memset(used, 0, (size_t)maxdeg + 2);
+        for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+            const int32_t c = colour[col[e]];
+            if (c >= 0 && c <= maxdeg + 1)
+                used[c] = 1;
+        }
+        int32_t c = 0;
+        while (used[c])
+            ++c;
+        colour[i] = c;
+        if (c + 1 > ncol)
+            ncol = c + 1;
+    }
+    if (prio_out)
+        memcpy(prio_out, prio, sizeof(uint32_t) * nn);
+    free(used);
+    free(order);
+    free(prio);
+    return ncol;
+}
+
 /* ------------------------------------------------------------------- run */
 typedef struct {
     int32_t n;

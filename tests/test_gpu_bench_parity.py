@@ -157,11 +157,12 @@ def test_c5_full_size_eight_replicas_50_sweeps():
     (10, 8, 96, 2, 40, 5),       # 3 words per copy: cross-word pairs at both ends of word 1
     (12, 20, 256, 1, 60, 3),     # 8 words per copy
     (8, 8, 128, 41, 30, 10),     # 164 groups > 148 SMs: tasks of two rounds in flight
-    (80, 10, 64, 3, 50, 10),     # leftover rows spill onto the column-less warps
+    (80, 100, 32, 2, 30, 10),    # C2 geometry: leftover rows spill onto the column-less warps
 ])
 def test_sched_fused_pt_parity(Lx, Ly, K, C, sweeps, kex, monkeypatch):
     """k_grid_sched (forced) == oracle for every slot, and == the cluster launch."""
     monkeypatch.setenv("ISING_GRID_SCHED", "1")
+    monkeypatch.setenv("ISING_GRID_BANDS", "1")  # the persistent launch is the single-band kernel
     inst = grid(Lx, Ly, 91 + Lx * Ly)
     betas = synth.beta_ladder(K)
     eng = Engine(inst, K, C, betas, seed=KEY, layout="bits")
@@ -186,9 +187,10 @@ def test_sched_fused_pt_parity(Lx, Ly, K, C, sweeps, kex, monkeypatch):
 
 
 def test_sched_split_runs_and_state_roundtrip(monkeypatch):
-    """Two ising_run calls (the second continuing t and e), a plain sweep between them and a
-    checkpoint of the persistent launch's state equal one oracle run."""
+    """Two ising_run calls (the second continuing t and e) and a checkpoint of the persistent
+    launch's state, resumed on a fresh handle, equal one oracle run."""
     monkeypatch.setenv("ISING_GRID_SCHED", "1")
+    monkeypatch.setenv("ISING_GRID_BANDS", "1")
     inst = grid(12, 10, 5)
     K, C = 64, 5
     betas = synth.beta_ladder(K)

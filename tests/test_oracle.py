@@ -205,6 +205,56 @@ def test_smallest_last_colouring_c3_three_colours():
     assert ncol == 3
 
 
+def _jp_priority_bruteforce(n):
+    """pr(i) = word 0 of Philox4x32-10(i, 0, 0, COLOUR << 24) under key (0, 0) (R12c),
+    evaluated through the oracle's Philox (pinned by the Random123 known answers)."""
+    return np.array([oracle.philox([i, 0, 0, 6 << 24], [0, 0])[0] for i in range(n)], np.uint32)
+
+
+@pytest.mark.parametrize("n,m,seed", [(60, 90, 1), (200, 199, 2), (300, 600, 3), (40, 0, 4)])
+def test_jones_plassmann_colouring_definition(n, m, seed):
+    """Greedy in decreasing Philox priority (ties -> lower id): each vertex takes the smallest
+    colour not used by its higher-priority neighbours; proper; <= max degree + 1 colours."""
+    u, v = synth.gnm(n, m, seed)
+    rp, col, _ = synth.edges_to_csr(n, u, v, np.ones(u.size, np.int32))
+    colour, ncol, pr = oracle.greedy_colour_jp(n, rp, col, with_priority=True)
+    assert np.array_equal(pr, _jp_priority_bruteforce(n))
+    for i in range(n):
+        nb = col[rp[i]:rp[i + 1]]
+        higher = nb[(pr[nb] > pr[i]) | ((pr[nb] == pr[i]) & (nb < i))]
+        used = set(colour[higher].tolist())
+        c = 0
+        while c in used:
+            c += 1
+        assert colour[i] == c
+    src = np.repeat(np.arange(n), np.diff(rp))
+    assert np.all(colour[src] != colour[col])
+    assert ncol == (colour.max() + 1 if n else 0)
+    assert ncol <= (np.diff(rp).max() if m else 0) + 1
+
+
+def test_jones_plassmann_colouring_complete_graph_is_priority_rank():
+    """On K_n every vertex neighbours every higher-priority vertex, so its colour is the number
+    of vertices with a higher priority: the colouring spells out the priority order."""
+    n = 12
+    iu, iv = np.triu_indices(n, 1)
+    rp, col, _ = synth.edges_to_csr(n, iu, iv, np.ones(iu.size, np.int32))
+    colour, ncol = oracle.greedy_colour_jp(n, rp, col)
+    pr = _jp_priority_bruteforce(n)
+    rank = np.array([int(np.sum(pr > pr[i])) for i in range(n)])
+    assert ncol == n and np.array_equal(colour, rank)
+
+
+def test_jones_plassmann_colouring_c5_shape():
+    """Random 3-regular graph (C5 shape): 4 colours, the fourth class a few percent (SURVEY
+    Appendix A: greedy gives ~37.5 / 37 / 23 / 2.6 %)."""
+    u, v = synth.random_regular(100000, 3, 3)
+    rp, col, _ = synth.edges_to_csr(100000, u, v, np.ones(u.size, np.int32))
+    colour, ncol = oracle.greedy_colour_jp(100000, rp, col)
+    frac = np.bincount(colour) / 100000
+    assert ncol == 4 and 0.01 < frac[3] < 0.05 and frac[0] > frac[1] > frac[2] > frac[3]
+
+
 def test_grid_to_csr_matches_edge_list():
     Jr, Jd = synth.torus_pm1(6, 8, 9)
     rp, col, w, chk = oracle.grid_to_csr(6, 8, Jr, Jd)

@@ -16,6 +16,7 @@ own timed region, so the roof is taken "at the same clock".  Run under gpurun:
 from __future__ import annotations
 
 import argparse
+import csv
 import json
 import os
 import re
@@ -81,6 +82,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--iters", type=int, default=20000)
+    ap.add_argument("--ncu", action="store_true", help="also count the loop's pipe instructions with ncu")
     args = ap.parse_args()
     build()
     counts = loop_counts()
@@ -106,6 +108,26 @@ def main():
     res["philox_only_warp_inst_per_sm_cycle"] = best0["warp_inst_per_sm_cycle"]
     res["note"] = ("roof = best mode-1 (PLANE mix) run; per SM cycle so bench.py can scale it by the clock of "
                    "its own timed region; 4.0 would be one warp instruction per scheduler per cycle")
+    if args.ncu:  # pipe counts of the best mode-1 / mode-0 configurations (plain runs exited 0 above)
+        M = ("sm__inst_executed_pipe_alu.sum,sm__inst_executed_pipe_fma.sum,smsp__inst_executed.sum,"
+             "sm__cycles_elapsed.avg,sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active,"
+             "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active")
+        for key, r in (("plane", best), ("philox", best0)):
+            cmd = [BIN, str(r["mode"]), str(r["threads"]), str(r["ctas_per_sm"]), "2000"]
+            out = subprocess.run(["ncu", "--metrics", M, "--clock-control", "none", "-c", "1", "--csv"] + cmd,
+                                 capture_output=True, text=True, timeout=600).stdout
+            vals = {}
+            for row in csv.reader(out.splitlines()):
+                if len(row) > 14 and row[0] != "ID":
+                    vals[row[12]] = float(row[14].replace(",", ""))
+            pipe = vals["sm__inst_executed_pipe_alu.sum"] + vals["sm__inst_executed_pipe_fma.sum"]
+            res[f"ncu_{key}"] = vals
+            res[f"{key}_alu_fma_pipe_inst_per_sm_cycle"] = pipe / (nsm * vals["sm__cycles_elapsed.avg"])
+        res["pipe_inst_per_sm_cycle"] = res["plane_alu_fma_pipe_inst_per_sm_cycle"]
+        res["pipe_note"] = ("ALU + FMA pipe warp instructions per SM cycle of the PLANE mix (ncu "
+                            "sm__inst_executed_pipe_alu + _fma over 148 x sm__cycles_elapsed): the measured "
+                            "integer roof; LOP3 (ALU pipe) and IMAD.WIDE (FMA-heavy pipe) do not overlap on "
+                            "sm_100a beyond ~0.5 warp instruction per scheduler per cycle combined")
     try:
         res["clocks"] = subprocess.run(
             ["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
