@@ -177,6 +177,8 @@ def cpu_oracle_sample(cfg, target_s=12.0):
     colour = None  # the workload's colouring, computed by the oracle's own implementation
     if cfg.get("colouring") == "sl":
         colour, _ = oracle.greedy_colour_sl(n, inst["row_ptr"], inst["col"])
+    elif cfg.get("colouring") == "jp":
+        colour, _ = oracle.greedy_colour_jp(n, inst["row_ptr"], inst["col"])
     # calibrate on one copy x 2 sweeps
     t0 = time.perf_counter()
     if cfg["C"] == 1 and cfg["K"] > 64:

@@ -79,6 +79,14 @@ typedef enum { ISING_SPINS_BITS = 0, ISING_SPINS_I8 = 1 } ising_layout;
  * replicas of a word, compared MSB-first; WORD = one 64-bit uniform per replica. */
 typedef enum { ISING_RNG_PLANE = 0, ISING_RNG_WORD = 1 } ising_rng;
 
+/* Colouring ising_create_csr computes when the caller passes none (SURVEY §8(c) #13,
+ * DESIGN.md R12/R12c).  GREEDY: vertices in ascending id, smallest colour unused by coloured
+ * neighbours (host, sequential).  JP: the same greedy rule in Jones-Plassmann priority order --
+ * decreasing pr(i) = word 0 of Philox4x32-10(i, 0, 0, 6 << 24) under key (0, 0), ties to the
+ * lower id -- computed on the GPU in parallel rounds (a vertex is coloured once all its
+ * higher-priority neighbours are); at most max degree + 1 colours. */
+typedef enum { ISING_COLOUR_GREEDY = 0, ISING_COLOUR_JP = 1 } ising_colouring;
+
 typedef struct {
     uint64_t seed;         /* Philox key = (seed & 0xffffffff, seed >> 32) */
     int32_t n_temps;       /* K >= 1; BITS layout needs K % 32 == 0 */
@@ -91,6 +99,7 @@ typedef struct {
     int32_t device;        /* CUDA device ordinal */
     int32_t block_threads; /* 0 = default; else threads per CTA of the sweep kernels */
     void *stream;          /* cudaStream_t or NULL */
+    int32_t colouring;     /* ising_colouring used by ising_create_csr when colour == NULL */
 } ising_run_desc;
 
 /* Per-slot record written by ising_exchange_begin (16 bytes): energy (int64, or
@@ -143,12 +152,14 @@ ISING_API int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, c
 /* Create from a symmetric CSR: row_ptr[n+1] (int64, row_ptr[0]=0, non-decreasing),
  * col[row_ptr[n]] (int32 in [0,n)), w[row_ptr[n]] (int32 or float32 per wtype).
  * Invariants: no self-loops, no duplicate neighbours in a row, and
- * (i,j,w) present iff (j,i,w) present.  colour[n] (optional, NULL -> greedy:
- * ascending id, smallest colour unused by coloured neighbours) must be a proper
+ * (i,j,w) present iff (j,i,w) present.  colour[n] (optional, NULL -> desc->colouring:
+ * greedy in ascending id or in Jones-Plassmann priority order) must be a proper
  * colouring with ids 0..ncol-1.  Row order is kept as given (it fixes the
- * float32 field summation order).  Errors: ISING_E_GRAPH (message names the
- * offending vertex/entry), ISING_E_UNSUPPORTED (BITS with weights not +-1,
- * float weights with BITS), ISING_E_ARG, ISING_E_CUDA/OOM. */
+ * float32 field summation order).  With the I8 layout the checks, the colouring, the
+ * colour-sorted internal order and the internal tables are computed on the GPU (one upload
+ * of the CSR); errors are the same (lowest failing vertex first).  Errors: ISING_E_GRAPH
+ * (message names the offending vertex/entry), ISING_E_UNSUPPORTED (BITS with weights not
+ * +-1, float weights with BITS), ISING_E_ARG, ISING_E_CUDA/OOM. */
 ISING_API int ising_create_csr(int32_t n, const int64_t *row_ptr, const int32_t *col, const void *w,
                      int32_t wtype, const int32_t *colour, const ising_run_desc *desc,
                      ising_handle **out);
@@ -300,6 +311,13 @@ ISING_API int ising_greedy_colour(int32_t n, const int64_t *row_ptr, const int32
  * int32 (caller-owned).  Returns the number of colours, or ISING_E_ARG on NULL / n < 1. */
 ISING_API int ising_greedy_colour_sl(int32_t n, const int64_t *row_ptr, const int32_t *col,
                         int32_t *colour_out);
+
+/* The Jones-Plassmann-order greedy colouring (ISING_COLOUR_JP) as ising_create_csr computes
+ * it, on GPU `device` (syncs): row_ptr n+1 int64, col row_ptr[n] int32 (symmetric, ids in
+ * range); colour_out n int32 (caller-owned).  Returns the number of colours, or < 0 on error
+ * (ISING_E_ARG, ISING_E_GRAPH for a bad row_ptr or column id, ISING_E_CUDA). */
+ISING_API int ising_colour_jp(int32_t device, int32_t n, const int64_t *row_ptr, const int32_t *col,
+                              int32_t *colour_out);
 
 /* Metropolis threshold floor(exp(-(beta*dE)) * 2^64) saturated to 2^64-1, as the
  * library's host tables compute it (integer dE > 0). */

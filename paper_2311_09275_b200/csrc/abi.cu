@@ -112,7 +112,7 @@ struct ising_handle {
     bool xc_ok = false;   // grid BITS, 2 bands: cooperative fused launch with copies over K/32 clusters
     bool sched_ok = false;     // grid BITS, 1 band: persistent ticket-scheduled fused launch (k_grid_sched)
     int32_t sched_ctas = 0;    // its resident CTAs
-    uint32_t *d_xs_ctl = nullptr, *d_xs_B = nullptr, *d_xs_M = nullptr;
+    uint32_t *d_xs_ctl = nullptr, *d_xs_B = nullptr, *d_xs_M = nullptr, *d_xs_S = nullptr;
     int64_t *d_xs_E = nullptr;
     int64_t *d_xc_E = nullptr;
     uint32_t *d_xc_B = nullptr, *d_xc_bar = nullptr;
@@ -220,6 +220,8 @@ int validate_desc(const ising_run_desc *d)
                                          std::to_string(d->device));
         cudaGetLastError();
     }
+    if (d->colouring != ISING_COLOUR_GREEDY && d->colouring != ISING_COLOUR_JP)
+        return fail(ISING_E_ARG, "unknown colouring");
     if (d->block_threads != 0 && (d->block_threads < 32 || d->block_threads > 1024 ||
                                   d->block_threads % 32 != 0))
         return fail(ISING_E_ARG, "block_threads must be 0 or a multiple of 32 in [32, 1024]");
@@ -401,6 +403,7 @@ GridBitsParams grid_params(ising_handle *h, int32_t n_rounds, int32_t k_ex, bool
     p.xs_E = h->d_xs_E;
     p.xs_B = h->d_xs_B;
     p.xs_M = h->d_xs_M;
+    p.xs_S = h->d_xs_S;
     return p;
 }
 
@@ -490,6 +493,95 @@ int32_t par_first_failing(int32_t n, F &&check)
     return *std::min_element(bad.begin(), bad.end());
 }
 
+// Row checks of vertex i in (entry) order: range, self-loop, duplicate of an earlier entry,
+// finite weight.  False with the message of the first failing entry.
+bool csr_row_ok(int32_t n, const int64_t *row_ptr, const int32_t *col, const int32_t *wi, const float *wf,
+                int32_t i, std::string *msg)
+{
+    const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    const bool small = e1 - e0 <= 64;
+    std::vector<int32_t> seen;  // earlier entries of a long row, kept sorted
+    for (int64_t e = e0; e < e1; ++e) {
+        const int32_t j = col[e];
+        if (j < 0 || j >= n) {
+            if (msg)
+                *msg = "col[" + std::to_string(e) + "] = " + std::to_string(j) + " out of range at vertex " +
+                       std::to_string(i);
+            return false;
+        }
+        if (j == i) {
+            if (msg)
+                *msg = "self-loop at vertex " + std::to_string(i);
+            return false;
+        }
+        bool dup = false;
+        if (small) {
+            for (int64_t f = e0; f < e && !dup; ++f)
+                dup = col[f] == j;
+        } else {
+            const auto it = std::lower_bound(seen.begin(), seen.end(), j);
+            dup = it != seen.end() && *it == j;
+            if (!dup)
+                seen.insert(it, j);
+        }
+        if (dup) {
+            if (msg)
+                *msg = "duplicate edge " + std::to_string(i) + "-" + std::to_string(j);
+            return false;
+        }
+        if (wf && !std::isfinite(wf[e])) {
+            if (msg)
+                *msg = "non-finite weight at entry " + std::to_string(e);
+            return false;
+        }
+    }
+    return true;
+}
+
+// Symmetry of vertex i's row: (i, j, w) present iff (j, i, w).
+bool csr_sym_ok(const int64_t *row_ptr, const int32_t *col, const int32_t *wi, const float *wf, int32_t i,
+                std::string *msg)
+{
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+        const int32_t j = col[e];
+        bool found = false;
+        for (int64_t f = row_ptr[j]; f < row_ptr[j + 1]; ++f)
+            if (col[f] == i) {
+                found = wi ? (wi[f] == wi[e]) : (wf[f] == wf[e]);
+                break;
+            }
+        if (!found) {
+            if (msg)
+                *msg = "asymmetric coupling " + std::to_string(i) + "-" + std::to_string(j);
+            return false;
+        }
+    }
+    return true;
+}
+
+// Device buffers that live only during create (returned to the stream-ordered pool).
+struct CreateTmp {
+    cudaStream_t st;
+    std::vector<void *> ptrs;
+    template <class T>
+    cudaError_t alloc(T **p, size_t count)
+    {
+        *p = nullptr;
+        cudaError_t e = cudaMallocAsync((void **)p, (count ? count : 1) * sizeof(T), st);
+        if (e == cudaSuccess)
+            ptrs.push_back((void *)*p);
+        return e;
+    }
+    ~CreateTmp()
+    {
+        for (void *p : ptrs)
+            cudaFreeAsync(p, st);
+    }
+};
+
+int create_csr_i8_device(int32_t n, const int64_t *row_ptr, const int32_t *col, const void *w, int32_t wtype,
+                         const int32_t *colour, const ising_run_desc *desc, ising_handle **out);
+
 int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const void *w,
                     int32_t wtype, const int32_t *colour, const ising_run_desc *desc,
                     ising_handle **out)
@@ -528,19 +620,16 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
         sum_abs += s;
     }
     sum_abs /= 2;
-    if (desc->layout == ISING_SPINS_BITS) {
-        if (!desc->block_threads)
-            h->threads = kCsrMaxThreads;
-        if (h->threads > kCsrMaxThreads)
-            return fail(ISING_E_ARG, "BITS: block_threads must be <= " + std::to_string(kCsrMaxThreads));
-        if (!wi || !pm1)
-            return fail(ISING_E_UNSUPPORTED, "BITS layout needs integer weights in {-1,+1}");
-        if (maxdeg > 15)
-            return fail(ISING_E_UNSUPPORTED, "BITS layout supports degree <= 15");
-        h->kernel = KER_CSR_BITS;
-    } else {
-        h->kernel = KER_CSR_I8;
-    }
+    // (the int8 layout is created on the device: create_csr_i8_device)
+    if (!desc->block_threads)
+        h->threads = kCsrMaxThreads;
+    if (h->threads > kCsrMaxThreads)
+        return fail(ISING_E_ARG, "BITS: block_threads must be <= " + std::to_string(kCsrMaxThreads));
+    if (!wi || !pm1)
+        return fail(ISING_E_UNSUPPORTED, "BITS layout needs integer weights in {-1,+1}");
+    if (maxdeg > 15)
+        return fail(ISING_E_UNSUPPORTED, "BITS layout supports degree <= 15");
+    h->kernel = KER_CSR_BITS;
     h->qmax = (int32_t)qmax;
 
     // colouring
@@ -577,13 +666,31 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
                 return fail(ISING_E_GRAPH, "colour ids must be 0..ncol-1 without gaps (missing " +
                                                std::to_string(c) + ")");
         h->ncol = mx + 1;
+    } else if (desc->colouring == ISING_COLOUR_JP) {  // on the device, as for the int8 layout
+        CK(cudaSetDevice(h->device));
+        CreateTmp tmp{h->st, {}};
+        int64_t *d_rp64;
+        int32_t *d_c, *d_colour, *d_cnt;
+        uint32_t *d_prio;
+        CK(tmp.alloc(&d_rp64, (size_t)n + 1));
+        CK(tmp.alloc(&d_c, (size_t)row_ptr[n]));
+        CK(tmp.alloc(&d_colour, (size_t)n));
+        CK(tmp.alloc(&d_prio, (size_t)n));
+        CK(tmp.alloc(&d_cnt, 2));
+        CK(cudaMemcpyAsync(d_rp64, row_ptr, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, h->st));
+        CK(cudaMemcpyAsync(d_c, col, (size_t)row_ptr[n] * 4, cudaMemcpyHostToDevice, h->st));
+        int32_t ncol = 0;
+        CK(colour_jp_device(n, d_rp64, d_c, d_prio, d_colour, d_cnt, &ncol, h->st));
+        CK(cudaMemcpyAsync(col_of.data(), d_colour, (size_t)n * 4, cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        h->ncol = ncol;
     } else {
         h->ncol = ising_greedy_colour(n, row_ptr, col, col_of.data());
         if (h->ncol < 0)
             return h->ncol;
     }
 
-    // internal order: (colour, [degree for BITS], original id)
+    // internal order: (colour, degree, original id)
     h->orig.resize(n);
     const bool by_deg = h->kernel == KER_CSR_BITS;
     {  // counting sort by key (colour, [degree]), ids ascending inside a key: O(n + keys)
@@ -662,62 +769,6 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
         CK(h->alloc(&h->d_copy_best, (size_t)h->C_local * 3));
         CK(h->alloc(&h->d_snap, (size_t)h->C_local * n));
         CK(launch_init_bits(h->d_state[0], h->G, n, h->d_orig, h->g0, h->rk, h->st));
-    } else {
-        CK(h->alloc(&h->d_col, m2));
-        CK(cudaMemcpyAsync(h->d_col, ci.data(), (size_t)m2 * 4, cudaMemcpyHostToDevice, h->st));
-        if (wi) {
-            CK(h->alloc(&h->d_wi, m2));
-            CK(cudaMemcpyAsync(h->d_wi, wiv.data(), (size_t)m2 * 4, cudaMemcpyHostToDevice, h->st));
-            // per LOCAL replica r (temperature k = (slot0 + r) mod K): T_r[r][q], q = dE/2
-            std::vector<uint64_t> Tk = accept_table(h->betas, h->qmax);
-            std::vector<uint64_t> T((size_t)h->R * (h->qmax + 1));
-            for (int64_t r = 0; r < h->R; ++r) {
-                const int32_t k = (int32_t)((h->slot0 + r) % h->K);
-                std::copy(Tk.begin() + (size_t)k * (h->qmax + 1), Tk.begin() + (size_t)(k + 1) * (h->qmax + 1),
-                          T.begin() + (size_t)r * (h->qmax + 1));
-            }
-            CK(h->alloc(&h->d_T, T.size()));
-            CK(cudaMemcpyAsync(h->d_T, T.data(), T.size() * 8, cudaMemcpyHostToDevice, h->st));
-        } else {
-            CK(h->alloc(&h->d_wf, m2));
-            CK(cudaMemcpyAsync(h->d_wf, wfv.data(), (size_t)m2 * 4, cudaMemcpyHostToDevice, h->st));
-            std::vector<float> bf(h->R);
-            for (int64_t r = 0; r < h->R; ++r)
-                bf[r] = 2.0f * (float)h->betas[(h->slot0 + r) % h->K];  // exact doubling
-            CK(h->alloc(&h->d_betaf, h->R));
-            CK(cudaMemcpyAsync(h->d_betaf, bf.data(), h->R * 4, cudaMemcpyHostToDevice, h->st));
-        }
-        if (maxdeg <= 4) {
-            h->ell_deg = maxdeg;
-            // padded 4-wide neighbour table (row order kept, pad col = self, w = 0)
-            // pads point at the vertex itself with weight 0: the kernel loads them
-            // unconditionally, own ^ own = 0 and the term is an exact zero
-            std::vector<int32_t> ec((size_t)n * 4, -1), ew((size_t)n * 4, 0);
-            for (int32_t v = 0; v < n; ++v)
-                for (int32_t u = 0; u < 4; ++u)
-                    ec[(size_t)v * 4 + u] = v;
-            for (int32_t v = 0; v < n; ++v)
-                for (int32_t u = 0; u < rp[v + 1] - rp[v]; ++u) {
-                    ec[(size_t)v * 4 + u] = ci[rp[v] + u];
-                    if (wi)
-                        ew[(size_t)v * 4 + u] = wiv[rp[v] + u];
-                    else
-                        std::memcpy(&ew[(size_t)v * 4 + u], &wfv[rp[v] + u], 4);
-                }
-            CK(h->alloc(&h->d_ell_col, ec.size()));
-            CK(h->alloc(&h->d_ell_w, ew.size()));
-            CK(cudaMemcpyAsync(h->d_ell_col, ec.data(), ec.size() * 4, cudaMemcpyHostToDevice, h->st));
-            CK(cudaMemcpyAsync(h->d_ell_w, ew.data(), ew.size() * 4, cudaMemcpyHostToDevice, h->st));
-            CK(cudaStreamSynchronize(h->st));  // host vectors die at scope end
-        }
-        CK(h->alloc(&h->d_s8, (size_t)n * h->R));
-        if (small_i8(h.get())) {  // fused PT launch scratch (k_i8_small)
-            CK(h->alloc(&h->d_copy_best, (size_t)h->C_local * 3));
-            CK(h->alloc(&h->d_snap, (size_t)h->C_local * n));
-        }
-        h->scratch_bytes = energy_i8_scratch(n, (int32_t)h->R);
-        CK(h->alloc((char **)&h->d_scratch, h->scratch_bytes));
-        CK(launch_init_i8(h->d_s8, n, (int32_t)h->R, h->d_orig, h->slot0, h->rk, h->st));
     }
     rc = refresh_energy(h.get());
     if (rc)
@@ -727,6 +778,174 @@ int create_csr_impl(int32_t n, const int64_t *row_ptr, const int32_t *col, const
     h->fingerprint = fnv1a(h->fingerprint, col, (size_t)m2 * 4);
     h->fingerprint = fnv1a(h->fingerprint, w, (size_t)m2 * 4);
     h->fingerprint = fnv1a(h->fingerprint, h->orig.data(), h->orig.size() * 4);
+    h->fingerprint = fnv1a(h->fingerprint, h->betas.data(), h->betas.size() * 8);
+    *out = h.release();
+    return ISING_OK;
+}
+
+// ising_create_csr for the int8 layout: the caller's CSR is uploaded once and
+// validated, coloured (caller colouring validated, or Jones-Plassmann on the device, or the
+// ascending-id greedy on the host), put in the colour-sorted internal order and turned into
+// the internal CSR / padded tables by kernels (k_create.cu).  Same checks, error precedence,
+// internal order and tables as the host path of the bit-packed layout.
+int create_csr_i8_device(int32_t n, const int64_t *row_ptr, const int32_t *col, const void *w, int32_t wtype,
+                         const int32_t *colour, const ising_run_desc *desc, ising_handle **out)
+{
+    std::unique_ptr<ising_handle> h(new ising_handle());
+    h->n = n;
+    h->wtype = wtype;
+    h->kernel = KER_CSR_I8;
+    fill_run(h.get(), desc);
+    const int64_t m2 = row_ptr[n];
+    if (m2 >= ((int64_t)1 << 31) - 1)
+        return fail(ISING_E_UNSUPPORTED, "more than 2^31-1 directed edges");
+    h->m = m2 / 2;
+    const int32_t *wi = wtype == ISING_W_I32 ? (const int32_t *)w : nullptr;
+    const float *wf = wtype == ISING_W_F32 ? (const float *)w : nullptr;
+    CK(cudaSetDevice(h->device));
+    CreateTmp tmp{h->st, {}};
+    int64_t *d_rp64;
+    int32_t *d_colin, *d_colour, *d_jp;
+    uint32_t *d_win, *d_prio;
+    CsrCheck *d_chk;
+    uint8_t *d_used;
+    CK(tmp.alloc(&d_rp64, (size_t)n + 1));
+    CK(tmp.alloc(&d_colin, (size_t)m2));
+    CK(tmp.alloc(&d_win, (size_t)m2));
+    CK(tmp.alloc(&d_colour, (size_t)n));
+    CK(tmp.alloc(&d_chk, 1));
+    CK(tmp.alloc(&d_used, (size_t)1 << 16));
+    CK(tmp.alloc(&d_jp, 2));
+    CK(cudaMemcpyAsync(d_rp64, row_ptr, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(d_colin, col, (size_t)m2 * 4, cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(d_win, w, (size_t)m2 * 4, cudaMemcpyHostToDevice, h->st));
+    if (colour)
+        CK(cudaMemcpyAsync(d_colour, colour, (size_t)n * 4, cudaMemcpyHostToDevice, h->st));
+    CK(launch_csr_check(n, d_rp64, d_colin, wi ? (const int32_t *)d_win : nullptr,
+                        wf ? (const float *)d_win : nullptr, colour ? d_colour : nullptr, d_chk, d_used, h->st));
+    CsrCheck chk;
+    CK(cudaMemcpyAsync(&chk, d_chk, sizeof(chk), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    // errors in the host path's order: row checks, symmetry, the |w| guard, the colouring
+    if (chk.bad_row != INT32_MAX || chk.bad_sym != INT32_MAX) {
+        std::string msg;
+        if (chk.bad_row != INT32_MAX)
+            csr_row_ok(n, row_ptr, col, wi, wf, chk.bad_row, &msg);
+        else
+            csr_sym_ok(row_ptr, col, wi, wf, chk.bad_sym, &msg);
+        return fail(ISING_E_GRAPH, msg);
+    }
+    if (chk.bad_sum != INT32_MAX)
+        return fail(ISING_E_GRAPH, "sum of |w| at vertex " + std::to_string(chk.bad_sum) + " >= 2^30");
+    if (colour) {
+        if (chk.bad_colrange != INT32_MAX)
+            return fail(ISING_E_GRAPH, "colour of vertex " + std::to_string(chk.bad_colrange) + " out of range");
+        if (chk.bad_proper != INT32_MAX) {
+            const int32_t i = chk.bad_proper;
+            int32_t j = -1;
+            for (int64_t e = row_ptr[i]; e < row_ptr[i + 1] && j < 0; ++e)
+                if (colour[col[e]] == colour[i])
+                    j = col[e];
+            return fail(ISING_E_GRAPH, "improper colouring: vertices " + std::to_string(i) + " and " +
+                                           std::to_string(j) + " share colour");
+        }
+        std::vector<uint8_t> used((size_t)chk.max_colour + 1);
+        CK(cudaMemcpyAsync(used.data(), d_used, used.size(), cudaMemcpyDeviceToHost, h->st));
+        CK(cudaStreamSynchronize(h->st));
+        for (int32_t c = 0; c <= chk.max_colour; ++c)
+            if (!used[c])
+                return fail(ISING_E_GRAPH, "colour ids must be 0..ncol-1 without gaps (missing " +
+                                               std::to_string(c) + ")");
+        h->ncol = chk.max_colour + 1;
+    } else if (desc->colouring == ISING_COLOUR_JP) {
+        CK(tmp.alloc(&d_prio, (size_t)n));
+        int32_t ncol = 0;
+        CK(colour_jp_device(n, d_rp64, d_colin, d_prio, d_colour, d_jp, &ncol, h->st));
+        h->ncol = ncol;
+    } else {  // ascending-id greedy (host, sequential by definition)
+        std::vector<int32_t> col_of(n);
+        h->ncol = ising_greedy_colour(n, row_ptr, col, col_of.data());
+        if (h->ncol < 0)
+            return h->ncol;
+        CK(cudaMemcpyAsync(d_colour, col_of.data(), (size_t)n * 4, cudaMemcpyHostToDevice, h->st));
+        CK(cudaStreamSynchronize(h->st));
+    }
+    h->qmax = (int32_t)chk.qmax;
+    h->W_int = chk.W_int;
+    const int32_t maxdeg = chk.maxdeg;
+    // colour-sorted internal order (ids ascending inside a class) and the internal CSR
+    CK(h->alloc(&h->d_orig, n));
+    CK(h->alloc(&h->d_o2i, n));
+    CK(h->alloc(&h->d_class_off, h->ncol + 1));
+    CK(h->alloc(&h->d_rp, (size_t)n + 1));
+    CK(build_order_device(n, h->ncol, d_colour, d_rp64, h->d_orig, h->d_o2i, h->d_class_off, h->d_rp, h->st));
+    CK(h->alloc(&h->d_col, m2));
+    uint32_t *d_wo;
+    if (wi) {
+        CK(h->alloc(&h->d_wi, m2));
+        d_wo = (uint32_t *)h->d_wi;
+    } else {
+        CK(h->alloc(&h->d_wf, m2));
+        d_wo = (uint32_t *)h->d_wf;
+    }
+    if (maxdeg <= 4) {
+        h->ell_deg = maxdeg;
+        CK(h->alloc(&h->d_ell_col, (size_t)n * 4));
+        CK(h->alloc(&h->d_ell_w, (size_t)n * 4));
+    }
+    CK(launch_build_internal(n, d_rp64, d_colin, d_win, h->d_orig, h->d_o2i, h->d_rp, h->d_col, d_wo,
+                             h->d_ell_col, (uint32_t *)h->d_ell_w, h->st));
+    unsigned long long *d_hash;
+    CK(tmp.alloc(&d_hash, 1));
+    CK(cudaMemsetAsync(d_hash, 0, 8, h->st));
+    CK(launch_hash_order(n, h->d_orig, d_hash, h->st));
+    h->class_off.assign(h->ncol + 1, 0);
+    CK(cudaMemcpyAsync(h->class_off.data(), h->d_class_off, (h->ncol + 1) * 4, cudaMemcpyDeviceToHost, h->st));
+    int rc = build_common_device(h.get(), chk.sum_abs / 2);
+    if (rc)
+        return rc;
+    if (wi) {  // per LOCAL replica r (temperature k = (slot0 + r) mod K): T_r[r][q], q = dE/2
+        std::vector<uint64_t> Tk = accept_table(h->betas, h->qmax);
+        std::vector<uint64_t> T((size_t)h->R * (h->qmax + 1));
+        for (int64_t r = 0; r < h->R; ++r) {
+            const int32_t k = (int32_t)((h->slot0 + r) % h->K);
+            std::copy(Tk.begin() + (size_t)k * (h->qmax + 1), Tk.begin() + (size_t)(k + 1) * (h->qmax + 1),
+                      T.begin() + (size_t)r * (h->qmax + 1));
+        }
+        CK(h->alloc(&h->d_T, T.size()));
+        CK(cudaMemcpyAsync(h->d_T, T.data(), T.size() * 8, cudaMemcpyHostToDevice, h->st));
+        CK(cudaStreamSynchronize(h->st));
+    } else {
+        std::vector<float> bf(h->R);
+        for (int64_t r = 0; r < h->R; ++r)
+            bf[r] = 2.0f * (float)h->betas[(h->slot0 + r) % h->K];  // exact doubling
+        CK(h->alloc(&h->d_betaf, h->R));
+        CK(cudaMemcpyAsync(h->d_betaf, bf.data(), h->R * 4, cudaMemcpyHostToDevice, h->st));
+        CK(cudaStreamSynchronize(h->st));
+    }
+    CK(h->alloc(&h->d_s8, (size_t)n * h->R));
+    if (small_i8(h.get())) {  // fused PT launch scratch (k_i8_small)
+        CK(h->alloc(&h->d_copy_best, (size_t)h->C_local * 3));
+        CK(h->alloc(&h->d_snap, (size_t)h->C_local * n));
+    }
+    h->scratch_bytes = energy_i8_scratch(n, (int32_t)h->R);
+    CK(h->alloc((char **)&h->d_scratch, h->scratch_bytes));
+    CK(launch_init_i8(h->d_s8, n, (int32_t)h->R, h->d_orig, h->slot0, h->rk, h->st));
+    rc = refresh_energy(h.get());
+    if (rc)
+        return rc;
+    // float weights: W = sum of w over edges in edge order, in float64 (a sequential sum, on
+    // the host while the device initialises)
+    if (wf)
+        for (int32_t i = 0; i < n; ++i)
+            for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e)
+                if (col[e] > i)
+                    h->W_f += (double)wf[e];
+    unsigned long long order_hash = 0;
+    CK(cudaMemcpyAsync(&order_hash, d_hash, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    const uint64_t hv[3] = {chk.hash, order_hash, (uint64_t)n};
+    h->fingerprint = fnv1a(kFnvBasis, hv, sizeof(hv));
     h->fingerprint = fnv1a(h->fingerprint, h->betas.data(), h->betas.size() * 8);
     *out = h.release();
     return ISING_OK;
@@ -846,15 +1065,14 @@ int check_handle(const ising_handle *h)
     return ISING_OK;
 }
 
-// Copy one local slot's configuration (original ids) into d_tmp.
+// Copy one local slot's configuration (original ids, original order) into d_tmp.
 int slot_to_tmp(ising_handle *h, int64_t rl)
 {
     if (h->layout == ISING_SPINS_BITS) {
         CK(launch_extract_bits(h->d_state[h->cur], h->n, (int32_t)(rl / 32), (int32_t)(rl % 32),
                                h->kernel == KER_GRID_BITS ? nullptr : h->d_o2i, h->d_tmp, h->st));
     } else {
-        CK(cudaMemcpy2DAsync(h->d_tmp, 1, h->d_s8 + rl, (size_t)h->R, 1, h->n,
-                             cudaMemcpyDeviceToDevice, h->st));
+        CK(launch_extract_i8(h->d_s8, h->R, h->n, rl, h->d_o2i, h->d_tmp, h->st));
     }
     return ISING_OK;
 }
@@ -893,6 +1111,39 @@ int ising_greedy_colour(int32_t n, const int64_t *row_ptr, const int32_t *col, i
         colour_out[i] = c;
         ncol = std::max(ncol, c + 1);
     }
+    return ncol;
+}
+
+int ising_colour_jp(int32_t device, int32_t n, const int64_t *row_ptr, const int32_t *col, int32_t *colour_out)
+{
+    g_err.clear();
+    if (n < 1 || !row_ptr || !col || !colour_out)
+        return fail(ISING_E_ARG, "NULL argument or n < 1");
+    if (row_ptr[0] != 0)
+        return fail(ISING_E_GRAPH, "row_ptr[0] != 0");
+    for (int32_t i = 0; i < n; ++i)
+        if (row_ptr[i + 1] < row_ptr[i])
+            return fail(ISING_E_GRAPH, "row_ptr decreases at vertex " + std::to_string(i));
+    for (int64_t e = 0; e < row_ptr[n]; ++e)
+        if (col[e] < 0 || col[e] >= n)
+            return fail(ISING_E_GRAPH, "col[" + std::to_string(e) + "] out of range");
+    CK(cudaSetDevice(device));
+    cudaStream_t st = nullptr;
+    CreateTmp tmp{st, {}};
+    int64_t *d_rp64;
+    int32_t *d_c, *d_colour, *d_cnt;
+    uint32_t *d_prio;
+    CK(tmp.alloc(&d_rp64, (size_t)n + 1));
+    CK(tmp.alloc(&d_c, (size_t)row_ptr[n]));
+    CK(tmp.alloc(&d_colour, (size_t)n));
+    CK(tmp.alloc(&d_prio, (size_t)n));
+    CK(tmp.alloc(&d_cnt, 2));
+    CK(cudaMemcpyAsync(d_rp64, row_ptr, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_c, col, (size_t)row_ptr[n] * 4, cudaMemcpyHostToDevice, st));
+    int32_t ncol = 0;
+    CK(colour_jp_device(n, d_rp64, d_c, d_prio, d_colour, d_cnt, &ncol, st));
+    CK(cudaMemcpyAsync(colour_out, d_colour, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     return ncol;
 }
 
@@ -1102,8 +1353,8 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
                 colour[i] = (x + y) & 1;
             }
         rp[n] = 4 * (int64_t)n;
-        rc = create_csr_impl(n, rp.data(), col.data(), w.data(), ISING_W_I32, colour.data(), desc,
-                             out);
+        rc = create_csr_i8_device(n, rp.data(), col.data(), w.data(), ISING_W_I32, colour.data(), desc,
+                                  out);
         if (rc == ISING_OK) {
             (*out)->Lx = Lx;
             (*out)->Ly = Ly;
@@ -1211,6 +1462,7 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
             CK(h->alloc(&h->d_xs_E, (size_t)h->G * 32));
             CK(h->alloc(&h->d_xs_B, (size_t)2 * h->G * 2 * nbw));
             CK(h->alloc(&h->d_xs_M, (size_t)h->C_local * h->wpc));
+            CK(h->alloc(&h->d_xs_S, (size_t)h->G * n));
             h->sched_ok = true;
             h->sched_ctas = std::min(ctas, h->G);
         }
@@ -1288,68 +1540,15 @@ int ising_create_csr(int32_t n, const int64_t *row_ptr, const int32_t *col, cons
             return fail(ISING_E_GRAPH, "row_ptr decreases at vertex " + std::to_string(i));
     const int32_t *wi = wtype == ISING_W_I32 ? (const int32_t *)w : nullptr;
     const float *wf = wtype == ISING_W_F32 ? (const float *)w : nullptr;
-    // Row checks in (vertex, entry) order: range, self-loop, duplicate of an earlier entry,
-    // finite weight.  Rows are independent, so the vertices are checked on host threads; the
-    // error reported is the one of the lowest failing vertex (the first one a sequential scan
-    // meets), its message produced by re-checking that row.
-    auto check_row = [&](int32_t i, std::string *msg) -> bool {
-        const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
-        const bool small = e1 - e0 <= 64;
-        std::vector<int32_t> seen;  // earlier entries of a long row, kept sorted
-        for (int64_t e = e0; e < e1; ++e) {
-            const int32_t j = col[e];
-            if (j < 0 || j >= n) {
-                if (msg)
-                    *msg = "col[" + std::to_string(e) + "] = " + std::to_string(j) + " out of range at vertex " +
-                           std::to_string(i);
-                return false;
-            }
-            if (j == i) {
-                if (msg)
-                    *msg = "self-loop at vertex " + std::to_string(i);
-                return false;
-            }
-            bool dup = false;
-            if (small) {
-                for (int64_t f = e0; f < e && !dup; ++f)
-                    dup = col[f] == j;
-            } else {
-                const auto it = std::lower_bound(seen.begin(), seen.end(), j);
-                dup = it != seen.end() && *it == j;
-                if (!dup)
-                    seen.insert(it, j);
-            }
-            if (dup) {
-                if (msg)
-                    *msg = "duplicate edge " + std::to_string(i) + "-" + std::to_string(j);
-                return false;
-            }
-            if (wf && !std::isfinite(wf[e])) {
-                if (msg)
-                    *msg = "non-finite weight at entry " + std::to_string(e);
-                return false;
-            }
-        }
-        return true;
-    };
-    // symmetry: (i, j, w) present iff (j, i, w)
-    auto check_sym = [&](int32_t i, std::string *msg) -> bool {
-        for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
-            const int32_t j = col[e];
-            bool found = false;
-            for (int64_t f = row_ptr[j]; f < row_ptr[j + 1]; ++f)
-                if (col[f] == i) {
-                    found = wi ? (wi[f] == wi[e]) : (wf[f] == wf[e]);
-                    break;
-                }
-            if (!found) {
-                if (msg)
-                    *msg = "asymmetric coupling " + std::to_string(i) + "-" + std::to_string(j);
-                return false;
-            }
-        }
-        return true;
-    };
+    // int8 layout: validation, colouring, internal order and tables on the device (k_create.cu)
+    if (desc->layout == ISING_SPINS_I8)
+        return create_csr_i8_device(n, row_ptr, col, w, wtype, colour, desc, out);
+    // Row checks in (vertex, entry) order, then symmetry.  Rows are independent, so the
+    // vertices are checked on host threads; the error reported is the one of the lowest
+    // failing vertex (the first one a sequential scan meets), its message produced by
+    // re-checking that row.
+    auto check_row = [&](int32_t i, std::string *msg) { return csr_row_ok(n, row_ptr, col, wi, wf, i, msg); };
+    auto check_sym = [&](int32_t i, std::string *msg) { return csr_sym_ok(row_ptr, col, wi, wf, i, msg); };
     for (int pass = 0; pass < 2; ++pass) {
         const int32_t i = pass == 0 ? par_first_failing(n, check_row) : par_first_failing(n, check_sym);
         if (i < n) {
@@ -1751,19 +1950,11 @@ int ising_get_spins(ising_handle *h, int64_t slot, int8_t *out)
         return fail(ISING_E_ARG, "out is NULL");
     if (slot < h->slot0 || slot >= h->slot0 + h->R)
         return fail(ISING_E_STATE, "slot " + std::to_string(slot) + " is not held by this handle");
-    rc = slot_to_tmp(h, slot - h->slot0);
+    rc = slot_to_tmp(h, slot - h->slot0);  // original order
     if (rc)
         return rc;
-    if (h->kernel == KER_CSR_I8) {
-        std::vector<int8_t> tmp(h->n);
-        CK(cudaMemcpyAsync(tmp.data(), h->d_tmp, h->n, cudaMemcpyDeviceToHost, h->st));
-        CK(cudaStreamSynchronize(h->st));
-        for (int32_t i = 0; i < h->n; ++i)
-            out[i] = tmp[h->o2i[i]];
-    } else {
-        CK(cudaMemcpyAsync(out, h->d_tmp, h->n, cudaMemcpyDeviceToHost, h->st));
-        CK(cudaStreamSynchronize(h->st));
-    }
+    CK(cudaMemcpyAsync(out, h->d_tmp, h->n, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
     return ISING_OK;
 }
 
@@ -1784,13 +1975,9 @@ int ising_set_spins(ising_handle *h, int64_t slot, const int8_t *in)
         CK(cudaMemcpyAsync(h->d_tmp, in, h->n, cudaMemcpyHostToDevice, h->st));
         CK(launch_insert_bits(h->d_state[h->cur], h->n, (int32_t)(rl / 32), (int32_t)(rl % 32),
                               h->kernel == KER_GRID_BITS ? nullptr : h->d_o2i, h->d_tmp, h->st));
-    } else {
-        std::vector<int8_t> tmp(h->n);
-        for (int32_t v = 0; v < h->n; ++v)
-            tmp[v] = in[h->orig[v]];
-        CK(cudaMemcpyAsync(h->d_tmp, tmp.data(), h->n, cudaMemcpyHostToDevice, h->st));
-        CK(cudaMemcpy2DAsync(h->d_s8 + rl, (size_t)h->R, h->d_tmp, 1, 1, h->n,
-                             cudaMemcpyDeviceToDevice, h->st));
+    } else {  // scatter through the internal order on the device
+        CK(cudaMemcpyAsync(h->d_tmp, in, h->n, cudaMemcpyHostToDevice, h->st));
+        CK(launch_insert_i8(h->d_s8, h->R, h->n, rl, h->d_o2i, h->d_tmp, h->st));
         CK(cudaStreamSynchronize(h->st));
     }
     rc = refresh_energy(h);

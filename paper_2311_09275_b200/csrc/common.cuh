@@ -9,7 +9,8 @@
 
 namespace ising {
 
-enum : uint32_t { ST_INIT = 0, ST_PLANE = 1, ST_WORD_HI = 2, ST_WORD_LO = 3, ST_EXCH = 4, ST_ICM = 5 };
+enum : uint32_t { ST_INIT = 0, ST_PLANE = 1, ST_WORD_HI = 2, ST_WORD_LO = 3, ST_EXCH = 4, ST_ICM = 5,
+                  ST_COLOUR = 6 };
 
 struct RoundKeys {
     uint32_t k[20];  // (k0, k1) for rounds 0..9

@@ -35,6 +35,18 @@ using namespace bits;
 // tail-queue item: {l | i_orig << 16, D, acc, m8} (the own word is re-read from S)
 constexpr int kGridQItem = 16;
 
+__device__ __forceinline__ void sts_u128(uint32_t a, uint4 v)
+{
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w));
+}
+
+__device__ __forceinline__ uint4 lds_u128(uint32_t a)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+
 // Site geometry of one thread in the 2-D mapping (column m of a colour class,
 // rows ty, ty + rpp, ...).
 struct ThreadGeom {
@@ -60,10 +72,11 @@ struct Ctx {
     int wlim;         // per-warp stage-2 limit
     int offR1, offL0; // horizontal neighbour offsets of the class column
     uint32_t hx4, wrapDb, wrapUb, sS, sJB;
+    uint32_t sQw;     // shared address of this warp's tail-queue region
 };
 
 __device__ __forceinline__ Ctx make_ctx(const GridGeom &G, int n, int qcap, const uint32_t *S, const uint8_t *JB,
-                                        bool SPILL)
+                                        const uint4 *Q4, bool SPILL)
 {
     Ctx X;
     X.G = G;
@@ -101,6 +114,7 @@ __device__ __forceinline__ Ctx make_ctx(const GridGeom &G, int n, int qcap, cons
     X.wrapUb = 4u * (uint32_t)((G.Ly - 1) * G.hx);
     X.sS = (uint32_t)__cvta_generic_to_shared(S);
     X.sJB = (uint32_t)__cvta_generic_to_shared(JB);
+    X.sQw = (uint32_t)__cvta_generic_to_shared(Q4) + 16u * (uint32_t)X.wq0;
     X.T.ty = X.tid / G.hx;
     X.T.m = X.tid - X.T.ty * G.hx;
     X.T.mL = X.T.m == 0 ? G.hx - 1 : X.T.m - 1;
@@ -181,11 +195,11 @@ __device__ __forceinline__ void finish_inline(uint32_t i_orig, const PlaneUnifor
 }
 
 // One colour phase c of sweep t for word group g: stage 1 over the thread's passes (+ the
-// leftover rows on the column-less warps), then the warp's own stage-2 queue, then a CTA
-// barrier.  S: colour-separated spins; Q4: tail queue; P: the word type's planes.
+// leftover rows on the column-less warps), then the warp's own stage-2 queue (X.sQw), then a
+// CTA barrier.  Spins (X.sS) in colour-separated order; P: the word type's planes.
 template <bool SPILL>
 __device__ __forceinline__ void colour_phase(const Ctx &X, int c, const PlaneUniform &U, const RoundKeys &rkr,
-                                             const uint32_t *P, uint4 *Q4)
+                                             const uint32_t *P)
 {
     const GridGeom &G = X.G;
     const ThreadGeom &T = X.T;
@@ -202,11 +216,12 @@ __device__ __forceinline__ void colour_phase(const Ctx &X, int c, const PlaneUni
     const uint32_t offLb = 4u * (uint32_t)(par ? 0 : X.offL0);
     const uint32_t rstep = (uint32_t)(X.rpp * hx), istep = (uint32_t)(G.Lx * X.rpp);
     uint32_t i_orig = (uint32_t)(2 * T.m + par + G.Lx * T.ty);
+    uint32_t lq = l0;  // the site's index in its class (queue items carry it)
     int wq = 0;  // warp-uniform
     int y = T.ty;
 #pragma unroll 1
     for (int pass = 0; pass < X.npass_main;
-         ++pass, y += X.rpp, aC += 4u * rstep, aO += 4u * rstep, aJ += rstep, i_orig += istep) {
+         ++pass, y += X.rpp, aC += 4u * rstep, aO += 4u * rstep, aJ += rstep, i_orig += istep, lq += rstep) {
         const bool valid = T.active && y < G.Ly;
         uint32_t own = 0, D = 0, acc = 0, m8 = 0;
         if (valid) {
@@ -218,8 +233,7 @@ __device__ __forceinline__ void colour_phase(const Ctx &X, int c, const PlaneUni
         const int slot = wq + __popc(pm & lanemask_lt());
         wq += __popc(pm);
         if (need && slot < X.wlim) {
-            const uint32_t l = (aC - X.sS) / 4u - (uint32_t)(c * G.half);
-            Q4[X.wq0 + slot] = make_uint4(l | (i_orig << 16), D, acc, m8);
+            sts_u128(X.sQw + 16u * (uint32_t)slot, make_uint4(lq | (i_orig << 16), D, acc, m8));
         } else if (valid) {
             if (need)
                 finish_inline(i_orig, U, rkr, P, m8, D, acc);
@@ -256,7 +270,7 @@ __device__ __forceinline__ void colour_phase(const Ctx &X, int c, const PlaneUni
             const int slot = wq + __popc(pm & lanemask_lt());
             wq += __popc(pm);
             if (need && slot < X.wlim) {
-                Q4[X.wq0 + slot] = make_uint4(ll | (io << 16), D, acc, m8);
+                sts_u128(X.sQw + 16u * (uint32_t)slot, make_uint4(ll | (io << 16), D, acc, m8));
             } else if (valid) {
                 if (need)
                     finish_inline(io, U, rkr, P, m8, D, acc);
@@ -271,7 +285,7 @@ __device__ __forceinline__ void colour_phase(const Ctx &X, int c, const PlaneUni
         const int q = qb + X.lane;
         if (q >= nown)
             continue;
-        const uint4 item = Q4[X.wq0 + q];
+        const uint4 item = lds_u128(X.sQw + 16u * (uint32_t)q);
         const int l = (int)(item.x & 0xFFFFu);
         const uint32_t io = item.x >> 16;
         uint32_t D = item.y, acc = item.z;

@@ -85,7 +85,8 @@ struct GridBitsParams {
     int32_t n_groups;          // local word groups G
     uint32_t *xs_ctl;          // [1 + 2 C_local]: ticket, per-copy finished tasks, published rounds
     int64_t *xs_E;             // [G][32] energies of the group's last round
-    uint32_t *xs_B;            // [2][G][2][nbw] bit 0 / bit 31 planes of each site, by round parity
+    uint32_t *xs_S;            // [G][n] the groups' states between rounds, colour-separated order
+    uint32_t *xs_B;            // [2][G][2][nbw] bit 0 / bit 31 planes (colour-separated order), by round parity
     uint32_t *xs_M;            // [C_local][K/32] swap mask of the copy's last exchange
 };
 
@@ -206,7 +207,38 @@ struct IcmParams {
     RoundKeys rk;
 };
 
+// Results of the device CSR checks (k_create.cu): the lowest failing vertex of each check
+// (INT32_MAX = none) and the per-graph quantities the host path computed in its loops.
+struct CsrCheck {
+    int32_t bad_row;       // range, self-loop, duplicate, non-finite weight
+    int32_t bad_sym;       // (i, j, w) without (j, i, w)
+    int32_t bad_sum;       // integer weights: sum |w| at a vertex >= 2^30
+    int32_t bad_colrange;  // caller colouring out of [0, 2^16)
+    int32_t bad_proper;    // caller colouring not proper
+    int32_t maxdeg;
+    int32_t max_colour;
+    uint32_t pm1;          // integer weights all +-1
+    int64_t qmax;          // max per-vertex sum |w| (integer weights)
+    int64_t sum_abs;       // sum over entries of |w| (each edge twice)
+    int64_t W_int;         // sum of w over edges (each once)
+    uint64_t hash;         // fingerprint of row_ptr / col / w (checkpoints)
+};
+
 // ----------------------------------------------------------------- launchers
+cudaError_t launch_csr_check(int32_t n, const int64_t *rp, const int32_t *col, const int32_t *wi, const float *wf,
+                             const int32_t *colour, CsrCheck *out, uint8_t *colour_used, cudaStream_t st);
+cudaError_t colour_jp_device(int32_t n, const int64_t *rp, const int32_t *col, uint32_t *prio, int32_t *colour,
+                             int32_t *counters, int32_t *ncol_out, cudaStream_t st);
+cudaError_t build_order_device(int32_t n, int32_t ncol, const int32_t *colour, const int64_t *rp, uint32_t *orig,
+                               uint32_t *o2i, int32_t *class_off, int32_t *rpi, cudaStream_t st);
+cudaError_t launch_build_internal(int32_t n, const int64_t *rp, const int32_t *col, const uint32_t *w,
+                                  const uint32_t *orig, const uint32_t *o2i, const int32_t *rpi, int32_t *ci,
+                                  uint32_t *wo, int32_t *ell_col, uint32_t *ell_w, cudaStream_t st);
+cudaError_t launch_hash_order(int32_t n, const uint32_t *orig, unsigned long long *hash, cudaStream_t st);
+cudaError_t launch_extract_i8(const int8_t *s, int64_t R, int32_t n, int64_t rl, const uint32_t *o2i, int8_t *out,
+                              cudaStream_t st);
+cudaError_t launch_insert_i8(int8_t *s, int64_t R, int32_t n, int64_t rl, const uint32_t *o2i, const int8_t *in,
+                             cudaStream_t st);
 cudaError_t launch_icm_bits(const IcmParams &p, int32_t pairs, int32_t threads, cudaStream_t st);
 cudaError_t launch_init_bits(uint32_t *state, int32_t G, int32_t n, const uint32_t *orig,
                              uint32_t g0, const RoundKeys &rk, cudaStream_t st);

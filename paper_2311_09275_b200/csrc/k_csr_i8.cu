@@ -60,20 +60,23 @@ __device__ __forceinline__ uint64_t thr_x(float x)
     return __float2ull_rz(v);
 }
 
-// The fast decision estimates T / 2^48 = cexp32(x) 2^16 (x = -(beta dE) = (2 beta) s_i h) by
+// The fast decision estimates c = T / 2^48 = cexp32(x) 2^16 (x = -(beta dE) = (2 beta) s_i h) by
 //   e = ex2.approx(RN(bl * sh + 16)),   bl = RN((2 beta) * log2 e),   sh = s_i h,
-// one FFMA and one MUFU per attempt (bl is computed once per thread).  Relative to the
-// contract value c = cexp32(x) 2^16 the error has four sources: bl vs log2e * x / sh
-// (two roundings, <= 2^-23 relative in the exponent argument), the FFMA rounding of the
-// argument, ex2.approx, and cexp32 vs exp.  Wherever c >= 1/2 (x >= -11.8, argument
-// <= 17 in magnitude) they sum to < 2^-18.5; ising_debug_exp_bound checks it for every
-// float sh and the ladder's betas, together with e < 1 wherever c < 1/2.  With the 2^-16
-// margin (> twice the error bound):
-//   2^23 + hi16 <= RN(e (1 - 2^-16) + 2^23 - 2)  =>  hi16 + 1 <= T / 2^48  =>  accept
-//   2^23 + hi16 >= RN(e (1 + 2^-16) + 2^23 + 1)  =>  hi16 > T / 2^48      =>  reject
-// (the RN of a value near 2^23 is within 1/2, covered by the -2 / +1 slack; where c < 1/2
-// no hi16 is accepted and hi16 >= 2 is rejected, both correct for T < 2^47)
-// and anything else is decided exactly.
+// one FFMA and one MUFU per attempt (bl is computed once per thread).  Relative to c the
+// error has four sources: bl vs log2e * x / sh (two roundings, <= 2^-23 relative in the
+// exponent argument), the FFMA rounding of the argument, ex2.approx, and cexp32 vs exp.
+// Wherever c >= 1/2 (x >= -11.8, argument <= 17 in magnitude) they sum to < 2^-18.5;
+// ising_debug_exp_bound checks |e/c - 1| < 2^-17 for every float sh and the ladder's betas,
+// together with e < 1 wherever c < 1/2.  Since c <= 2^16, |e - c| <= 1/2 where c >= 1/2.
+// The decision compares d = RN(hf - e), hf = 2^23 + hi16 (|d - (hf - e)| <= 1/2, the result
+// lies in [2^22, 2^24)):
+//   d <= 2^23 - 2  =>  hi16 + 1 <= e - 1/2 <= c  =>  (hi16 + 1) 2^48 <= T  =>  U < T: accept
+//                      (c < 1/2: e < 1 makes it impossible, as it must be)
+//   d >= 2^23 + 1  =>  hi16 >= e + 1/2 >= c      =>  U >= hi16 2^48 >= T: reject
+//                      (c < 1/2: hi16 >= 1 > 2 c, and U >= 2^48 > T)
+// (T saturated at 2^64 - 1, c = 2^16: accept needs hi16 <= 65534, so U < T still holds);
+// anything in between (d in (2^23 - 2, 2^23 + 1), ~3 values of hi16 in 2^16) is decided
+// exactly from the contract threshold.
 constexpr float kLog2e = 0x1.715476p+0f;
 
 __device__ __forceinline__ float exp_est16(float bl, float sh)
@@ -83,7 +86,10 @@ __device__ __forceinline__ float exp_est16(float bl, float sh)
     return e;
 }
 
-constexpr float kLoMargin = 1.0f - 0x1p-16f, kHiMargin = 1.0f + 0x1p-16f;
+// d = RN(hf - e) of the fast decision; accepted if d <= 2^23 - 2, rejected if d >= 2^23 + 1
+__device__ __forceinline__ float fast_d(float hf, float e) { return __fsub_rn(hf, e); }
+__device__ __forceinline__ bool fast_accept(float d) { return d <= 0x1p23f - 2.0f; }
+__device__ __forceinline__ bool fast_reject(float d) { return d >= 0x1p23f + 1.0f; }
 
 // lo48 of replica r: Philox(i, t, r, WORD_LO<<24) words 0 and 1
 __device__ __forceinline__ uint64_t lo48_of(uint32_t io, uint32_t t, uint32_t r, const RoundKeys &rk)
@@ -226,8 +232,9 @@ __device__ __forceinline__ void float_decide(const CsrI8Params &p, int32_t v, co
                 const float e = exp_est16(b2[b], sh[b]);
                 const uint32_t hword = hw[2 * half + (b >> 1)];
                 const float hf = (b & 1) ? hi16_f<1>(hword) : hi16_f<0>(hword);  // 2^23 + hi16
-                const bool acc = sh[b] >= 0.0f || hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f);
-                const bool dec = acc || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f);
+                const float d = fast_d(hf, e);
+                const bool acc = sh[b] >= 0.0f || fast_accept(d);
+                const bool dec = acc || fast_reject(d);
                 fm |= acc ? (0xFEu << (8 * b)) : 0u;
                 und |= !dec;
             }
@@ -264,8 +271,8 @@ __device__ __forceinline__ void float_decide(const CsrI8Params &p, int32_t v, co
                 if (shb >= 0.0f)
                     continue;
                 const float e = exp_est16(__fmul_rn(b2v, kLog2e), shb);
-                const float hf = __uint_as_float(0x4B000000u | hb);
-                if (hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f) || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f))
+                const float d = fast_d(__uint_as_float(0x4B000000u | hb), e);
+                if (fast_accept(d) || fast_reject(d))
                     continue;  // decided by the fast path (same expressions)
                 if (exact_less(hb, thr_x(xv), io, p.t, 8u * g0 + (uint32_t)b, p.rk)) {
                     if (b < 4)
@@ -525,8 +532,9 @@ __device__ __forceinline__ void pipe_decide(const CsrI8Params &p, const I8Rows<D
             const float e = exp_est16(bl[4 * half + b], sh[b]);
             const uint32_t hword = hw[2 * half + (b >> 1)];
             const float hf = (b & 1) ? hi16_fr<1>(hword, c4b) : hi16_fr<0>(hword, c4b);  // 2^23 + hi16
-            const bool acc = sh[b] >= 0.0f || hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f);
-            const bool dec = acc || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f);
+            const float d = fast_d(hf, e);
+            const bool acc = sh[b] >= 0.0f || fast_accept(d);
+            const bool dec = acc || fast_reject(d);
             f |= acc ? (0xFEu << (8 * b)) : 0u;
             und |= !dec;
         }
@@ -551,8 +559,8 @@ __device__ __forceinline__ void pipe_decide(const CsrI8Params &p, const I8Rows<D
             const uint32_t hb = (b & 1) ? (hword >> 16) : (hword & 0xFFFFu);
             const float b2v = __ldg(p.betaf + 8u * o + (uint32_t)b);
             const float e = exp_est16(__fmul_rn(b2v, kLog2e), shb);
-            const float hf = __uint_as_float(0x4B000000u | hb);
-            if (hf <= __fmaf_rn(e, kLoMargin, 0x1p23f - 2.0f) || hf >= __fmaf_rn(e, kHiMargin, 0x1p23f + 1.0f))
+            const float d = fast_d(__uint_as_float(0x4B000000u | hb), e);
+            if (fast_accept(d) || fast_reject(d))
                 continue;  // decided by the fast path (same expressions)
             if (exact_less(hb, thr_x(__fmul_rn(b2v, shb)), m.io, p.t, 8u * g0 + (uint32_t)b, p.rk)) {
                 if (b < 4)  // scalar updates: a dynamically indexed fm[] would live in local memory

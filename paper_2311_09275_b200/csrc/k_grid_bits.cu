@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
     const bool pt = p.pt != 0;
     const int c_local = gl / KW;
     const uint32_t c_global = g / (uint32_t)KW;
-    const grid::Ctx X = grid::make_ctx(G, n, qcap, S, JB, SPILL);
+    const grid::Ctx X = grid::make_ctx(G, n, qcap, S, JB, Q4, SPILL);
 
     // ---- load: original order -> colour-separated order
     const uint32_t *src = p.state_in + (size_t)gl * n;
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bits(const GridBits
             }
 #pragma unroll 1
             for (int c = 0; c < 2; ++c)
-                grid::colour_phase<SPILL>(X, c, U, rkr, P, Q4);
+                grid::colour_phase<SPILL>(X, c, U, rkr, P);
         }
 
         // ---- energy of the 32 replicas: E = 2U - 2n

@@ -19,7 +19,8 @@
 // not touch the configurations: it publishes the copy's swap mask, and each group applies it
 // when it loads its state for the next round -- pairs inside a word by a delta swap, the pair
 // that crosses two words from the neighbouring group's boundary bit plane (bit 0 / bit 31 of
-// every site) saved at the end of the round (double-buffered by round parity).  After the
+// every site, in colour-separated order) saved at the end of the round (double-buffered by
+// round parity).  After the
 // last round the PT step applies the swaps to the stored states itself.  A task of round r
 // waits (acquire spin) until its copy's exchange r-1 is published; tickets are handed out in
 // order and every CTA is resident, so a wait is always on an earlier ticket that a running
@@ -47,6 +48,39 @@ __device__ __forceinline__ void st_release(uint32_t *a, uint32_t v)
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// TMA bulk copy global -> shared (bytes % 16 == 0, both 16-byte aligned), completing on mbar
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase)
+{
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                     " selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(mbar), "r"(phase) : "memory");
+}
+
+// TMA bulk copy shared -> global, waited for completion and ordered before later generic
+// accesses (fence.proxy.async) -- the CTA's release of the copy counter follows it
+__device__ __forceinline__ void bulk_store_wait(void *dst, uint32_t src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // The PT step of copy c_local after round `round` (all its K/32 groups stored).  Run by
 // every thread of the CTA that completed the copy's last task of the round.
 __device__ void copy_pt_step(PtShared &ps, const GridBitsParams &p, int round, int c_local, int Gl)
@@ -57,14 +91,18 @@ __device__ void copy_pt_step(PtShared &ps, const GridBitsParams &p, int round, i
     const uint32_t t_now = p.t0 + (uint32_t)((round + 1) * p.k_ex), e_now = p.e0 + (uint32_t)round;
     const int64_t *Eg = p.xs_E + (size_t)c_local * K;
     int64_t *Wg = p.walker + (size_t)c_local * K;
-    for (int k = tid; k < K; k += nt) {
+    int64_t *cb = p.copy_best + 3 * (size_t)c_local;
+    for (int k = tid; k < K; k += nt) {  // one round trip: energies, walkers, the copy's best
         ps.Ecopy[k] = __ldcg(Eg + k);
         ps.Wcopy[k] = __ldcg(Wg + k);
+    }
+    if (tid == 0) {
+        ps.bestE = __ldcg(cb);
+        ps.bestSlot = __ldcg(cb + 1);
     }
     for (int q = tid; q < KW; q += nt)
         ps.Mswap[q] = 0u;
     __syncthreads();
-    int64_t *cb = p.copy_best + 3 * (size_t)c_local;
     if (warp == 0) {  // best-so-far of the copy: argmin, ties -> lowest slot; strict improvement
         int64_t bE = INT64_MAX;
         int bk = -1;
@@ -82,8 +120,7 @@ __device__ void copy_pt_step(PtShared &ps, const GridBitsParams &p, int round, i
             }
         }
         if (lane == 0) {
-            const int64_t oldE = __ldcg(cb), oldSlot = __ldcg(cb + 1);
-            const bool imp = oldSlot < 0 || bE < oldE;
+            const bool imp = ps.bestSlot < 0 || bE < ps.bestE;
             ps.improve = imp;
             ps.kmin = bk;
             if (imp) {
@@ -95,11 +132,16 @@ __device__ void copy_pt_step(PtShared &ps, const GridBitsParams &p, int round, i
     }
     __syncthreads();
     if (ps.improve) {  // snapshot of the configuration (stored this round, before the swap)
-        const uint32_t *src = p.state_out + (size_t)(c_local * KW + (ps.kmin >> 5)) * n;
-        const int bit = ps.kmin & 31;
+        const int gk = c_local * KW + (ps.kmin >> 5), bit = ps.kmin & 31;
         int8_t *dst = p.snap + (size_t)c_local * n;
-        for (int i = tid; i < n; i += nt)
-            dst[i] = ((__ldcg(src + i) >> bit) & 1u) ? -1 : 1;
+        const bool last = round + 1 == p.n_rounds;  // the last round stores original order
+        const uint32_t *src = (last ? p.state_out : p.xs_S) + (size_t)gk * n;
+        for (int y = warp; y < p.Ly; y += nt / 32)
+            for (int x = lane; x < p.Lx; x += 32) {
+                const int i = y * p.Lx + x;
+                const int l = last ? i : ((x + y) & 1) * p.half + y * p.hx + (x >> 1);
+                dst[i] = ((__ldcg(src + l) >> bit) & 1u) ? -1 : 1;
+            }
     }
     const int par = (int)(e_now & 1u);
     const int npairs = (K - par) / 2;
@@ -109,10 +151,10 @@ __device__ void copy_pt_step(PtShared &ps, const GridBitsParams &p, int round, i
         bool accept = d >= 0;
         if (!accept) {
             const int64_t j = -d - 1;
-            if (j < p.Tx_len[k]) {
+            if (j < __ldg(p.Tx_len + k)) {
                 const uint4 w = philox((uint32_t)k, e_now, c_global, ST_EXCH << 24, p.rk);
                 const uint64_t Ux = ((uint64_t)w.x << 32) | (uint64_t)w.y;
-                accept = Ux < p.Tx[p.Tx_off[k] + j];
+                accept = Ux < __ldg(p.Tx + __ldg(p.Tx_off + k) + j);
             }
         }
         if (accept) {
@@ -168,6 +210,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_sched(const GridBit
     __shared__ int32_t Ucnt[32];
     __shared__ PtShared ps;
     __shared__ int32_t s_task, s_last;
+    __shared__ __align__(8) uint64_t mbar;
     const int n = p.n;
     const GridGeom G{p.Lx, p.Ly, p.hx, p.half, p.ymagic};
     uint32_t *S = sm;
@@ -180,57 +223,76 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_sched(const GridBit
     const int C_local = Gl / KW;
     const int32_t ntask = Gl * p.n_rounds;  // host guarantees < 2^31
     const int nbw = (n + 31) / 32;
+    const uint32_t bytes = 4u * (uint32_t)n;  // n % 4 == 0 (even tori): whole 16-byte units
     uint32_t *ticket = p.xs_ctl, *cnt = p.xs_ctl + 1, *ready = p.xs_ctl + 1 + C_local;
 
     RoundKeys rkr;
 #pragma unroll
     for (int r = 0; r < 20; ++r)
         rkr.k[r] = p.rk.k[r];
-    const grid::Ctx X = grid::make_ctx(G, n, p.qcap, S, JB, SPILL);
+    const grid::Ctx X = grid::make_ctx(G, n, p.qcap, S, JB, Q4, SPILL);
     for (int l = tid; l < n; l += nt)  // the couplings are the same for every task
         JB[l] = p.jbyte[l];
+    const uint32_t mb = smem_u32(&mbar), sS = smem_u32(S);
+    uint32_t phase = 0;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_task = (int32_t)atomicAdd(ticket, 1u);
+    }
+    __syncthreads();
 
     for (;;) {
-        if (tid == 0)
-            s_task = (int32_t)atomicAdd(ticket, 1u);
-        __syncthreads();
         const int32_t task = s_task;
+        __syncthreads();  // every thread has read s_task before thread 0 overwrites it
         if (task >= ntask)
             break;
+        uint32_t next = 0;  // the next ticket, fetched while this task runs (thread 0)
+        if (tid == 0)
+            next = atomicAdd(ticket, 1u);
         const int round = task / Gl, gl = task - round * Gl;
+        const bool last = round + 1 == p.n_rounds;
         const uint32_t g = p.g0 + (uint32_t)gl;
         const int wt = (int)(g % (uint32_t)KW);
         const int c_local = gl / KW;
-        if (round > 0) {  // the copy's exchange of the previous round must be published
-            if (tid == 0)
+        uint32_t *scratch = p.xs_S + (size_t)gl * n;  // colour-separated state between rounds
+        if (round == 0) {
+            // ---- first round: the launch's input, original order -> colour-separated
+            const uint32_t *src = p.state_in + (size_t)gl * n;
+            for (int y = X.warp; y < G.Ly; y += X.nwarps)
+                for (int x = X.lane; x < G.Lx; x += 32)
+                    S[((x + y) & 1) * G.half + y * G.hx + (x >> 1)] = __ldcg(src + y * G.Lx + x);
+        } else {
+            // ---- the copy's exchange of the previous round must be published; then one TMA
+            // bulk copy of the stored state straight into S and the pending swaps applied in place
+            if (tid == 0) {
                 while (ld_acquire(ready + c_local) < (uint32_t)round)
                     __nanosleep(256);
-            __syncthreads();
-        }
-        // ---- load (original order -> colour-separated), applying the copy's pending swaps
-        const uint32_t *src = (round == 0 ? p.state_in : p.state_out) + (size_t)gl * n;
-        uint32_t Min = 0u;
-        bool clo = false, chi = false;
-        const uint32_t *nB31 = nullptr, *nB0 = nullptr;
-        if (round > 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired data -> async proxy
+                bulk_load(sS, scratch, bytes, mb);
+            }
             const uint32_t *M = p.xs_M + (size_t)c_local * KW;
             const uint32_t Mw = __ldcg(M + wt);
-            Min = Mw & 0x7FFFFFFFu;
-            clo = wt > 0 && ((__ldcg(M + wt - 1) >> 31) & 1u);
-            chi = wt + 1 < KW && ((Mw >> 31) & 1u);
+            const uint32_t Min = Mw & 0x7FFFFFFFu;
+            const bool clo = wt > 0 && ((__ldcg(M + wt - 1) >> 31) & 1u);
+            const bool chi = wt + 1 < KW && ((Mw >> 31) & 1u);
             const uint32_t *Bp = p.xs_B + (size_t)((round - 1) & 1) * Gl * 2 * nbw;
-            nB31 = Bp + ((size_t)(gl - 1) * 2 + 1) * nbw;  // used only if clo (wt > 0)
-            nB0 = Bp + (size_t)(gl + 1) * 2 * nbw;         // used only if chi (wt < KW - 1)
-        }
-        for (int i = tid; i < n; i += nt) {
-            uint32_t w = __ldcg(src + i);
-            const uint32_t tt = (w ^ (w >> 1)) & Min;
-            w ^= tt ^ (tt << 1);
-            if (clo)
-                w = (w & ~1u) | ((__ldcg(nB31 + (i >> 5)) >> (i & 31)) & 1u);
-            if (chi)
-                w = (w & 0x7FFFFFFFu) | (((__ldcg(nB0 + (i >> 5)) >> (i & 31)) & 1u) << 31);
-            S[grid::colsep(G, i)] = w;
+            const uint32_t *nB31 = Bp + ((size_t)(gl - 1) * 2 + 1) * nbw;  // used only if clo (wt > 0)
+            const uint32_t *nB0 = Bp + (size_t)(gl + 1) * 2 * nbw;         // used only if chi (wt < KW - 1)
+            mbar_wait(mb, phase);
+            phase ^= 1u;
+            if (Min | clo | chi) {
+                for (int l = tid; l < n; l += nt) {
+                    uint32_t w = S[l];
+                    const uint32_t tt = (w ^ (w >> 1)) & Min;
+                    w ^= tt ^ (tt << 1);
+                    if (clo)
+                        w = (w & ~1u) | ((__ldcg(nB31 + (l >> 5)) >> (l & 31)) & 1u);
+                    if (chi)
+                        w = (w & 0x7FFFFFFFu) | (((__ldcg(nB0 + (l >> 5)) >> (l & 31)) & 1u) << 31);
+                    S[l] = w;
+                }
+            }
         }
         for (int j = tid; j < 128; j += nt)
             P[j] = __ldg(p.planes + wt * 128 + j);
@@ -243,32 +305,43 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_sched(const GridBit
             const PlaneUniform U = plane_uniform(g, t, rkr);
 #pragma unroll 1
             for (int c = 0; c < 2; ++c)
-                grid::colour_phase<SPILL>(X, c, U, rkr, P, Q4);
+                grid::colour_phase<SPILL>(X, c, U, rkr, P);
         }
         atomicAdd(&Ucnt[X.lane], grid::unsat_counts(X, S, JB));
-        // ---- store + this round's boundary bit planes (parity round & 1)
-        uint32_t *dst = p.state_out + (size_t)gl * n;
-        uint32_t *Bo = p.xs_B + ((size_t)(round & 1) * Gl + gl) * 2 * nbw;
-        for (int b = X.warp * 32; b < nbw * 32; b += nt) {
-            const int i = b + X.lane;
-            const uint32_t w = i < n ? S[grid::colsep(G, i)] : 0u;
-            if (i < n)
-                dst[i] = w;
-            const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, w & 1u);
-            const uint32_t b31 = __ballot_sync(0xFFFFFFFFu, w >> 31);
-            if (X.lane == 0) {
-                Bo[b >> 5] = b0;
-                Bo[nbw + (b >> 5)] = b31;
+        if (last) {
+            // ---- the launch's output, original order (the PT step applies the last swaps there)
+            uint32_t *dst = p.state_out + (size_t)gl * n;
+            for (int y = X.warp; y < G.Ly; y += X.nwarps)
+                for (int x = X.lane; x < G.Lx; x += 32)
+                    dst[y * G.Lx + x] = S[((x + y) & 1) * G.half + y * G.hx + (x >> 1)];
+        } else {
+            // ---- this round's boundary bit planes (parity round & 1), then one bulk store of S
+            uint32_t *Bo = p.xs_B + ((size_t)(round & 1) * Gl + gl) * 2 * nbw;
+            for (int b = X.warp * 32; b < nbw * 32; b += nt) {
+                const int l = b + X.lane;
+                const uint32_t w = l < n ? S[l] : 0u;
+                const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, w & 1u);
+                const uint32_t b31 = __ballot_sync(0xFFFFFFFFu, w >> 31);
+                if (X.lane == 0) {
+                    Bo[b >> 5] = b0;
+                    Bo[nbw + (b >> 5)] = b31;
+                }
             }
         }
-        __syncthreads();  // Ucnt complete
+        // every thread's generic accesses of S are ordered before the async proxy's (the bulk
+        // store below reads S, the next task's bulk load overwrites it)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();  // Ucnt complete; S final
         if (tid < 32)
             p.xs_E[(size_t)gl * 32 + tid] = 2 * (int64_t)Ucnt[tid] - 2 * (int64_t)n;
+        if (tid == 0 && !last)
+            bulk_store_wait(scratch, sS, bytes);
         __threadfence();
         __syncthreads();
         if (tid == 0) {
             const uint32_t done = atomicAdd(cnt + c_local, 1u) + 1u;
             s_last = done == (uint32_t)KW * (uint32_t)(round + 1);
+            s_task = (int32_t)next;
         }
         __syncthreads();
         if (s_last) {  // this CTA completed the copy's round: its PT step

@@ -26,7 +26,8 @@ from . import ising as L
 class Engine:
     """One libising handle.  inst: dict from synth.make_instance (grid or csr).  colour (csr):
     None = the library's ascending-id greedy colouring, "sl" = smallest-last greedy
-    (ising_greedy_colour_sl), or an explicit int32 array (validated by the library)."""
+    (ising_greedy_colour_sl, host), "jp" = greedy in Jones-Plassmann priority order (computed
+    by the library on the GPU), or an explicit int32 array (validated by the library)."""
 
     def __init__(self, inst: dict, K: int, C: int, betas, seed: int, copy_begin: int = 0,
                  copy_end: int | None = None, layout: str = "bits", device: int = 0,
@@ -37,10 +38,14 @@ class Engine:
         if inst["kind"] == "grid":
             self.h = L.ising_create_grid(inst["Lx"], inst["Ly"], inst["J_right"], inst["J_down"], **kw)
         else:
-            if isinstance(colour, str):  # "sl": the library's smallest-last greedy colouring
-                if colour != "sl":
+            if isinstance(colour, str):
+                if colour == "sl":  # the library's smallest-last greedy colouring (host)
+                    colour, _ = L.ising_greedy_colour_sl(inst["n"], inst["row_ptr"], inst["col"])
+                elif colour == "jp":  # greedy in Jones-Plassmann order, computed on the GPU in create
+                    kw["colouring"] = L.ISING_COLOUR_JP
+                    colour = None
+                else:
                     raise ValueError(f"unknown colouring {colour!r}")
-                colour, _ = L.ising_greedy_colour_sl(inst["n"], inst["row_ptr"], inst["col"])
             self.h = L.ising_create_csr(inst["n"], inst["row_ptr"], inst["col"], inst["w"],
                                         colour=colour, **kw)
         self.info = L.ising_info(self.h)

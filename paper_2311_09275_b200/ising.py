@@ -18,6 +18,7 @@ ISING_E_CUDA, ISING_E_OOM, ISING_E_STATE = -4, -5, -6
 ISING_W_I32, ISING_W_F32 = 0, 1
 ISING_SPINS_BITS, ISING_SPINS_I8 = 0, 1
 ISING_RNG_PLANE, ISING_RNG_WORD = 0, 1
+ISING_COLOUR_GREEDY, ISING_COLOUR_JP = 0, 1
 
 LAYOUTS = {"bits": ISING_SPINS_BITS, "i8": ISING_SPINS_I8}
 
@@ -25,7 +26,7 @@ EXPORTED = [
     "ising_create_grid", "ising_create_csr", "ising_sweep", "ising_run", "ising_anneal", "ising_energy", "ising_cut",
     "ising_exchange", "ising_icm", "ising_exchange_begin", "ising_exchange_end", "ising_check_best",
     "ising_best", "ising_merge_best", "ising_copy_best", "ising_get_spins", "ising_set_spins", "ising_get_walkers", "ising_info",
-    "ising_sync", "ising_last_error", "ising_destroy", "ising_greedy_colour", "ising_greedy_colour_sl", "ising_threshold",
+    "ising_sync", "ising_last_error", "ising_destroy", "ising_greedy_colour", "ising_greedy_colour_sl", "ising_colour_jp", "ising_threshold",
     "ising_version", "ising_debug_philox", "ising_debug_exp_bound",
     "ising_state_size", "ising_state_save", "ising_state_load",
 ]
@@ -41,7 +42,7 @@ class RunDesc(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("n_temps", C.c_int32), ("n_copies", C.c_int32),
                 ("copy_begin", C.c_int32), ("copy_end", C.c_int32), ("betas", C.c_void_p),
                 ("layout", C.c_int32), ("rng", C.c_int32), ("device", C.c_int32),
-                ("block_threads", C.c_int32), ("stream", C.c_void_p)]
+                ("block_threads", C.c_int32), ("stream", C.c_void_p), ("colouring", C.c_int32)]
 
 
 class Record(C.Structure):
@@ -100,6 +101,7 @@ def lib(build_if_missing: bool = True):
         "ising_destroy": ([vp], None),
         "ising_greedy_colour": ([i32, vp, vp, vp], C.c_int),
         "ising_greedy_colour_sl": ([i32, vp, vp, vp], C.c_int),
+        "ising_colour_jp": ([i32, i32, vp, vp, vp], C.c_int),
         "ising_threshold": ([C.c_double, i64], C.c_uint64),
         "ising_version": ([], C.c_char_p),
         "ising_debug_philox": ([i32, vp, i32, vp, vp], C.c_int),
@@ -137,14 +139,15 @@ def _current_stream(stream, device=0):
 
 
 def _desc(seed, n_temps, n_copies, betas, copy_begin=0, copy_end=None, layout="bits", device=0,
-          block_threads=0, stream=None):
+          block_threads=0, stream=None, colouring=ISING_COLOUR_GREEDY):
     betas = np.ascontiguousarray(betas, np.float64)
     lay = LAYOUTS[layout] if isinstance(layout, str) else int(layout)
     d = RunDesc(seed=seed & (2**64 - 1), n_temps=n_temps, n_copies=n_copies,
                 copy_begin=copy_begin, copy_end=n_copies if copy_end is None else copy_end,
                 betas=betas.ctypes.data, layout=lay,
                 rng=ISING_RNG_PLANE if lay == ISING_SPINS_BITS else ISING_RNG_WORD,
-                device=device, block_threads=block_threads, stream=_current_stream(stream, device))
+                device=device, block_threads=block_threads, stream=_current_stream(stream, device),
+                colouring=colouring)
     return d, betas
 
 
@@ -332,6 +335,18 @@ def ising_greedy_colour_sl(n, row_ptr, col):
     cc = np.ascontiguousarray(col, np.int32)
     out = np.zeros(n, np.int32)
     rc = lib().ising_greedy_colour_sl(int(n), _ptr(rp), _ptr(cc), _ptr(out))
+    if rc < 0:
+        _check(rc)
+    return out, rc
+
+
+def ising_colour_jp(n, row_ptr, col, device: int = 0):
+    """Greedy colouring in Jones-Plassmann priority order, computed on the GPU (include/ising.h);
+    returns (colour, n_colours)."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cc = np.ascontiguousarray(col, np.int32)
+    out = np.zeros(n, np.int32)
+    rc = lib().ising_colour_jp(int(device), int(n), _ptr(rp), _ptr(cc), _ptr(out))
     if rc < 0:
         _check(rc)
     return out, rc

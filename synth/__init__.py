@@ -196,7 +196,7 @@ CONFIGS = {
                 layout="bits"),
     # configs[4]: random 3-regular 4e6 vertices, N(0,1) f32, 256 replicas/GPU, 1000 sweeps
     "c5": dict(kind="regular", n=4_000_000, d=3, seed=3, K=256, C=1, sweeps=1000, k_ex=0,
-               layout="i8", colouring="sl"),
+               layout="i8", colouring="jp"),
 }
 
 

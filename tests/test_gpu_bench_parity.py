@@ -133,7 +133,8 @@ def test_c5_full_size_eight_replicas_50_sweeps():
     sweeps = 50
     eng.sweep(sweeps)
     E = eng.energies()
-    col, _ = oracle.greedy_colour_sl(inst["n"], inst["row_ptr"], inst["col"])
+    col, _ = (oracle.greedy_colour_jp if cfg["colouring"] == "jp" else oracle.greedy_colour_sl)(
+        inst["n"], inst["row_ptr"], inst["col"])
     slots = (0, 37, 64, 101, 128, 170, 211, 255)
     res = {}
 

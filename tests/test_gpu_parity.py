@@ -246,7 +246,8 @@ def test_c3_full_size_sampled_copies():
     eng = Engine(inst, cfg["K"], cfg["C"], betas, seed=KEY, layout="bits", colour=cfg["colouring"])
     assert eng.info.n_colours == 3  # smallest-last greedy on G(1e4, 9999)
     run_pt(eng, 20, 10, fused=True)
-    col, _ = oracle.greedy_colour_sl(inst["n"], inst["row_ptr"], inst["col"])
+    col, _ = (oracle.greedy_colour_jp if cfg["colouring"] == "jp" else oracle.greedy_colour_sl)(
+        inst["n"], inst["row_ptr"], inst["col"])
     for c0 in (0, 50):
         o = oracle.Oracle(inst, cfg["K"], betas, KEY, c0, c0 + 1, rng=oracle.RNG_PLANE, colour=col).run(20, 10)
         compare_copies(eng, o, check_best=False)
@@ -335,7 +336,8 @@ def test_float_int8_parity_small():
     (2000, 4, 10, 64, 8, 8),      # R = 512: two slices, DEG 4 with pads (every 10th edge dropped)
     (38, 3, 0, 16, 16, 20),       # fewer vertices per class than warps: 1-vertex chunks
 ])
-def test_float_int8_ring_parity(n, d, drop, K, C, sweeps):
+@pytest.mark.parametrize("colouring", ["sl", "jp"])
+def test_float_int8_ring_parity(n, d, drop, K, C, sweeps, colouring):
     """cp.async ring kernel (float weights, padded table, R % 256 == 0): identical spins and
     energies within 1e-5 relative of the oracle, over ragged chunks and table widths."""
     u, v = synth.random_regular(n, d, 40 + n)
@@ -346,9 +348,9 @@ def test_float_int8_ring_parity(n, d, drop, K, C, sweeps):
     rp, col, ww = synth.edges_to_csr(n, u, v, w)
     inst = dict(kind="csr", n=n, row_ptr=rp, col=col, w=ww.astype(np.float32))
     betas = synth.beta_ladder(K)
-    eng = Engine(inst, K, C, betas, seed=KEY, layout="i8", colour="sl")
+    eng = Engine(inst, K, C, betas, seed=KEY, layout="i8", colour=colouring)
     run_pt(eng, sweeps, 0)
-    colour, _ = oracle.greedy_colour_sl(n, rp, col)
+    colour, _ = (oracle.greedy_colour_jp if colouring == "jp" else oracle.greedy_colour_sl)(n, rp, col)
     o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=oracle.RNG_WORD, colour=colour).run(sweeps, 0)
     for r in range(o.R):
         assert np.array_equal(eng.spins(r), o.s[r]), f"slot {r}"
@@ -364,7 +366,8 @@ def test_c5_full_size_sampled_replicas():
     sweeps = 4
     eng.sweep(sweeps)
     E = eng.energies()
-    col, _ = oracle.greedy_colour_sl(inst["n"], inst["row_ptr"], inst["col"])
+    col, _ = (oracle.greedy_colour_jp if cfg["colouring"] == "jp" else oracle.greedy_colour_sl)(
+        inst["n"], inst["row_ptr"], inst["col"])
     for lo in (0, 255):
         o = oracle.Oracle(inst, cfg["K"], betas, KEY, 0, 1, rng=oracle.RNG_WORD, colour=col,
                           slots=(lo, lo + 1))

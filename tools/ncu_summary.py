@@ -1,5 +1,6 @@
 """Per-kernel key metrics of an ncu report (raw page): python tools/ncu_summary.py <rep>"""
 import csv, subprocess, sys
+csv.field_size_limit(1 << 30)
 rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-metric-instances", "details"], capture_output=True, text=True).stdout
 r = list(csv.reader(out.splitlines()))
