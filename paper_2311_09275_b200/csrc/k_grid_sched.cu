@@ -271,6 +271,11 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_sched(const GridBit
                 asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired data -> async proxy
                 bulk_load(sS, scratch, bytes, mb);
             }
+            // the barrier's completion follows thread 0's acquire of `ready` (its arrive releases
+            // at CTA scope, the wait acquires): the copy's swap mask and the neighbours' boundary
+            // planes are read only after it
+            mbar_wait(mb, phase);
+            phase ^= 1u;
             const uint32_t *M = p.xs_M + (size_t)c_local * KW;
             const uint32_t Mw = __ldcg(M + wt);
             const uint32_t Min = Mw & 0x7FFFFFFFu;
@@ -279,8 +284,6 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_sched(const GridBit
             const uint32_t *Bp = p.xs_B + (size_t)((round - 1) & 1) * Gl * 2 * nbw;
             const uint32_t *nB31 = Bp + ((size_t)(gl - 1) * 2 + 1) * nbw;  // used only if clo (wt > 0)
             const uint32_t *nB0 = Bp + (size_t)(gl + 1) * 2 * nbw;         // used only if chi (wt < KW - 1)
-            mbar_wait(mb, phase);
-            phase ^= 1u;
             if (Min | clo | chi) {
                 for (int l = tid; l < n; l += nt) {
                     uint32_t w = S[l];
