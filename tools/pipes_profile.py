@@ -48,6 +48,9 @@ def plan(w):
     if w == "c4b:share16":
         return (["--workload", "c4b", "--copies", "16", "--sweeps", str(SWEEPS)] + base, "k_grid_bands", 1,
                 n * cfg["K"] * 16 * SWEEPS)
+    if w in ("c4b:full", "c4a:full"):  # the bench's own launch: the whole 50,000-sweep schedule
+        ww = w.split(":")[0]
+        return (["--workload", ww] + base, "k_grid_sched", 0, n * cfg["K"] * cfg["C"] * cfg["sweeps"])
     if w == "c4b:clusters":  # the cluster launch the persistent one replaced (ISING_GRID_SCHED=0)
         return (["--workload", "c4b", "--sweeps", str(SWEEPS)] + base, "k_grid_bits", 1,
                 n * cfg["K"] * cfg["C"] * SWEEPS)
@@ -96,10 +99,12 @@ def run(w):
 def merge():
     path = os.path.join(ROOT, "profiles", "inst_per_attempt.json")
     db = json.load(open(path))
-    for f in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "pipes_*.json"))):
+    # the bench's full launch (":full") wins over a short profiled launch of the same kernel
+    files = sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "pipes_*.json")), key=lambda f: "_full" in f)
+    for f in files:
         d = json.load(open(f))
         key = {"c4b:share16": "c4b_bands", "c4b": "c4b_sched", "c4a": "c4a_sched",
-               "c4b:clusters": "c4b"}.get(d["workload"], d["workload"])
+               "c4b:clusters": "c4b", "c4b:full": "c4b_sched", "c4a:full": "c4a_sched"}.get(d["workload"], d["workload"])
         e = db.setdefault(key, {})
         e.update({"kernel": d["kernel"], "layout": "bits" if d["kernel"] != "k_i8_cluster" else "i8",
                   "warp_inst_per_attempt": d["warp_inst_per_attempt"],
@@ -108,7 +113,7 @@ def merge():
                   "issue_active_pct": d["ncu"].get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                   "alu_pipe_pct": d["ncu"].get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
                   "fmaheavy_pipe_pct": d["ncu"].get("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active"),
-                  "pipes_source": f"profiles/{os.path.basename(f)} (ncu --metrics, one launch of "
+                  "pipes_source": f"profiles/r02/{os.path.basename(f)} (ncu --metrics, one launch of "
                                   f"{d['attempts_per_launch']:.4g} attempts: {d['command']})"})
     with open(path, "w") as f:
         json.dump(db, f, indent=1)
