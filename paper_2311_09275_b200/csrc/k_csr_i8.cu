@@ -74,7 +74,10 @@ __device__ __forceinline__ uint64_t thr_x(float x)
 //                      (c < 1/2: e < 1 makes it impossible, as it must be)
 //   d >= 2^23 + 1  =>  hi16 >= e + 1/2 >= c      =>  U >= hi16 2^48 >= T: reject
 //                      (c < 1/2: hi16 >= 1 > 2 c, and U >= 2^48 > T)
-// (T saturated at 2^64 - 1, c = 2^16: accept needs hi16 <= 65534, so U < T still holds);
+// (T saturated at 2^64 - 1, c = 2^16: accept needs hi16 <= 65534, so U < T still holds).
+// s h >= 0 (dE <= 0, always flips) needs no test of its own: the argument is >= 16, so
+// e >= 2^16 (1 - 2^-22) and d <= 2^23 - 1 + 2^-6: never rejected, accepted unless hi16 = 65535
+// near s h = 0, which the undecided path flips;
 // anything in between (d in (2^23 - 2, 2^23 + 1), ~3 values of hi16 in 2^16) is decided
 // exactly from the contract threshold.
 constexpr float kLog2e = 0x1.715476p+0f;
@@ -233,7 +236,7 @@ __device__ __forceinline__ void float_decide(const CsrI8Params &p, int32_t v, co
                 const uint32_t hword = hw[2 * half + (b >> 1)];
                 const float hf = (b & 1) ? hi16_f<1>(hword) : hi16_f<0>(hword);  // 2^23 + hi16
                 const float d = fast_d(hf, e);
-                const bool acc = sh[b] >= 0.0f || fast_accept(d);
+                const bool acc = fast_accept(d);  // s h >= 0: e >= 2^16, accepted here or left undecided
                 const bool dec = acc || fast_reject(d);
                 fm |= acc ? (0xFEu << (8 * b)) : 0u;
                 und |= !dec;
@@ -268,8 +271,13 @@ __device__ __forceinline__ void float_decide(const CsrI8Params &p, int32_t v, co
                 const float xv = __fmul_rn(b2v, shb);  // x = -(beta dE), the contract's product
                 const uint32_t hword = (b >> 1) == 0 ? hw[0] : (b >> 1) == 1 ? hw[1] : (b >> 1) == 2 ? hw[2] : hw[3];
                 const uint32_t hb = (b & 1) ? (hword >> 16) : (hword & 0xFFFFu);
-                if (shb >= 0.0f)
+                if (shb >= 0.0f) {  // dE <= 0 always flips
+                    if (b < 4)
+                        fm0 |= 0xFEu << (8 * (b & 3));
+                    else
+                        fm1 |= 0xFEu << (8 * (b & 3));
                     continue;
+                }
                 const float e = exp_est16(__fmul_rn(b2v, kLog2e), shb);
                 const float d = fast_d(__uint_as_float(0x4B000000u | hb), e);
                 if (fast_accept(d) || fast_reject(d))
@@ -533,7 +541,7 @@ __device__ __forceinline__ void pipe_decide(const CsrI8Params &p, const I8Rows<D
             const uint32_t hword = hw[2 * half + (b >> 1)];
             const float hf = (b & 1) ? hi16_fr<1>(hword, c4b) : hi16_fr<0>(hword, c4b);  // 2^23 + hi16
             const float d = fast_d(hf, e);
-            const bool acc = sh[b] >= 0.0f || fast_accept(d);
+            const bool acc = fast_accept(d);  // s h >= 0: e >= 2^16, accepted here or left undecided
             const bool dec = acc || fast_reject(d);
             f |= acc ? (0xFEu << (8 * b)) : 0u;
             und |= !dec;
@@ -553,8 +561,13 @@ __device__ __forceinline__ void pipe_decide(const CsrI8Params &p, const I8Rows<D
                 const int bb = b & 3;
                 shb = bb == 0 ? s4[0] : bb == 1 ? s4[1] : bb == 2 ? s4[2] : s4[3];
             }
-            if (shb >= 0.0f)
+            if (shb >= 0.0f) {  // dE <= 0 always flips (left undecided only when s h ~ +0)
+                if (b < 4)
+                    fm[0] |= 0xFEu << (8 * (b & 3));
+                else
+                    fm[1] |= 0xFEu << (8 * (b & 3));
                 continue;
+            }
             const uint32_t hword = (b >> 1) == 0 ? hw[0] : (b >> 1) == 1 ? hw[1] : (b >> 1) == 2 ? hw[2] : hw[3];
             const uint32_t hb = (b & 1) ? (hword >> 16) : (hword & 0xFFFFu);
             const float b2v = __ldg(p.betaf + 8u * o + (uint32_t)b);
