@@ -63,6 +63,7 @@ struct Ctx {
     int wq0;          // this warp's queue region
     int rpp;          // class rows per pass (even when possible)
     int npass;        // passes of the full mapping
+    int y0, y1;       // the thread block's rows [y0, y1) (a band of the lattice, or all of it)
     int main_rows;    // rows covered by the full passes
     int idle_w0;      // first warp with no column thread
     int spill_sites;  // leftover-row sites taken by the column-less warps
@@ -75,12 +76,19 @@ struct Ctx {
     uint32_t sQw;     // shared address of this warp's tail-queue region
 };
 
+// y0, y1: the rows this thread block updates (band split: one band of the lattice; the rows
+// outside it are kept current by the other band).  limit_stage2: cap the per-warp stage-2 queue
+// (the band kernel measured faster without the cap).
 __device__ __forceinline__ Ctx make_ctx(const GridGeom &G, int n, int qcap, const uint32_t *S, const uint8_t *JB,
-                                        const uint4 *Q4, bool SPILL)
+                                        const uint4 *Q4, bool SPILL, int y0 = 0, int y1 = -1,
+                                        bool limit_stage2 = true)
 {
     Ctx X;
     X.G = G;
     X.n = n;
+    X.y0 = y0;
+    X.y1 = y1 < 0 ? G.Ly : y1;
+    const int nrows = X.y1 - X.y0;
     X.tid = threadIdx.x;
     X.nt = blockDim.x;
     X.lane = X.tid & 31;
@@ -89,13 +97,13 @@ __device__ __forceinline__ Ctx make_ctx(const GridGeom &G, int n, int qcap, cons
     const int wcap = qcap / X.nwarps;
     X.wq0 = X.warp * wcap;
     X.rpp = grid_rows_per_pass(X.nt, G.hx);  // even when possible (host guarantees >= 1)
-    X.npass = (G.Ly + X.rpp - 1) / X.rpp;
+    X.npass = (nrows + X.rpp - 1) / X.rpp;
     // leftover rows beyond the last full pass go to the warps without a class column when
     // they can finish them within the full passes
-    const int full_passes = G.Ly / X.rpp;
-    X.main_rows = full_passes * X.rpp;
+    const int full_passes = nrows / X.rpp;
+    X.main_rows = X.y0 + full_passes * X.rpp;
     X.idle_w0 = (X.rpp * G.hx + 31) / 32;
-    X.spill_sites = (G.Ly - X.main_rows) * G.hx;
+    X.spill_sites = (X.y1 - X.main_rows) * G.hx;
     const int nidle_all = (X.nwarps - X.idle_w0) * 32;
     X.spill_iters = nidle_all > 0 ? (X.spill_sites + nidle_all - 1) / nidle_all : 0;
     X.spill = SPILL && X.spill_sites > 0 && nidle_all > 0 && X.spill_iters <= full_passes;
@@ -103,7 +111,7 @@ __device__ __forceinline__ Ctx make_ctx(const GridGeom &G, int n, int qcap, cons
     // per-warp stage-2 limit: about one 32-lane round of queued words per 8 passes (~11% of the
     // words stay undecided after stage 1); beyond it a word is finished inline in stage 1, so a
     // warp rarely pays a second, mostly empty stage-2 round after the others are done
-    X.wlim = min(wcap, 32 * max(1, (X.npass_main + 7) / 8));
+    X.wlim = limit_stage2 ? min(wcap, 32 * max(1, (X.npass_main + 7) / 8)) : wcap;
     {
         const int m = X.tid % G.hx;
         X.offR1 = m + 1 == G.hx ? 1 - G.hx : 1;
@@ -154,15 +162,15 @@ __device__ __forceinline__ void site_unsat(const uint32_t *S, const uint8_t *JB,
 
 // The update of one site word: unsatisfied-bond classes, then planes 0..7 (both Philox calls
 // issued together: two independent chains).  Returns with D = still undecided lanes.
-__device__ __forceinline__ void stage1_site(const Ctx &X, uint32_t aO, uint32_t offRb, uint32_t offLb,
-                                            uint32_t aJ, bool ylast, bool yfirst, uint32_t own, uint32_t i_orig,
+__device__ __forceinline__ void stage1_site(uint32_t aO, uint32_t offRb, uint32_t offLb, uint32_t offDb,
+                                            uint32_t offUb, uint32_t aJ, uint32_t own, uint32_t i_orig,
                                             const PlaneUniform &U, const RoundKeys &rkr, const uint32_t *P,
                                             uint32_t &D, uint32_t &acc, uint32_t &m8)
 {
     const uint32_t xr = lds_u32(aO + offRb);
     const uint32_t xl = lds_u32(aO + offLb);
-    const uint32_t xd = lds_u32(aO + (ylast ? X.wrapDb : X.hx4));
-    const uint32_t xu = lds_u32(aO + (yfirst ? X.wrapUb : 0u - X.hx4));
+    const uint32_t xd = lds_u32(aO + offDb);
+    const uint32_t xu = lds_u32(aO + offUb);
     const uint32_t jw = lds_u8(aJ) * 0x10204080u;
     const uint32_t a0 = ~(own ^ xr ^ byte_sign_mask<0>(jw));
     const uint32_t a1 = ~(own ^ xl ^ byte_sign_mask<1>(jw));
@@ -194,6 +202,51 @@ __device__ __forceinline__ void finish_inline(uint32_t i_orig, const PlaneUnifor
     } while (D && j4 < 16u);
 }
 
+struct PassConst {
+    uint32_t dO;    // other class, same cell (bytes)
+    uint32_t jb;    // J bytes of the class
+    uint32_t offRb, offLb;  // horizontal neighbour offsets (bytes, within the other class)
+    uint32_t rstep, istep;  // per pass: class words (not bytes), original ids
+    int c;
+};
+
+struct PassState {
+    uint32_t aC, lq, i_orig;
+    int wq;
+};
+
+// One pass of stage 1 for the thread's site in row y (then advances the state to the next
+// pass).  WRAP: the pass may hold row 0 or row Ly-1 (vertical neighbours wrap) or rows >= y1.
+template <bool WRAP>
+__device__ __forceinline__ void pass_site(const Ctx &X, const PassConst &pc, PassState &ps, int y,
+                                          const PlaneUniform &U, const RoundKeys &rkr, const uint32_t *P)
+{
+    const GridGeom &G = X.G;
+    const bool valid = X.T.active && (!WRAP || y < X.y1);
+    uint32_t own = 0, D = 0, acc = 0, m8 = 0;
+    if (valid) {
+        own = lds_u32(ps.aC);
+        const uint32_t offD = WRAP && y + 1 == G.Ly ? X.wrapDb : X.hx4;
+        const uint32_t offU = WRAP && y == 0 ? X.wrapUb : 0u - X.hx4;
+        stage1_site(ps.aC + pc.dO, pc.offRb, pc.offLb, offD, offU, pc.jb + ps.lq, own, ps.i_orig, U, rkr, P, D, acc,
+                    m8);
+    }
+    const bool need = D != 0u;
+    const uint32_t pm = __ballot_sync(0xFFFFFFFFu, need);
+    const int slot = ps.wq + __popc(pm & lanemask_lt());
+    ps.wq += __popc(pm);
+    if (need && slot < X.wlim) {
+        sts_u128(X.sQw + 16u * (uint32_t)slot, make_uint4(ps.lq | (ps.i_orig << 16), D, acc, m8));
+    } else if (valid) {
+        if (need)
+            finish_inline(ps.i_orig, U, rkr, P, m8, D, acc);
+        sts_u32(ps.aC, own ^ acc);
+    }
+    ps.aC += 4u * pc.rstep;
+    ps.lq += pc.rstep;
+    ps.i_orig += pc.istep;
+}
+
 // One colour phase c of sweep t for word group g: stage 1 over the thread's passes (+ the
 // leftover rows on the column-less warps), then the warp's own stage-2 queue (X.sQw), then a
 // CTA barrier.  Spins (X.sS) in colour-separated order; P: the word type's planes.
@@ -206,40 +259,35 @@ __device__ __forceinline__ void colour_phase(const Ctx &X, int c, const PlaneUni
     // rpp is even, so a thread's sites all have parity par = (c + ty) & 1 and fixed
     // horizontal neighbour offsets; rows advance by rpp per pass.  Shared-memory addresses
     // are explicit 32-bit byte addresses advanced per pass.
-    const int par = (c + T.ty) & 1;
+    const int ys = X.y0 + T.ty;  // the thread's first row
+    const int par = (c + ys) & 1;
     const int hx = G.hx;
-    const uint32_t l0 = (uint32_t)(T.ty * hx + T.m);
-    uint32_t aC = X.sS + 4u * ((uint32_t)(c * G.half) + l0);        // own word
-    uint32_t aO = X.sS + 4u * ((uint32_t)((1 - c) * G.half) + l0);  // same cell, other class
-    uint32_t aJ = X.sJB + (uint32_t)(c * G.half) + l0;
-    const uint32_t offRb = 4u * (uint32_t)(par ? X.offR1 : 0);
-    const uint32_t offLb = 4u * (uint32_t)(par ? 0 : X.offL0);
-    const uint32_t rstep = (uint32_t)(X.rpp * hx), istep = (uint32_t)(G.Lx * X.rpp);
-    uint32_t i_orig = (uint32_t)(2 * T.m + par + G.Lx * T.ty);
-    uint32_t lq = l0;  // the site's index in its class (queue items carry it)
-    int wq = 0;  // warp-uniform
-    int y = T.ty;
+    const uint32_t l0 = (uint32_t)(ys * hx + T.m);
+    // the site's words: own at aC, neighbours of the other class at aC + dO + (right, left, down,
+    // up) offsets, J bytes at jb + lq; dO, jb and the vertical offsets are CTA-uniform
+    PassState ps;
+    ps.aC = X.sS + 4u * ((uint32_t)(c * G.half) + l0);
+    ps.lq = l0;  // the site's index in its class (queue items carry it)
+    ps.i_orig = (uint32_t)(2 * T.m + par + G.Lx * ys);
+    ps.wq = 0;   // warp-uniform
+    const PassConst pc{4u * (uint32_t)((1 - 2 * c) * G.half), X.sJB + (uint32_t)(c * G.half),
+                       4u * (uint32_t)(par ? X.offR1 : 0), 4u * (uint32_t)(par ? 0 : X.offL0),
+                       (uint32_t)(X.rpp * hx), (uint32_t)(G.Lx * X.rpp), c};
+    // rows 0 and Ly-1 (the vertical wrap) can only be in the first and the last pass: the passes
+    // in between take the plain offsets and need no row test (their rows lie inside [y0, y1))
+    const int np = X.npass_main;
+    int y = ys;
+    pass_site<true>(X, pc, ps, y, U, rkr, P);
+    if (np > 1) {
 #pragma unroll 1
-    for (int pass = 0; pass < X.npass_main;
-         ++pass, y += X.rpp, aC += 4u * rstep, aO += 4u * rstep, aJ += rstep, i_orig += istep, lq += rstep) {
-        const bool valid = T.active && y < G.Ly;
-        uint32_t own = 0, D = 0, acc = 0, m8 = 0;
-        if (valid) {
-            own = lds_u32(aC);
-            stage1_site(X, aO, offRb, offLb, aJ, y + 1 == G.Ly, y == 0, own, i_orig, U, rkr, P, D, acc, m8);
+        for (int k = 1; k + 1 < np; ++k) {
+            y += X.rpp;
+            pass_site<false>(X, pc, ps, y, U, rkr, P);
         }
-        const bool need = D != 0u;
-        const uint32_t pm = __ballot_sync(0xFFFFFFFFu, need);
-        const int slot = wq + __popc(pm & lanemask_lt());
-        wq += __popc(pm);
-        if (need && slot < X.wlim) {
-            sts_u128(X.sQw + 16u * (uint32_t)slot, make_uint4(lq | (i_orig << 16), D, acc, m8));
-        } else if (valid) {
-            if (need)
-                finish_inline(i_orig, U, rkr, P, m8, D, acc);
-            sts_u32(aC, own ^ acc);
-        }
+        y += X.rpp;
+        pass_site<true>(X, pc, ps, y, U, rkr, P);
     }
+    int wq = ps.wq;
     // leftover rows (Ly not a multiple of rpp): the warps that hold no class column take them,
     // concurrently with the main passes, instead of a last partial pass of the column threads
     // (C2: rows 96..99 on the 16th warp, 8 passes per warp instead of 9 for five warps)
@@ -262,8 +310,8 @@ __device__ __forceinline__ void colour_phase(const Ctx &X, int c, const PlaneUni
             uint32_t own = 0, D = 0, acc = 0, m8 = 0;
             if (valid) {
                 own = lds_u32(bC);
-                stage1_site(X, bO, 4u * (uint32_t)oR, 4u * (uint32_t)oL, bJ, yy + 1 == G.Ly, yy == 0, own, io, U,
-                            rkr, P, D, acc, m8);
+                stage1_site(bO, 4u * (uint32_t)oR, 4u * (uint32_t)oL, yy + 1 == G.Ly ? X.wrapDb : X.hx4,
+                            yy == 0 ? X.wrapUb : 0u - X.hx4, bJ, own, io, U, rkr, P, D, acc, m8);
             }
             const bool need = D != 0u;
             const uint32_t pm = __ballot_sync(0xFFFFFFFFu, need);
@@ -304,9 +352,9 @@ __device__ __forceinline__ void colour_phase(const Ctx &X, int c, const PlaneUni
     __syncthreads();
 }
 
-// Per-lane count of unsatisfied bonds of the group's 32 replicas (lane b: replica b): every
-// bond joins a colour-0 and a colour-1 site, so the four bonds of the colour-1 sites count
-// each bond exactly once; E = 2U - 2n.
+// Per-lane count of unsatisfied bonds of the group's 32 replicas (lane b: replica b) over the
+// rows [y0, y1): every bond joins a colour-0 and a colour-1 site, so the four bonds of the
+// colour-1 sites count each bond exactly once; E = 2U - 2n (band split: the bands' counts add).
 __device__ __forceinline__ int32_t unsat_counts(const Ctx &X, const uint32_t *S, const uint8_t *JB)
 {
     const GridGeom &G = X.G;
@@ -316,8 +364,8 @@ __device__ __forceinline__ int32_t unsat_counts(const Ctx &X, const uint32_t *S,
         c7[l] = 0;
     const uint32_t *S1 = S + G.half;
     for (int pass = 0; pass < X.npass; ++pass) {
-        const int y = X.T.ty + pass * X.rpp;
-        if (X.T.active && y < G.Ly) {
+        const int y = X.y0 + X.T.ty + pass * X.rpp;
+        if (X.T.active && y < X.y1) {
             uint32_t a0, a1, a2, a3, i_orig;
             site_unsat(S, JB, G, X.T, 1, y, S1[y * G.hx + X.T.m], a0, a1, a2, a3, i_orig);
             vadd(c7, a0);

@@ -1,98 +1,26 @@
-// k_grid_bands.cu -- the torus sweep kernel of k_grid_bits.cu with each word group's rows
-// split over a CTA pair (sm_100a).  Used when a handle holds at most half as many word
-// groups as the GPU has SMs (e.g. one rank's share of C4 at 8 GPUs: 64 groups), so twice
-// as many SMs work.  Everything but the band bookkeeping is k_grid_bits;
-// kept as its own kernel so the single-band kernel's code generation is untouched.
+// k_grid_bands.cu -- the torus PT kernel with each word group's rows split over a CTA pair
+// (sm_100a).  Used when a handle holds at most half as many word groups as the GPU has SMs
+// (one rank's share of C4 at 8 GPUs: 64 groups), so twice as many SMs work.
 //
 // Band b of a group owns rows [y0, y1) = [b Ly/2, (b+1) Ly/2) and keeps a full copy of the
-// group's lattice in shared memory.  After every colour phase it pushes its edge rows of the
-// class just updated into the other band's copy through DSMEM and the cluster synchronises,
-// so the neighbour rows a phase reads are current.  Energies are the sum of the bands'
-// bond counts; the fused PT step runs on clusters of (K/32) x 2 CTAs (bits_core.cuh).
+// group's lattice in shared memory.  The colour phase and the bond count are grid_core.cuh's
+// (the same code as k_grid_bits / k_grid_sched) restricted to the band's rows; after every
+// colour phase the band pushes its edge rows of the class just updated into the other band's
+// copy through DSMEM and the cluster synchronises, so the neighbour rows a phase reads are
+// current.  Energies are the sum of the bands' bond counts; the fused PT step runs on clusters
+// of (K/32) x 2 CTAs (bits_core.cuh), or -- when those do not all fit at once -- on K/32
+// clusters of 2 that meet at global-memory copy barriers in one cooperative launch.
 //
-// Hot path rows a3-a6 of SURVEY.md §8(a) for the grid workloads (C2, C4; Gset
-// spin-glass tori, Table I).  One CTA owns one 32-replica word
-// group g (32 consecutive global slots = 32 temperatures of one copy) for all
-// n sites and keeps it resident in shared memory for a whole ising_sweep call:
-// load -> n_sweeps x {colour 0, colour 1} -> energy of the 32 replicas -> store.
-// Shared memory holds the spins in colour-separated order (each colour class
-// contiguous per row), so lane l of a warp touches word l of a row:
-// conflict-free LDS/STS for the site and all four neighbours.
-//
-// Per (site, word) -- 32 attempts at once, bit b = slot 32g+b:
-//   a_b   = ~(s_i ^ s_j ^ J_b)                 unsatisfied-bond bits (J_b s_i s_j = +1)
-//   u     = #unsatisfied among 4;  dE = 8 - 4u  (dE = -2 s_i h_i)
-//   m8/m4 = lanes with dE = 8 / 4 (u = 0 / 1); all other lanes flip (dE <= 0).
-//   PLANE contract: U64 bit (63-j) = bit b of word (j&3) of
-//       Philox(i, t, g, PLANE<<24 | j>>2); accept iff U64 < T[beta_k][dE].
-//   The comparison runs MSB plane first over the undecided lanes D:
-//       acc |= D & ~u_j & t_j;  D &= ~(u_j ^ t_j)
-//   and stops when D is empty (the first differing bit fixes U < T), so the
-//   result is exactly the 64-bit comparison.  t_j (threshold
-//   plane j of the word's 32 temperatures) comes from the host plane table
-//   P[wt][dE][j]; slot temperatures never change (exchanges move
-//   configurations), so the table is fixed for the whole run.
-//
-// Work compaction of the RNG tail: a colour phase runs in two
-// stages.  Stage 1: every site draws planes 0..7 (two Philox calls); ~89% of
-// words are then decided and written.  The rest are pushed to a shared-memory
-// queue and stage 2 finishes them with all 32 lanes of a warp busy, instead of
-// leaving most lanes of a warp idle while one lane draws its 3rd/4th call.
-// Philox rounds 0-1 are partially hoisted: the parts that depend only on the
-// CTA's group g, the sweep t or the site i are computed once, not per call.
-#include "bits_core.cuh"
+// Hot path rows a3-a6 of SURVEY.md §8(a) for the grid workloads (C4's 8-GPU share; Gset
+// spin-glass tori, Table I).
+#include "grid_core.cuh"
 
 namespace ising {
 
 using namespace bits;
 
-namespace {
 
-__device__ __forceinline__ int T_m_plus1_off(int tid, int hx)
-{
-    const int m = tid % hx;
-    return m + 1 == hx ? 1 - hx : 1;
-}
-
-__device__ __forceinline__ int T_m_minus1_off(int tid, int hx)
-{
-    const int m = tid % hx;
-    return m == 0 ? hx - 1 : -1;
-}
-
-// Site geometry of one thread in the 2-D mapping (column m of a colour class,
-// rows ty, ty + rpp, ...).
-struct ThreadGeom {
-    int m, mL, mR;  // class column and its wrapped neighbours
-    int ty;
-    bool active;
-};
-
-__device__ __forceinline__ void site_unsat(const uint32_t *S, const uint8_t *JB, const GridGeom &G,
-                                           const ThreadGeom &T, int c, int y, uint32_t own,
-                                           uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3,
-                                           uint32_t &i_orig)
-{
-    const int par = (c + y) & 1;
-    const int yd = (y + 1 == G.Ly) ? 0 : y + 1;
-    const int yu = (y == 0) ? G.Ly - 1 : y - 1;
-    const uint32_t *So = S + (1 - c) * G.half;
-    const int row = y * G.hx;
-    const uint32_t xr = So[row + (par ? T.mR : T.m)];
-    const uint32_t xl = So[row + (par ? T.m : T.mL)];
-    const uint32_t xd = So[yd * G.hx + T.m];
-    const uint32_t xu = So[yu * G.hx + T.m];
-    const uint32_t jw = (uint32_t)JB[c * G.half + row + T.m] * 0x10204080u;
-    a0 = ~(own ^ xr ^ byte_sign_mask<0>(jw));
-    a1 = ~(own ^ xl ^ byte_sign_mask<1>(jw));
-    a2 = ~(own ^ xd ^ byte_sign_mask<2>(jw));
-    a3 = ~(own ^ xu ^ byte_sign_mask<3>(jw));
-    i_orig = (uint32_t)(2 * T.m + par + G.Lx * y);
-}
-
-}  // namespace
-
-constexpr int kGridQItem = 16;  // tail-queue item, as k_grid_bits
+using grid::kGridQItem;
 
 // Copy-wide barrier over the copy's clusters through a global counter (the launch is
 // cooperative, so every CTA of the grid is resident and the spin cannot deadlock).
@@ -252,14 +180,11 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBit
     uint8_t *JB = reinterpret_cast<uint8_t *>(sm + n);
     uint32_t *P = reinterpret_cast<uint32_t *>(JB + ((n + 15) & ~15));  // P[0..63] dE=4, P[64..127] dE=8
     uint4 *Q4 = reinterpret_cast<uint4 *>(P + 128);  // tail queue (16-byte items)
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    const int nwarps = nt >> 5;
+    const int tid = threadIdx.x, nt = blockDim.x;
     const int qcap = p.qcap;
-    const int wcap = qcap / nwarps;  // per-warp queue region
     const int nbw = (n + 31) / 32;
     uint32_t *B0 = reinterpret_cast<uint32_t *>(Q4 + qcap);  // boundary bit planes (PT mode)
     uint32_t *B31 = B0 + nbw;
-    const int wq0 = warp * wcap;
 
     RoundKeys rkr;  // round keys held in registers for the whole launch
 #pragma unroll
@@ -280,21 +205,8 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBit
     const int c_local = gl / KW;
     const uint32_t c_global = g / (uint32_t)KW;
 
-    // 2-D thread mapping: column m = tid % hx of a class row, rows ty + k*rpp
-    const int rpp = grid_rows_per_pass(nt, G.hx);  // even when possible (host guarantees >= 1)
-    const int npass = (y1 - y0 + rpp - 1) / rpp;
-    // neighbour offsets of a class column: m+1 and m-1 wrapped, rows below/above wrapped
-    const int offR1 = T_m_plus1_off(tid, G.hx), offL0 = T_m_minus1_off(tid, G.hx);
-    const uint32_t hx4 = 4u * (uint32_t)G.hx;
-    const uint32_t wrapDb = 4u * (uint32_t)((1 - G.Ly) * G.hx), wrapUb = 4u * (uint32_t)((G.Ly - 1) * G.hx);
-    const uint32_t sS = (uint32_t)__cvta_generic_to_shared(S);
-    const uint32_t sJB = (uint32_t)__cvta_generic_to_shared(JB);
-    ThreadGeom T;
-    T.ty = tid / G.hx;
-    T.m = tid - T.ty * G.hx;
-    T.mL = T.m == 0 ? G.hx - 1 : T.m - 1;
-    T.mR = T.m + 1 == G.hx ? 0 : T.m + 1;
-    T.active = T.ty < rpp;
+    // the colour phase and the bond count of grid_core.cuh over this band's rows [y0, y1)
+    const grid::Ctx X = grid::make_ctx(G, n, qcap, S, JB, Q4, false, y0, y1, /*limit_stage2=*/false);
 
     // ---- load: original order -> colour-separated order
     const uint32_t *src = p.state_in + (size_t)gl * n;
@@ -328,106 +240,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBit
             }
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
-                uint32_t *Sc = S + c * G.half;
-#ifdef ISING_GRID_TIMING
-                long long tA = clock64();
-#endif
-                // stage 1: planes 0..7 for every site; undecided words go to this warp's queue.
-                // rpp is even, so a thread's sites all have parity par = (c + ty) & 1 and fixed
-                // horizontal neighbour offsets; rows advance by rpp per pass.  Shared-memory
-                // addresses are explicit 32-bit byte addresses advanced per pass.
-                const int par = (c + y0 + T.ty) & 1;
-                const int hx = G.hx;
-                const uint32_t l0 = (uint32_t)((y0 + T.ty) * hx + T.m);
-                uint32_t aC = sS + 4u * ((uint32_t)(c * G.half) + l0);        // own word
-                uint32_t aO = sS + 4u * ((uint32_t)((1 - c) * G.half) + l0);  // same cell, other class
-                uint32_t aJ = sJB + (uint32_t)(c * G.half) + l0;
-                const uint32_t offRb = 4u * (uint32_t)(par ? offR1 : 0);
-                const uint32_t offLb = 4u * (uint32_t)(par ? 0 : offL0);
-                const uint32_t rstep = (uint32_t)(rpp * hx), istep = (uint32_t)(G.Lx * rpp);
-                uint32_t i_orig = (uint32_t)(2 * T.m + par + G.Lx * (y0 + T.ty));
-                int wq = 0;  // warp-uniform
-                int y = y0 + T.ty;
-#pragma unroll 1
-                for (int pass = 0; pass < npass;
-                     ++pass, y += rpp, aC += 4u * rstep, aO += 4u * rstep, aJ += rstep, i_orig += istep) {
-                    const bool valid = T.active && y < y1;
-                    uint32_t own = 0, D = 0, acc = 0, m8 = 0;
-                    if (valid) {
-                        own = lds_u32(aC);
-                        const uint32_t xr = lds_u32(aO + offRb);
-                        const uint32_t xl = lds_u32(aO + offLb);
-                        const uint32_t xd = lds_u32(aO + (y + 1 == G.Ly ? wrapDb : hx4));
-                        const uint32_t xu = lds_u32(aO + (y == 0 ? wrapUb : 0u - hx4));
-                        const uint32_t jw = lds_u8(aJ) * 0x10204080u;
-                        const uint32_t a0 = ~(own ^ xr ^ byte_sign_mask<0>(jw));
-                        const uint32_t a1 = ~(own ^ xl ^ byte_sign_mask<1>(jw));
-                        const uint32_t a2 = ~(own ^ xd ^ byte_sign_mask<2>(jw));
-                        const uint32_t a3 = ~(own ^ xu ^ byte_sign_mask<3>(jw));
-                        const uint32_t s01 = a0 ^ a1, c01 = a0 & a1;
-                        const uint32_t s23 = a2 ^ a3, c23 = a2 & a3;
-                        m8 = ~(s01 | c01 | s23 | c23);                   // u = 0 -> dE = 8
-                        const uint32_t m4 = (s01 ^ s23) & ~(c01 | c23);  // u = 1 -> dE = 4
-                        D = m8 | m4;
-                        acc = ~D;  // dE <= 0 always flips
-                        if (D) {  // planes 0..7: both calls issued together (two independent chains)
-                            uint32_t sA, sB;
-                            plane_site(i_orig, U, rkr, sA, sB);
-                            plane_call2(sA, sB, U, rkr, P, m8, D, acc);
-                        }
-                    }
-                    const bool need = D != 0u;
-                    const uint32_t pm = __ballot_sync(0xFFFFFFFFu, need);
-                    const int slot = wq + __popc(pm & lanemask_lt());
-                    wq += __popc(pm);
-                    if (need && slot < wcap) {
-                        const uint32_t l = (aC - sS) / 4u - (uint32_t)(c * G.half);
-                        Q4[wq0 + slot] = make_uint4(l | (i_orig << 16), D, acc, m8);
-                    } else if (valid) {
-                        if (need) {  // this warp's queue region is full: finish inline
-                            uint32_t sA, sB;
-                            plane_site(i_orig, U, rkr, sA, sB);
-                            uint32_t j4 = 2;
-                            do {
-                                plane_call(sA, sB, j4, U, rkr, P, m8, D, acc);
-                                ++j4;
-                            } while (D && j4 < 16u);
-                        }
-                        sts_u32(aC, own ^ acc);
-                    }
-                }
-#ifdef ISING_GRID_TIMING
-                long long tB = clock64();
-#endif
-#ifdef ISING_GRID_TIMING
-                long long tC = clock64();
-#endif
-                // stage 2: each warp finishes its own queued words right after its stage 1
-                const int nown = min(wq, wcap);
-                for (int qb = 0; qb < nown; qb += 32) {
-                    const int q = qb + lane;
-                    if (q >= nown)
-                        continue;
-                    const uint4 item = Q4[wq0 + q];
-                    const int l = (int)(item.x & 0xFFFFu);
-                    const uint32_t i_orig = item.x >> 16;
-                    uint32_t D = item.y, acc = item.z;
-                    const uint32_t m8 = item.w;
-                    uint32_t sA, sB;
-                    plane_site(i_orig, U, rkr, sA, sB);
-                    plane_call2(sA, sB, U, rkr, P, m8, D, acc, 2u);  // planes 8..15, calls interleaved
-                    uint32_t j4 = 4;
-                    while (D && j4 < 16u) {
-                        plane_call(sA, sB, j4, U, rkr, P, m8, D, acc);
-                        ++j4;
-                    }
-                    const uint32_t a = sS + 4u * ((uint32_t)(c * G.half) + (uint32_t)l);
-                    sts_u32(a, lds_u32(a) ^ acc);  // queued words were not written in stage 1
-                }
-#ifdef ISING_GRID_TIMING
-                long long tD = clock64();
-#endif
-                __syncthreads();
+                grid::colour_phase<false>(X, c, U, rkr, P);  // ends with a CTA barrier
                 if (NB > 1) {  // push this band's edge rows of class c into the neighbours' copies
                     cg::cluster_group cl = cg::this_cluster();
                     const unsigned rbase = cl.block_rank() - (unsigned)band;
@@ -441,49 +254,15 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBit
                     }
                     cl.sync();
                 }
-#ifdef ISING_GRID_TIMING
-                long long tE = clock64();
-                if (blockIdx.x == 0 && lane == 0 && round == 2 && s == 0)
-                    printf("T c=%d w=%2d s1=%lld b1=%lld s2=%lld b2=%lld nq=%d wq=%d\n", c, warp, tB - tA, tC - tB,
-                           tD - tC, tE - tD, nq, wq);
-#endif
             }
         }
 
-        // ---- energy: every bond joins a colour-0 and a colour-1 site, so the four
-        // bonds of the colour-1 sites count each bond exactly once.  E = 2U - 2n.
+        // ---- energy of this band's rows (the bands' counts add up to the group's)
         {
-            uint32_t c7[7];  // per-thread counts <= 4 * npass <= 124
-#pragma unroll
-            for (int l = 0; l < 7; ++l)
-                c7[l] = 0;
-            const uint32_t *S1 = S + G.half;
-            for (int pass = 0; pass < npass; ++pass) {
-                const int y = y0 + T.ty + pass * rpp;
-                if (T.active && y < y1) {
-                    uint32_t a0, a1, a2, a3, i_orig;
-                    site_unsat(S, JB, G, T, 1, y, S1[y * G.hx + T.m], a0, a1, a2, a3, i_orig);
-                    vadd(c7, a0);
-                    vadd(c7, a1);
-                    vadd(c7, a2);
-                    vadd(c7, a3);
-                }
-            }
-            uint32_t cnt[kCntLevels];
-#pragma unroll
-            for (int l = 0; l < kCntLevels; ++l)
-                cnt[l] = l < 7 ? c7[l] : 0u;
-            // warp total by a butterfly of bit-sliced additions, then lane b reads bit b
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1)
-                vsum_xor(cnt, off);
-            int32_t acc = 0;
-#pragma unroll
-            for (int l = 0; l < kCntLevels; ++l)
-                acc += (int32_t)((cnt[l] >> lane) & 1u) << l;
+            const int32_t acc = grid::unsat_counts(X, S, JB);
             if (p.k_ex == 0)  // no colour phase (hence no barrier) since the zeroing
                 __syncthreads();
-            atomicAdd(&Ucnt[lane], acc);
+            atomicAdd(&Ucnt[X.lane], acc);
             if (!pt)  // pt_step opens with a cluster barrier
                 __syncthreads();
         }

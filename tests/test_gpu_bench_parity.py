@@ -5,7 +5,8 @@
   SM taking (word group, round) tasks) and the cluster launch it replaced (k_grid_bits, clusters
   of 4 CTAs in ~4 waves) -- sampled copies from every wave, >= 100 sweeps (10 exchanges), bit for
   bit: spins of every slot of the copy, energies, walker ids and the per-copy best record.
-* C2 (configs[1]): 2 whole copies x 2,000 sweeps of the full 64-copy fused launch.
+* C2 (configs[1]) and C3 (configs[2]): 2 whole copies x 2,000 sweeps of the full 64-copy fused
+  launch.
 * C5 (configs[4]): 8 replicas of the full 4e6-vertex instance x 50 sweeps of the ring kernel:
   identical spins, energies within 1e-5 relative.
 * k_grid_sched on small tori (forced with ISING_GRID_SCHED=1): every slot against the oracle and
@@ -62,12 +63,14 @@ def check_copy(eng, o, cb):
     assert (cb[0][c], cb[1][c], cb[2][c]) == (ob.E, ob.slot, ob.sweep)
 
 
-@pytest.mark.parametrize("workload", ["c4b", "c4a"])
-@pytest.mark.parametrize("sched", ["1", "0"], ids=["sched", "clusters"])
-def test_c4_full_launch_sampled_copies(workload, sched, monkeypatch):
-    """The bench's C4 launch at 1 GPU: 128 copies x 128 temperatures, 100 sweeps, exchange
-    every 10; copies 0, 41, 86, 127 (first/middle/last waves of the cluster launch, tasks
-    handed out across the whole grid by the persistent launch) equal the oracle bit for bit."""
+@pytest.mark.parametrize("workload,sched,sweeps", [("c4b", "1", 1000), ("c4a", "1", 300), ("c4b", "0", 100),
+                                                    ("c4a", "0", 100)],
+                         ids=["c4b-sched", "c4a-sched", "c4b-clusters", "c4a-clusters"])
+def test_c4_full_launch_sampled_copies(workload, sched, sweeps, monkeypatch):
+    """The bench's C4 launch at 1 GPU: 128 copies x 128 temperatures, exchange every 10 --
+    1,000 sweeps (100 exchanges) on C4b's persistent launch, the bench's kernel; copies 0, 41,
+    86, 127 (first/middle/last waves of the cluster launch, tasks handed out across the whole
+    grid by the persistent launch) equal the oracle bit for bit."""
     monkeypatch.setenv("ISING_GRID_SCHED", sched)
     cfg = synth.CONFIGS[workload]
     inst = synth.make_instance(cfg)
@@ -75,7 +78,6 @@ def test_c4_full_launch_sampled_copies(workload, sched, monkeypatch):
     betas = synth.beta_ladder(K)
     eng = Engine(inst, K, C, betas, seed=KEY, layout="bits")
     assert eng.info.fused_pt == (3 if sched == "1" else 1)
-    sweeps = 100
     run_pt(eng, sweeps, cfg["k_ex"])
     cb = eng.copy_best()
     for c0, o in oracle_copies(inst, K, betas, (0, 41, 86, 127), sweeps, cfg["k_ex"]).items():
@@ -119,6 +121,21 @@ def test_c2_two_whole_copies_2000_sweeps():
     run_pt(eng, 2000, cfg["k_ex"])
     cb = eng.copy_best()
     for c0, o in oracle_copies(inst, K, betas, (5, 58), 2000, cfg["k_ex"]).items():
+        check_copy(eng, o, cb)
+
+
+def test_c3_two_whole_copies_2000_sweeps():
+    """C3's fused launch (G(1e4, 9999), smallest-last colouring, 64 copies) over 2,000 sweeps:
+    copies 3 and 60 equal the oracle bit for bit, including walker ids and per-copy best."""
+    cfg = synth.CONFIGS["c3"]
+    inst = synth.make_instance(cfg)
+    K, C = cfg["K"], cfg["C"]
+    betas = synth.beta_ladder(K)
+    eng = Engine(inst, K, C, betas, seed=KEY, layout="bits", colour=cfg["colouring"])
+    run_pt(eng, 2000, cfg["k_ex"])
+    cb = eng.copy_best()
+    col, _ = oracle.greedy_colour_sl(inst["n"], inst["row_ptr"], inst["col"])
+    for c0, o in oracle_copies(inst, K, betas, (3, 60), 2000, cfg["k_ex"], colour=col).items():
         check_copy(eng, o, cb)
 
 
