@@ -172,3 +172,20 @@ def test_grid_band_override_is_validated(monkeypatch):
     monkeypatch.setenv("ISING_GRID_BANDS", "2")
     c, msg = _code(L.ising_create_grid, 8, 8, Jr, Jd, **_desc(n_temps=256, betas=synth.beta_ladder(256)))
     assert c == L.ISING_E_UNSUPPORTED and "ISING_GRID_BANDS" in msg
+
+
+def test_colour_jp_argument_errors_without_gpu():
+    """ising_colour_jp validates its CSR before any device work (include/ising.h)."""
+    rp = np.array([0, 1, 2], np.int64)
+    c, _ = _code(L.ising_colour_jp, 2, rp, np.array([1, 5], np.int32))
+    assert c == L.ISING_E_GRAPH
+    c, _ = _code(L.ising_colour_jp, 2, np.array([1, 1, 2], np.int64), np.array([1, 0], np.int32))
+    assert c == L.ISING_E_GRAPH
+
+
+def test_desc_colouring_is_validated():
+    """An unknown ising_run_desc.colouring is an argument error, checked before device work."""
+    rp = np.array([0, 1, 2], np.int64)
+    c, msg = _code(L.ising_create_csr, 2, rp, np.array([1, 0], np.int32), np.array([1, 1], np.int32),
+                   **_desc(layout="i8", n_temps=8, betas=synth.beta_ladder(8), colouring=7))
+    assert c == L.ISING_E_ARG and "colouring" in msg
