@@ -59,6 +59,48 @@ __device__ __forceinline__ CsrSite csr_eval(const uint32_t *S, const CsrBitsPara
     return r;
 }
 
+// csr_eval for a vertex of small, compile-time degree DEG (the warp's vertices share it: a
+// class is sorted by degree): the unsatisfied-bond count u of the DEG bonds by a fixed adder and
+// D = {u < ceil(DEG/2)} directly, instead of the general loop's 4-bit vertical counter and
+// bit-sliced comparison.  u1, u2 are only used by the threshold multiplexer for DEG > 4.
+template <int DEG>
+__device__ __forceinline__ CsrSite csr_eval_fixed(const uint32_t *S, const CsrBitsParams &p, int v, int e0)
+{
+    CsrSite r;
+    r.own = S[v];
+    r.d = DEG;
+    uint32_t a[DEG > 0 ? DEG : 1];
+#pragma unroll
+    for (int k = 0; k < DEG; ++k) {
+        const uint32_t nb = __ldg(p.nbr + e0 + k);
+        a[k] = ~(r.own ^ S[nb & 0x7FFFFFFFu] ^ (uint32_t)((int32_t)nb >> 31));
+    }
+    r.u1 = r.u2 = 0u;
+    if (DEG == 0) {
+        r.u0 = 0u;
+        r.D = 0u;  // h = 0: dE = 0 always flips
+    } else if (DEG == 1) {
+        r.u0 = a[0];
+        r.D = ~a[0];
+    } else if (DEG == 2) {
+        r.u0 = a[0] ^ a[1];
+        r.u1 = a[0] & a[1];
+        r.D = ~(a[0] | a[1]);
+    } else if (DEG == 3) {
+        r.u0 = a[0] ^ a[1] ^ a[2];
+        r.u1 = (a[0] & a[1]) | (a[2] & (a[0] | a[1]));  // majority
+        r.D = ~r.u1;                                    // u <= 1
+    } else {  // DEG == 4
+        const uint32_t s3 = a[0] ^ a[1] ^ a[2], c3 = (a[0] & a[1]) | (a[2] & (a[0] | a[1]));
+        r.u0 = s3 ^ a[3];
+        const uint32_t c4 = s3 & a[3];
+        r.u1 = c3 ^ c4;
+        r.u2 = c3 & c4;
+        r.D = ~(r.u1 | r.u2);  // u <= 1
+    }
+    return r;
+}
+
 // m ? a : b bitwise, as ONE lop3 (the compiler otherwise splits it when ~m is live)
 __device__ __forceinline__ uint32_t mux(uint32_t m, uint32_t a, uint32_t b)
 {
@@ -227,9 +269,27 @@ __global__ void __launch_bounds__(kCsrMaxThreads, 1) k_csr_bits(const CsrBitsPar
                     const int v = b + lane;
                     const bool valid = v < v1;
                     uint32_t D = 0u, acc = 0u, io = 0u, own = 0u;
+                    // the warp's degree when its vertices share one (classes are degree-sorted)
+                    int e0 = 0, dv = -1;
+                    if (valid) {
+                        e0 = __ldg(p.rp + v);
+                        dv = __ldg(p.rp + v + 1) - e0;
+                    }
+                    const int dw = __reduce_max_sync(0xFFFFFFFFu, dv);
+                    const bool uni = __all_sync(0xFFFFFFFFu, dv == dw || dv < 0) && dw <= 4;
                     CsrSite st;
                     if (valid) {
-                        st = csr_eval(S, p, v);
+                        if (uni) {
+                            switch (dw) {  // warp-uniform
+                            case 0: st = csr_eval_fixed<0>(S, p, v, e0); break;
+                            case 1: st = csr_eval_fixed<1>(S, p, v, e0); break;
+                            case 2: st = csr_eval_fixed<2>(S, p, v, e0); break;
+                            case 3: st = csr_eval_fixed<3>(S, p, v, e0); break;
+                            default: st = csr_eval_fixed<4>(S, p, v, e0); break;
+                            }
+                        } else {
+                            st = csr_eval(S, p, v);
+                        }
                         own = st.own;
                         D = st.D;
                         acc = ~D;  // dE <= 0 always flips
