@@ -249,3 +249,29 @@ def test_merge_best_records_on_device():
     recs = np.stack([fr[:, 0].view(np.int64), fr[:, 1].astype(np.int64), fr[:, 2].astype(np.int64)], 1)
     r = feng.merge_best(torch.from_numpy(np.ascontiguousarray(recs)))
     assert (r["E"], r["sweep"], r["slot"]) == (-2.25, 9, 0)
+
+
+def test_c4b_gpu_count_invariance_with_each_shares_kernel():
+    """The strong-scaling shares of C4b -- 2 / 4 / 8 GPUs hold 64 / 32 / 16 copies, run by the
+    persistent launch / the cluster launch / the band-split cooperative launch -- reproduce the
+    1-GPU run (persistent launch over all 128 copies) bit for bit: energies, walkers and
+    per-copy best of every slot, 200 sweeps (every RNG counter uses global ids)."""
+    cfg = synth.CONFIGS["c4b"]
+    inst = synth.make_instance(cfg)
+    K, C = cfg["K"], cfg["C"]
+    betas = synth.beta_ladder(K)
+    full = Engine(inst, K, C, betas, seed=KEY, layout="bits")
+    run_pt(full, 200, cfg["k_ex"])
+    E, W = full.energies(), full.walkers()
+    cb = full.copy_best()
+    for N, kernel_fused in ((2, 3), (4, 1), (8, 2)):
+        share = C // N
+        for rank in (0, N - 1):
+            a, b = rank * share, (rank + 1) * share
+            eng = Engine(inst, K, C, betas, seed=KEY, copy_begin=a, copy_end=b, layout="bits")
+            assert eng.info.fused_pt == kernel_fused, (N, eng.info.fused_pt)
+            run_pt(eng, 200, cfg["k_ex"])
+            assert np.array_equal(eng.energies(), E[a * K:b * K]), N
+            assert np.array_equal(eng.walkers(), W[a * K:b * K]), N
+            for x, y in zip(eng.copy_best(), cb):
+                assert np.array_equal(x, y[a:b]), N
