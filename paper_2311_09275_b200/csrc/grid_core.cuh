@@ -249,8 +249,9 @@ __device__ __forceinline__ void pass_site(const Ctx &X, const PassConst &pc, Pas
 
 // One colour phase c of sweep t for word group g: stage 1 over the thread's passes (+ the
 // leftover rows on the column-less warps), then the warp's own stage-2 queue (X.sQw), then a
-// CTA barrier.  Spins (X.sS) in colour-separated order; P: the word type's planes.
-template <bool SPILL>
+// CTA barrier (BARRIER = false: only the warp's, for a caller that ends the phase with a
+// cluster barrier).  Spins (X.sS) in colour-separated order; P: the word type's planes.
+template <bool SPILL, bool BARRIER = true>
 __device__ __forceinline__ void colour_phase(const Ctx &X, int c, const PlaneUniform &U, const RoundKeys &rkr,
                                              const uint32_t *P)
 {
@@ -349,7 +350,10 @@ __device__ __forceinline__ void colour_phase(const Ctx &X, int c, const PlaneUni
         const uint32_t a = X.sS + 4u * ((uint32_t)(c * G.half) + (uint32_t)l);
         sts_u32(a, lds_u32(a) ^ acc);  // queued words were not written in stage 1
     }
-    __syncthreads();
+    if (BARRIER)
+        __syncthreads();
+    else
+        __syncwarp();  // the caller's barrier follows; the warp's own sites are final here
 }
 
 // Per-lane count of unsatisfied bonds of the group's 32 replicas (lane b: replica b) over the

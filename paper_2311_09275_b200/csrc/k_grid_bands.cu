@@ -240,20 +240,25 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_bands(const GridBit
             }
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
-                grid::colour_phase<false>(X, c, U, rkr, P);  // ends with a CTA barrier
-                if (NB > 1) {  // push this band's edge rows of class c into the neighbours' copies
-                    cg::cluster_group cl = cg::this_cluster();
+                // the band's edge rows of class c go to the other band's copy as soon as the
+                // warp that owns them has finished its phase (its stage-2 queue holds only its
+                // own sites), so one cluster barrier ends the phase
+                grid::colour_phase<false, false>(X, c, U, rkr, P);
+                cg::cluster_group cl = cg::this_cluster();
+                if (X.T.active) {
                     const unsigned rbase = cl.block_rank() - (unsigned)band;
-                    const int bup = (band + NB - 1) % NB, bdn = (band + 1) % NB;
-                    for (int x = tid; x < 2 * G.hx; x += nt) {
-                        const bool top = x < G.hx;  // row y0 -> band above, row y1-1 -> band below
-                        const int row = top ? y0 : y1 - 1;
-                        const int off = c * G.half + row * G.hx + (top ? x : x - G.hx);
-                        uint32_t *dst = cl.map_shared_rank(S, rbase + (unsigned)(top ? bup : bdn));
-                        dst[off] = S[off];
+                    const int nrows = y1 - y0;
+                    const int off0 = c * G.half + X.T.m;
+                    if (X.T.ty == 0) {  // row y0 -> the band above
+                        const int off = off0 + y0 * G.hx;
+                        cl.map_shared_rank(S, rbase + (unsigned)((band + NB - 1) % NB))[off] = S[off];
                     }
-                    cl.sync();
+                    if (X.T.ty == (nrows - 1) % X.rpp) {  // row y1 - 1 -> the band below
+                        const int off = off0 + (y1 - 1) * G.hx;
+                        cl.map_shared_rank(S, rbase + (unsigned)((band + 1) % NB))[off] = S[off];
+                    }
                 }
+                cl.sync();
             }
         }
 

@@ -70,11 +70,10 @@ def run(w):
         print(w, "plain run failed:", plain.stderr[-2000:])
         return
     csvp = os.path.join(ROOT, "gpurun_out", f"pipes_{tag}.csv")
-    # the band split's cooperative launch (global-memory copy barriers) cannot be replayed kernel by
-    # kernel: the whole application is replayed instead
-    replay = ["--replay-mode", "application"] if w == "c4b:share16" else []
-    prof = subprocess.run(["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none"] + replay +
-                          ["-k", f"regex:{kern}", "-s", str(skip), "-c", "1", "--csv"] + cmd, cwd=ROOT,
+    # (the band split's cooperative launch, c4b:share16, fails under ncu in kernel and in
+    # application replay alike: its copy barriers spin on global memory)
+    prof = subprocess.run(["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "-k",
+                           f"regex:{kern}", "-s", str(skip), "-c", "1", "--csv"] + cmd, cwd=ROOT,
                           capture_output=True, text=True, timeout=1800, env=env)
     with open(csvp, "w") as f:
         f.write(prof.stdout + prof.stderr)
