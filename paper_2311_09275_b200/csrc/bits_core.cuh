@@ -49,13 +49,11 @@ __device__ __forceinline__ void plane_site(uint32_t i, const PlaneUniform &u, co
     sB = u.H0r1 ^ L0 ^ rk.k[3];
 }
 
-// Philox4x32-10 of counter (i, t, g, PLANE<<24 | j4) from the hoisted parts.  Round
-// keys are re-derived from the 64-bit key (k0 + r W0, k1 + r W1): kernel-uniform values
-// the compiler keeps in uniform registers instead of reloading them per call.
+// Philox4x32-10 of counter (i, t, g, PLANE<<24 | j4) from the hoisted parts (rounds 2-9 in
+// full; the round keys are kernel-uniform values the compiler keeps in uniform registers).
 __device__ __forceinline__ uint4 philox_plane(uint32_t sA, uint32_t sB, uint32_t j4,
                                               const PlaneUniform &u, const RoundKeys &rk)
 {
-    const uint32_t k0 = rk.k[0], k1 = rk.k[1];
     const uint32_t X = sA ^ j4;  // round-0 output word 2 (j4 < 2^24)
     uint32_t c0 = __umulhi(kM1, X) ^ u.U0;
     uint32_t c1 = kM1 * X;

@@ -6,12 +6,13 @@
 // whole schedule and runs each copy as a cluster of K/32 CTAs.  With 512 groups in clusters
 // of 4, only 33 clusters (132 CTAs) fit on a B200 at once (GPC sizes), so 128 copies take 4
 // waves on 132 SMs: 86% of the GPU's SM-time.  Here one CTA per SM (a cooperative launch)
-// loops over TASKS = (word group, round): load the group's state from global memory (L2:
-// the whole C4b state is 41 MB), run the round's k_ex sweeps and the bond count in shared
-// memory exactly as k_grid_bits does (grid_core.cuh), store it, and publish the 32 energies.
-// Tasks are handed out by one atomic ticket in round-major order, so every SM stays busy
-// until the last round and the state round trip (~160 KB of L2 traffic per task of ~0.3 ms)
-// costs ~1%.
+// loops over TASKS = (word group, round): one TMA bulk copy brings the group's state (kept
+// colour-separated between rounds in a global scratch; the whole C4b state is 41 MB, L2-
+// resident) straight into the lattice array, the round's k_ex sweeps and the bond count run in
+// shared memory exactly as in k_grid_bits (grid_core.cuh), one bulk copy stores the state back
+// and the 32 energies are published.  Tasks are handed out by one atomic ticket in round-major
+// order (the next ticket is fetched while the current task runs), so every SM stays busy until
+// the last round; the state round trip (~160 KB of L2 traffic per task of ~0.3 ms) costs ~1%.
 //
 // The PT step of a copy (best-so-far check, exchange decisions, walker and energy swaps;
 // same rule and RNG counters as bits::pt_step / k_exchange) is run by the
@@ -83,7 +84,7 @@ __device__ __forceinline__ void bulk_store_wait(void *dst, uint32_t src, uint32_
 
 // The PT step of copy c_local after round `round` (all its K/32 groups stored).  Run by
 // every thread of the CTA that completed the copy's last task of the round.
-__device__ void copy_pt_step(PtShared &ps, const GridBitsParams &p, int round, int c_local, int Gl)
+__device__ void copy_pt_step(PtShared &ps, const GridBitsParams &p, int round, int c_local)
 {
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int KW = p.words_per_copy, K = 32 * KW, n = p.n;
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_sched(const GridBit
         __syncthreads();
         if (s_last) {  // this CTA completed the copy's round: its PT step
             __threadfence();
-            copy_pt_step(ps, p, round, c_local, Gl);
+            copy_pt_step(ps, p, round, c_local);
             __threadfence();
             __syncthreads();
             if (tid == 0)
