@@ -26,8 +26,19 @@ constexpr bool kI8Pipe = true;
 constexpr int32_t kI8PipeMinBlocks = 4;
 // float + padded-table graphs with R % 256 == 0: cp.async ring kernel with this many vertices
 // in flight per warp (0 = use the register pipeline)
-constexpr int32_t kI8Ring = 4;
-constexpr int32_t kI8RingUnroll = 4;  // ring kernel main-loop unroll (multiple of kI8Ring, divides 32; 8 measured -1.3%)
+// (the ISING_* macros only serve A/B builds of variants, abtest/variant.sh)
+#ifndef ISING_I8_RING
+#define ISING_I8_RING 4
+#endif
+#ifndef ISING_I8_RING_UNROLL
+#define ISING_I8_RING_UNROLL 4
+#endif
+#ifndef ISING_I8_RING_MINB
+#define ISING_I8_RING_MINB 3
+#endif
+constexpr int32_t kI8Ring = ISING_I8_RING;
+constexpr int32_t kI8RingUnroll = ISING_I8_RING_UNROLL;  // main-loop unroll (multiple of kI8Ring, divides 32; 8 measured -1.3%)
+constexpr int32_t kI8RingMinBlocks = ISING_I8_RING_MINB;  // resident CTAs per SM the ring kernel's registers are sized for
 
 // Rows of a colour class per pass of the 2-D thread mapping: threads / (Lx/2), rounded
 // down to an even number when >= 2 so that the parity (c + y) & 1 of a thread's sites is
