@@ -251,6 +251,7 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ our arm
 ALU_PEAK_FILE = os.path.join(ROOT, "profiles", "alu_peak.json")
+GATHER_PEAK_FILE = os.path.join(ROOT, "profiles", "gather_peak.json")
 
 
 def kernel_name(eng, inst, cfg, K, R, fused_one_launch):
@@ -289,11 +290,20 @@ def roofline_entry(kernel_ms, attempts_per_launch, layout, clocks, ipa_key):
         bpa = ipa.get("alg_bytes_per_attempt", 5.11) if ipa else 5.11
         ach = attempts_per_launch * bpa / (kernel_ms * 1e-3) / 1e9
         peak = peaks.get("hbm_gbs", 6551.4)
-        return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": (ipa or {}).get("dram_bytes_per_attempt") and
-                ipa["dram_bytes_per_attempt"] * attempts_per_launch,
-                "alg_bytes_per_attempt": bpa,
-                "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)"}
+        out = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+               "traffic": (ipa or {}).get("dram_bytes_per_attempt") and
+               ipa["dram_bytes_per_attempt"] * attempts_per_launch,
+               "alg_bytes_per_attempt": bpa,
+               "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)"}
+        if os.path.exists(GATHER_PEAK_FILE):
+            # the same access pattern without arithmetic (tools/gather_peak.cu): what this kernel's
+            # memory traffic alone can reach on a B200 (~23% of its gathers hit L2)
+            gp = json.load(open(GATHER_PEAK_FILE))
+            rate = attempts_per_launch / (kernel_ms * 1e-3)
+            out["pattern_roof"] = {"attempts_per_s": gp["attempts_per_s"], "frac": rate / gp["attempts_per_s"],
+                                   "source": "profiles/gather_peak.json (tools/gather_peak.cu, best of "
+                                             f"{len(gp.get('runs', []))} configurations)"}
+        return out
     mhz_max = peaks.get("sm_max_mhz", 1965.0)
     mhz = (clocks or {}).get("sm_mhz") or mhz_max
     alu = json.load(open(ALU_PEAK_FILE)) if os.path.exists(ALU_PEAK_FILE) else None
