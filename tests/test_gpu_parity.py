@@ -357,6 +357,31 @@ def test_float_int8_ring_parity(n, d, drop, K, C, sweeps, colouring):
     assert np.allclose(eng.energies(), o.energies(), rtol=1e-5, atol=0)
 
 
+@pytest.mark.parametrize("wset", [
+    [-1.0, 0.0, 1.0],                      # integer-valued: s h = 0 ties on every third term pattern
+    [0.0, -0.0, 0.5, -0.5, 1e-3, -1e-3, 1e-38, -1e-38, 1e-41, -1e-41, 3.0, -3.0],  # zeros, tiny, subnormal
+])
+def test_float_int8_degenerate_weights(wset):
+    """Float-weight ring kernel on degenerate couplings: exact zeros of both signs, ties s h = 0
+    (the estimate e = 2^16 leaves hi16 = 65535 to the exact path), subnormal and tiny terms in
+    the left fold.  Spins identical to the oracle; energies within 1e-5 of the scale sum |w|."""
+    n, K, C, sweeps = 2000, 32, 8, 20
+    u, v = synth.random_regular(n, 3, 60)
+    pick = (synth.splitmix64(61, u.size) % np.uint64(len(wset))).astype(np.int64)
+    w = np.asarray(wset, np.float32)[pick]
+    rp, col, ww = synth.edges_to_csr(n, u, v, w)
+    inst = dict(kind="csr", n=n, row_ptr=rp, col=col, w=ww.astype(np.float32))
+    betas = synth.beta_ladder(K)
+    eng = Engine(inst, K, C, betas, seed=KEY, layout="i8", colour="jp")
+    run_pt(eng, sweeps, 0)
+    colour, _ = oracle.greedy_colour_jp(n, rp, col)
+    o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=oracle.RNG_WORD, colour=colour).run(sweeps, 0)
+    for r in range(o.R):
+        assert np.array_equal(eng.spins(r), o.s[r]), f"slot {r}"
+    scale = float(np.abs(w.astype(np.float64)).sum())
+    assert np.allclose(eng.energies(), o.energies(), rtol=1e-5, atol=1e-5 * scale)
+
+
 def test_c5_full_size_sampled_replicas():
     cfg = synth.CONFIGS["c5"]
     inst = synth.make_instance(cfg)
