@@ -20,6 +20,9 @@ The same JSON line carries:
     the same run (value, roofline against measured HBM, clocks, e2e);
   * "scaling_projection" (N=1 only): one GPU's share of the N = 2/4/8 job (64/32/16 copies)
     timed on this GPU, i.e. the strong-scaling efficiency the kernels allow;
+  * "north_star_mode" (N=1 only): driver.run_pt(gather=True)'s per-round path (sweep launch,
+    16-byte record export, record all-gather, global best + exchange) over 2,000 C4b sweeps,
+    next to the fused schedule's rate;
   * "roofline" of the dominant kernel against the MEASURED issue roof of its instruction mix
     (tools/alu_peak.cu -> profiles/alu_peak.json) at the clock sampled in the timed region.
 Other workloads: --workload c1|c2|c3|c4a|c5 (c2/c3 weak scaling: a 64-copy shard per rank);
@@ -557,6 +560,54 @@ def scaling_projection(args, main_value, local):
     return out
 
 
+def north_star_mode(args, main_value, local, sweeps=2000):
+    """The record-gather mode of driver.run_pt(gather=True) (BASELINE.json north_star: an all-gather
+    of the per-replica records at every tempering exchange) on this GPU's C4b handle: per round one
+    sweep launch (k_ex sweeps), ising_exchange_begin (16-byte records), the all-gather -- at one
+    rank a device copy of the records, the data NCCL would move -- and ising_exchange_end (global
+    best over the gathered records, exchange decisions, swaps).  Timed with CUDA events over
+    `sweeps` sweeps; reported next to the fused single-launch rate of the main line."""
+    import torch
+
+    from paper_2311_09275_b200.driver import Engine
+
+    cfg = workload_params(args.workload, sweeps)
+    inst = synth.make_instance(cfg)
+    K, C, kex = cfg["K"], cfg["C"], cfg["k_ex"]
+    stream = torch.cuda.current_stream(local)
+    eng = Engine(inst, K, C, synth.beta_ladder(K), seed=synth.PHILOX_KEY, layout=cfg["layout"], device=local,
+                 block_threads=args.threads, stream=stream.cuda_stream)
+    send, recv = eng.record_buffers(1)
+    rounds = sweeps // kex
+
+    def step():
+        for _ in range(rounds):
+            eng.sweep(kex)
+            eng.exchange_begin(send)
+            recv.copy_(send)
+            eng.exchange_end(recv)
+
+    step()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(2):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    eng.close()
+    value = inst["n"] * K * C * rounds * kex / (min(ms) * 1e-3)
+    return {"value": value, "unit": "attempts/s", "sweeps": rounds * kex, "rounds": rounds,
+            "launches_per_round": "1 sweep launch + exchange_begin + record copy + exchange_end",
+            "frac_of_fused_value": value / main_value,
+            "note": "driver.run_pt(gather=True) device work at one rank; the default line runs the "
+                    "fused schedule (local exchanges, one best-record all-gather per step), which "
+                    "gives the same final best record (min over ranks of the per-rank first-reached "
+                    "minima, DESIGN.md §7)"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -570,6 +621,10 @@ def run_ours(args):
                    copies=args.copies, sweeps=args.sweeps, cpu=not args.no_cpu)
     if args.workload in STRONG and world == 1 and not args.copies and not args.no_projection:
         line["scaling_projection"] = scaling_projection(args, line["value"], local)
+        try:  # context record; never allowed to break the main line
+            line["north_star_mode"] = north_star_mode(args, line["value"], local)
+        except Exception as exc:  # pragma: no cover
+            line["north_star_mode"] = {"error": repr(exc)[:200]}
     if args.workload != "c5" and not args.no_c5:
         # the HBM-bound config (BASELINE.json configs[4], the north star's 60%-of-HBM target),
         # measured in the same run: 256 replicas per GPU, weak scaling
