@@ -1626,6 +1626,9 @@ int ising_run(ising_handle *h, int32_t n_rounds, int32_t k_ex)
         SmallI8Params p{};
         p.s = h->d_s8; p.rp = h->d_rp; p.col = h->d_col; p.wi = h->d_wi; p.orig = h->d_orig;
         p.class_off = h->d_class_off; p.T = h->d_T;
+        p.ell_col = h->ell_deg > 0 ? h->d_ell_col : nullptr; p.ell_w = h->d_ell_w;
+        for (int32_t c = 0; c < h->ncol; ++c)
+            p.max_class = std::max(p.max_class, h->class_off[c + 1] - h->class_off[c]);
         p.E_out = h->d_E; p.walker = h->d_walker; p.copy_best = h->d_copy_best; p.snap = h->d_snap;
         p.Tx = h->d_Tx; p.Tx_off = h->d_Tx_off; p.Tx_len = h->d_Tx_len;
         p.n = h->n; p.R = (int32_t)h->R; p.K = h->K; p.qmax = h->qmax; p.ncol = h->ncol;

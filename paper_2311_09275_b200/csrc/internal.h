@@ -157,6 +157,8 @@ struct SmallI8Params {
     const int32_t *rp, *col, *wi;  // internal CSR, integer weights
     const uint32_t *orig;      // internal -> original id
     const int32_t *class_off;  // [ncol+1]
+    const int32_t *ell_col, *ell_w;  // [n][4] padded neighbour table (pad -1, weight 0) or null
+    int32_t max_class;         // largest colour class (vertices)
     const uint64_t *T;         // [R][qmax+1] per local replica
     int64_t *E_out, *walker, *copy_best;
     int8_t *snap;              // [C_local][n] original order

@@ -1129,9 +1129,27 @@ __global__ void __launch_bounds__(kI8SmallThreads, 1) k_i8_small(const SmallI8Pa
 // through distributed shared memory, every CTA takes the same decisions, and the pair that
 // crosses two CTAs in odd exchanges (slots 8q+7, 8q+8) trades its byte columns over DSMEM
 // (both sides copy the other's column into a buffer, synchronise, then write).
+//
+// REG (every colour class has at most kI8ClusterThreads vertices, at most kRegCol classes, degree
+// <= 4: C1's 16 x 16 torus): thread tid owns vertex tid of every class for the whole launch and
+// keeps its padded neighbour row, weights and original id in registers, so a colour phase is one
+// dependent chain of shared-memory loads, one hoisted Philox call and the decisions, with no
+// global CSR loads; the per-round energies come from the same registers (each bond from its
+// lower internal endpoint) and a warp-shuffle reduction.
+// The 8 slots of a vertex are split over 8 / kRegRPT threads (kRegRPT replicas each, one
+// redundant Philox call per thread): more warps per SM to hide the dependent chain of a phase.
 constexpr int kI8ClusterThreads = 128;
+constexpr int kRegCol = 4;
+constexpr int kRegVerts = 128;  // vertices of a class per CTA row of threads
+#ifndef ISING_I8_REG_RPT
+#define ISING_I8_REG_RPT 4
+#endif
+constexpr int kRegRPT = ISING_I8_REG_RPT;  // replicas per thread
+constexpr int kI8ClusterRegThreads = kRegVerts * (8 / kRegRPT);
 
-__global__ void __launch_bounds__(kI8ClusterThreads, 1) k_i8_cluster(const SmallI8Params p)
+template <bool REG>
+__global__ void __launch_bounds__(REG ? kI8ClusterRegThreads : kI8ClusterThreads, 1)
+    k_i8_cluster(const SmallI8Params p)
 {
     extern __shared__ __align__(16) unsigned char cl_smem[];
     const int K = p.K, n = p.n, tid = threadIdx.x, nt = blockDim.x;
@@ -1167,9 +1185,113 @@ __global__ void __launch_bounds__(kI8ClusterThreads, 1) k_i8_cluster(const Small
     __syncthreads();
     const uint32_t g = (uint32_t)(slot_c >> 3) + (uint32_t)q;
     int8_t *Sb = reinterpret_cast<int8_t *>(S);
+    // REG: this thread's vertex of each class (-1: none), its padded row, weights, original id
+    int rv[kRegCol], rnb[kRegCol][4];
+    int32_t rw[kRegCol][4];
+    uint32_t rio[kRegCol];
+#pragma unroll
+    for (int cc = 0; cc < kRegCol; ++cc) {
+        rv[cc] = -1;
+        rio[cc] = 0u;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            rnb[cc][u] = 0;
+            rw[cc][u] = 0;
+        }
+        if (REG && cc < p.ncol) {
+            const int v = __ldg(p.class_off + cc) + tid % kRegVerts;
+            if (v < __ldg(p.class_off + cc + 1)) {
+                rv[cc] = v;
+                const int4 c4 = __ldg(reinterpret_cast<const int4 *>(p.ell_col) + v);
+                const int4 w4 = __ldg(reinterpret_cast<const int4 *>(p.ell_w) + v);
+                const int cs[4] = {c4.x, c4.y, c4.z, c4.w}, ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    rnb[cc][u] = cs[u] >= 0 ? cs[u] : v;  // pad: own row, weight 0
+                    rw[cc][u] = cs[u] >= 0 ? ws[u] : 0;
+                }
+                rio[cc] = __ldg(p.orig + v);
+            }
+        }
+    }
     for (int round = 0; round < p.n_rounds; ++round) {
         for (int sw = 0; sw < p.k_ex; ++sw) {
             const uint32_t t = p.t0 + (uint32_t)(round * p.k_ex + sw);
+            if (REG) {
+                // thread (vertex tid % kRegVerts, replicas sub*kRegRPT .. +kRegRPT-1 of the 8)
+                const int sub = tid / kRegVerts;
+                const int wi = (sub * kRegRPT) >> 2, bo = (sub * kRegRPT) & 3;  // word, first byte
+                uint32_t *Sw = reinterpret_cast<uint32_t *>(S);
+                const PhiloxHoist ph = philox_hoist(t, g, p.rk);
+#pragma unroll
+                for (int cc = 0; cc < kRegCol; ++cc) {
+                    if (cc >= p.ncol)
+                        break;
+                    const int v = rv[cc];
+                    if (v >= 0) {
+                        const uint32_t own = Sw[2 * v + wi];
+                        uint32_t nbw[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            nbw[u] = Sw[2 * rnb[cc][u] + wi];
+                        const uint4 h = philox_hoisted(rio[cc], ph, p.rk);
+                        // word (b >> 1) of the call for slot b = sub * kRegRPT + j, selected without
+                        // a dynamically indexed array (which would live in local memory)
+                        auto hword = [&](int j) {
+                            const int k = (sub * kRegRPT + j) >> 1;
+                            return k == 0 ? h.x : k == 1 ? h.y : k == 2 ? h.z : h.w;
+                        };
+                        int32_t sh[kRegRPT];
+#pragma unroll
+                        for (int j = 0; j < kRegRPT; ++j)
+                            sh[j] = 0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t x = own ^ nbw[u];
+                            const int32_t w = rw[cc][u];
+#pragma unroll
+                            for (int j = 0; j < kRegRPT; ++j) {
+                                const int32_t m = (int32_t)(x << (24 - 8 * (bo + j))) >> 31;  // -1 iff s_i != s_j
+                                sh[j] += (w ^ m) - m;
+                            }
+                        }
+                        // branch-free decisions: every threshold row entry is loaded (row 0 for
+                        // s h >= 0, unused), U < T is decided on the 16-bit high words, and only a
+                        // tie of the high words (probability 2^-16) takes the lo48 call
+                        uint64_t Tj[kRegRPT];
+#pragma unroll
+                        for (int j = 0; j < kRegRPT; ++j) {
+                            const int b = sub * kRegRPT + j;
+                            Tj[j] = Ts[(size_t)b * (p.qmax + 1) + (uint32_t)(sh[j] < 0 ? -sh[j] : 0)];
+                        }
+                        uint32_t fm = 0u;
+#pragma unroll
+                        for (int j = 0; j < kRegRPT; ++j) {
+                            const int b = sub * kRegRPT + j;  // slot within this CTA's 8
+                            const uint32_t hwj = hword(j);
+                            const uint32_t hb = (b & 1) ? (hwj >> 16) : (hwj & 0xFFFFu);
+                            const uint32_t th = (uint32_t)(Tj[j] >> 48);
+                            bool acc = sh[j] >= 0 || hb < th;  // dE = -2 s h <= 0, or U < T by the high word
+                            if (!acc && sh[j] < 0 && hb == th)
+                                acc = lo48_of(rio[cc], t, (uint32_t)(slot_c + 8 * q + b), p.rk) <
+                                      (Tj[j] & 0xFFFFFFFFFFFFull);
+                            if (acc)
+                                fm |= 0xFEu << (8 * (bo + j));
+                        }
+                        if (kRegRPT == 4) {
+                            Sw[2 * v + wi] = own ^ fm;
+                        } else if (kRegRPT == 2) {  // this thread's bytes only (the rest belong to peers)
+                            uint16_t *Sh = reinterpret_cast<uint16_t *>(S);
+                            Sh[4 * v + ((sub * kRegRPT) >> 1)] = (uint16_t)((own ^ fm) >> (8 * bo));
+                        } else {
+                            uint8_t *S8 = reinterpret_cast<uint8_t *>(S);
+                            S8[8 * v + sub] = (uint8_t)((own ^ fm) >> (8 * bo));
+                        }
+                    }
+                    __syncthreads();
+                }
+                continue;
+            }
             for (int ccl = 0; ccl < p.ncol; ++ccl) {
                 const int v0 = p.class_off[ccl], v1 = p.class_off[ccl + 1];
                 for (int v = v0 + tid; v < v1; v += nt) {
@@ -1213,7 +1335,55 @@ __global__ void __launch_bounds__(kI8ClusterThreads, 1) k_i8_cluster(const Small
                 __syncthreads();
             }
         }
-        {  // energies of this CTA's 8 slots (each edge once, fixed-order partial sums)
+        if (REG) {  // energies of this CTA's 8 slots from the register rows (each bond once)
+            const int sub = tid / kRegVerts;
+            const int wi = (sub * kRegRPT) >> 2, bo = (sub * kRegRPT) & 3;
+            const uint32_t *Sw = reinterpret_cast<const uint32_t *>(S);
+            int32_t ea[kRegRPT];
+#pragma unroll
+            for (int j = 0; j < kRegRPT; ++j)
+                ea[j] = 0;
+#pragma unroll
+            for (int cc = 0; cc < kRegCol; ++cc) {
+                const int v = rv[cc];
+                if (v < 0)
+                    continue;
+                const uint32_t own = Sw[2 * v + wi];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int jv = rnb[cc][u];
+                    if (jv <= v)  // the bond is counted from its lower endpoint (pads: jv = v)
+                        continue;
+                    const uint32_t x = own ^ Sw[2 * jv + wi];
+                    const int32_t w = rw[cc][u];
+#pragma unroll
+                    for (int j = 0; j < kRegRPT; ++j) {
+                        const int32_t m = (int32_t)(x << (24 - 8 * (bo + j))) >> 31;
+                        ea[j] += (w ^ m) - m;  // w s_v s_j
+                    }
+                }
+            }
+            // |partial| <= sum |w| < 2^30 (create-time guard): int32 warp sums, int64 over warps;
+            // the warps of one replica group (sub) are tid / 32 in [sub * 4, sub * 4 + 4)
+#pragma unroll
+            for (int j = 0; j < kRegRPT; ++j)
+                ea[j] = __reduce_add_sync(0xFFFFFFFFu, ea[j]);
+            if ((tid & 31) == 0)
+#pragma unroll
+                for (int j = 0; j < kRegRPT; ++j)
+                    part[(tid >> 5) * kRegRPT + j] = ea[j];
+            __syncthreads();
+            if (tid < 8) {
+                constexpr int wpg = kRegVerts / 32;  // warps per replica group
+                const int sb = tid / kRegRPT, jb = tid % kRegRPT;
+                int64_t e = 0;
+                for (int w = 0; w < wpg; ++w)
+                    e += part[(sb * wpg + w) * kRegRPT + jb];
+                Eown[tid] = e;
+            }
+            if (tid < 2)
+                mswap[tid] = 0u;
+        } else {  // energies of this CTA's 8 slots (each edge once, fixed-order partial sums)
             const int b = tid & 7, pt = tid >> 3, np = nt >> 3;
             int64_t acc = 0;
             for (int v = pt; v < n; v += np) {
@@ -1353,14 +1523,19 @@ cudaError_t launch_i8_small(const SmallI8Params &p, int32_t C_local, cudaStream_
                         (size_t)p.K * (p.qmax + 1) * 8;
     if (kI8Cluster && p.K / 8 <= 8) {  // each copy on a cluster of K/8 CTAs (8 slots each)
         const int NC = p.K / 8;
-        const size_t cs = (((size_t)p.n * 10 + 15) & ~(size_t)15) + (size_t)(2 * p.K + 8 + kI8ClusterThreads) * 8 +
+        // register rows: every class fits one thread row per vertex, at most kRegCol classes,
+        // degree <= 4
+        const bool reg = p.ell_col != nullptr && p.ncol <= kRegCol && p.max_class <= kRegVerts;
+        const int nthr = reg ? kI8ClusterRegThreads : kI8ClusterThreads;
+        const size_t cs = (((size_t)p.n * 10 + 15) & ~(size_t)15) + (size_t)(2 * p.K + 8 + nthr) * 8 +
                           (size_t)8 * (p.qmax + 1) * 8;
-        cudaError_t e = cudaFuncSetAttribute(k_i8_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
+        auto kern = reg ? k_i8_cluster<true> : k_i8_cluster<false>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cs);
         if (e != cudaSuccess)
             return e;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(C_local * NC));
-        cfg.blockDim = dim3(kI8ClusterThreads);
+        cfg.blockDim = dim3((unsigned)nthr);
         cfg.dynamicSmemBytes = cs;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
@@ -1370,7 +1545,7 @@ cudaError_t launch_i8_small(const SmallI8Params &p, int32_t C_local, cudaStream_
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, k_i8_cluster, p);
+        return cudaLaunchKernelEx(&cfg, kern, p);
     }
     cudaError_t e = cudaFuncSetAttribute(k_i8_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
