@@ -298,6 +298,36 @@ def test_int8_fused_small_pt_parity(n, m, K, C, sweeps, kex):
         assert np.array_equal(x, y)
 
 
+@pytest.mark.parametrize("n,drop,K,C,sweeps,kex", [
+    (256, 7, 32, 2, 43, 5),   # <= 4 classes of <= 128 vertices, degree <= 3 with pads: register path
+    (220, 0, 64, 1, 30, 10),  # 3-regular, 8 CTAs per copy: register path at the C1 cluster size
+    (600, 0, 16, 2, 20, 4),   # a class of > 128 vertices: the CSR path of the same kernel
+])
+def test_int8_cluster_register_path_parity(n, drop, K, C, sweeps, kex):
+    """k_i8_cluster's register path (each thread's class vertices, rows and weights in registers,
+    4 replicas per thread, branch-free threshold lookups) and its CSR path == per-round launches
+    == oracle on non-torus graphs with padded rows, integer weights in [-3, 3] \\ {0}."""
+    u, v = synth.random_regular(n, 3, 90 + n)
+    if drop:
+        keep = np.arange(u.size) % drop != 0
+        u, v = u[keep], v[keep]
+    w = (synth._below(synth.splitmix64(91 + n, u.size), 7) - 3).astype(np.int32)
+    w[w == 0] = 2
+    rp, col, ww = synth.edges_to_csr(n, u, v, w)
+    inst = dict(kind="csr", n=n, row_ptr=rp, col=col, w=ww.astype(np.int32))
+    betas = synth.beta_ladder(K)
+    a = Engine(inst, K, C, betas, seed=KEY, layout="i8")
+    assert a.info.fused_pt == 1
+    run_pt(a, sweeps, kex, fused=True)
+    b = Engine(inst, K, C, betas, seed=KEY, layout="i8")
+    run_pt(b, sweeps, kex, fused=False)
+    o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=oracle.RNG_WORD).run(sweeps, kex)
+    compare_copies(a, o)
+    compare_copies(b, o)
+    for x, y in zip(a.copy_best(), b.copy_best()):
+        assert np.array_equal(x, y)
+
+
 def _regular_inst(n, seed):
     u, v = synth.random_regular(n, 3, seed)
     w = synth.gaussian_f32(u.size, seed + 5)
