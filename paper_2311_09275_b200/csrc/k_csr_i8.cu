@@ -590,8 +590,19 @@ __device__ __forceinline__ void pipe_decide(const CsrI8Params &p, const I8Rows<D
             const float b2v = __ldg(p.betaf + 8u * o + (uint32_t)b);
             const float e = exp_est16(__fmul_rn(b2v, kLog2e), shb);
             const float d = fast_d(__uint_as_float(0x4B000000u | hb), e);
-            if (fast_accept(d) || fast_reject(d))
-                continue;  // decided by the fast path (same expressions)
+            // the two-comparison bracket decides every replica the k form decided (same bands,
+            // tests/test_fast_decision_classes.py); an accept is applied here as well, so this
+            // path stays correct for any valid fast test
+            const bool fa = fast_accept(d);
+            if (fa || fast_reject(d)) {
+                if (fa) {
+                    if (b < 4)
+                        fm[0] |= 0xFEu << (8 * (b & 3));
+                    else
+                        fm[1] |= 0xFEu << (8 * (b & 3));
+                }
+                continue;
+            }
             if (exact_less(hb, thr_x(__fmul_rn(b2v, shb)), m.io, p.t, 8u * g0 + (uint32_t)b, p.rk)) {
                 if (b < 4)  // scalar updates: a dynamically indexed fm[] would live in local memory
                     fm[0] |= 0xFEu << (8 * (b & 3));
