@@ -80,6 +80,8 @@ def parse():
                          "e.g. --workload c4b --copies 16 measures one rank's share at 8 GPUs")
     ap.add_argument("--threads", type=int, default=0, help="CTA size override")
     ap.add_argument("--no-c5", action="store_true", help="skip the nested C5 (HBM-bound) record")
+    ap.add_argument("--no-c5-int8", action="store_true",
+                    help="skip the nested C5 record on the int8 rows (ISING_I8_PACKED=0)")
     ap.add_argument("--no-projection", action="store_true",
                     help="skip the one-GPU share runs of the strong-scaling workload (N = 2, 4, 8)")
     return ap.parse_args()
@@ -265,7 +267,11 @@ def kernel_name(eng, inst, cfg, K, R, fused_one_launch):
     if cfg["layout"] == "bits":
         return "k_csr_bits"
     if inst.get("w") is not None and inst["w"].dtype == np.float32 and R % 256 == 0:
-        return "k_csr_i8_ring"
+        # the library sweeps a packed-row working copy when a call has >= 4 sweeps
+        # (ISING_I8_PACKED=0|1 overrides)
+        mode = os.environ.get("ISING_I8_PACKED")
+        calls = cfg["sweeps"] if cfg["k_ex"] <= 0 else cfg["k_ex"]
+        return "k_csr_packed" if mode == "1" or (mode != "0" and calls >= 4) else "k_csr_i8_ring"
     if fused_one_launch:
         return "k_i8_cluster" if K <= 64 else "k_i8_small"
     return "k_csr_i8_phase"
@@ -460,9 +466,19 @@ def measure(args, workload, world, rank, local, steps, warmup, e2e_steps, copies
     per_launch_attempts = n * R * (rounds * kex if fused else (kex if kex > 0 else sweeps_))
     kname = kernel_name(eng, inst, cfg, K, R, fused_one_launch)
     # instruction counts per attempt are kernel-specific
-    ipa_key = workload + {"k_grid_bands": "_bands", "k_grid_sched": "_sched"}.get(kname, "")
+    ipa_key = workload + {"k_grid_bands": "_bands", "k_grid_sched": "_sched", "k_csr_packed": "_packed"}.get(kname, "")
     roof = roofline_entry(avg_launch_ms, per_launch_attempts,
-                          "bits" if cfg["layout"] == "bits" or fused_one_launch else cfg["layout"], clk, ipa_key)
+                          "bits" if cfg["layout"] == "bits" or fused_one_launch or kname == "k_csr_packed"
+                          else cfg["layout"], clk, ipa_key)
+    if kname == "k_csr_packed":
+        # the packed rows move 196 algorithmic bytes per 256 attempts (own row read +
+        # written 64, three neighbour rows 96, table entry 36): against HBM for reference; the
+        # kernel is bound by the integer pipes (the roofline above)
+        pk_bpa = 196 / 256
+        roof["hbm"] = {"alg_bytes_per_attempt": pk_bpa,
+                       "achieved_gbs": per_launch_attempts * pk_bpa / (avg_launch_ms * 1e-3) / 1e9,
+                       "frac": per_launch_attempts * pk_bpa / (avg_launch_ms * 1e-3) / 1e9 /
+                       json.load(open(PEAKS_FILE)).get("hbm_gbs", 6551.4) if os.path.exists(PEAKS_FILE) else None}
     roof["kernel"] = kname
     if kname in ("k_i8_small", "k_i8_cluster"):
         per = K // 8 if kname == "k_i8_cluster" else 1
@@ -517,7 +533,7 @@ def measure(args, workload, world, rank, local, steps, warmup, e2e_steps, copies
         cpu_rec = cpu_oracle_sample(cfg, target_s=12.0 if not quiet_cfg else 8.0)
 
     peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
-    bpa = 0.25 if cfg["layout"] == "bits" else 5.11
+    bpa = 0.25 if cfg["layout"] == "bits" else (196 / 256 if kname == "k_csr_packed" else 5.11)
     return {
         "metric": "spin-flip attempts/s", "value": value, "unit": "attempts/s",
         "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": total_ms / steps,
@@ -633,6 +649,21 @@ def run_ours(args):
         line["c5"] = {k: c5[k] for k in ("value", "unit", "ms_per_step", "step_ms_rank0", "steps", "warmup",
                                          "scaling", "dtype", "config", "roofline", "hbm_frac", "e2e",
                                          "gpu_launches", "clocks", "cpu_baseline", "best")}
+        if c5["roofline"].get("kernel") == "k_csr_packed" and not args.no_c5_int8:
+            # the same workload on the int8 rows themselves (the HBM-bound kernel):
+            # the memory-roofline record of BASELINE.json's 60%-of-HBM target
+            prev = os.environ.get("ISING_I8_PACKED")
+            os.environ["ISING_I8_PACKED"] = "0"
+            try:
+                c5b = measure(args, "c5", world, rank, local, min(args.steps, 3), min(args.warmup, 3), 0,
+                              cpu=False, quiet_cfg=True)
+            finally:
+                if prev is None:
+                    os.environ.pop("ISING_I8_PACKED", None)
+                else:
+                    os.environ["ISING_I8_PACKED"] = prev
+            line["c5"]["int8_rows"] = {k: c5b[k] for k in ("value", "unit", "ms_per_step", "steps", "roofline",
+                                                            "hbm_frac", "clocks", "best")}
     if rank == 0:
         json_line(line)
     if world > 1:

@@ -169,7 +169,11 @@ ISING_API int ising_create_csr(int32_t n, const int64_t *row_ptr, const int32_t 
  * dE = -2 s_i h_i, h_i = sum_j w_ij s_j; accept if dE <= 0, else iff
  * U64 < floor(exp(-beta_k dE) 2^64) (float weights: the float32 contract
  * exponential).  Advances t by n_sweeps and refreshes the per-slot energies
- * at the end.  n_sweeps >= 0. */
+ * at the end.  n_sweeps >= 0.  I8 layout with float weights, maximum degree <= 4 and
+ * n_slots % 256 == 0: a call of >= 4 sweeps packs the int8 spins into a bit-packed working
+ * copy (n x n_slots/8 bytes, allocated on first use; without room for it the int8 kernels
+ * run), sweeps that, and unpacks it at the end -- the same decisions, so the same result
+ * (environment ISING_I8_PACKED=0 / 1 forces the int8 / packed kernels). */
 ISING_API int ising_sweep(ising_handle *h, int32_t n_sweeps);
 
 /* Per-local-slot energies (syncs).  out: int64[n_slots] for integer weights,

@@ -121,6 +121,7 @@ struct ising_handle {
     uint32_t *d_state[2] = {nullptr, nullptr};
     int cur = 0;
     int8_t *d_s8 = nullptr;
+    uint32_t *d_pk = nullptr;  // packed-row working copy of d_s8 (float + padded table, §5.4c), lazily allocated
     int64_t *d_E = nullptr;
     double *d_Ef = nullptr;
     int64_t *d_walker = nullptr;
@@ -969,7 +970,37 @@ int launch_sweeps_i8(ising_handle *h, int32_t ns, const void *sched)
             p.nq_shift = sh;
     p.slot0 = h->slot0; p.qmax = h->qmax; p.rk = h->rk;
     const int32_t thr = h->threads > kI8Threads ? kI8Threads : h->threads;
-    for (int32_t s = 0; s < ns; ++s) {
+    // float weights + padded table + R % 256 == 0: sweep a packed-row working copy of the
+    // state (same contract and decisions as the int8 kernels, so the result is
+    // identical), packed before the first and unpacked after the last sweep of this call.
+    // ISING_I8_PACKED=0 keeps the int8 kernels, =1 uses the packed rows for any sweep count.
+    bool packed = h->wtype == ISING_W_F32 && h->d_ell_col && h->R % 256 == 0 && h->slot0 % 8 == 0;
+    if (packed) {
+        int mode = -1;
+        if (const char *env = std::getenv("ISING_I8_PACKED"))
+            mode = std::atoi(env);
+        packed = mode == 1 || (mode != 0 && ns >= kI8PackedMinSweeps);
+    }
+    if (packed && !h->d_pk && h->alloc(&h->d_pk, (size_t)h->n * (size_t)(h->R / 32)) != cudaSuccess) {
+        (void)cudaGetLastError();  // no room for the working copy: the int8 kernels run instead
+        h->d_pk = nullptr;
+        packed = false;
+    }
+    if (packed) {
+        CK(launch_pack_rows(h->d_s8, h->d_pk, h->n, h->R, false, h->st));
+        for (int32_t s = 0; s < ns; ++s) {
+            p.t = h->t + (uint32_t)s;
+            if (sched)
+                p.betaf = (const float *)sched + (size_t)s * h->R;
+            for (int32_t c = 0; c < h->ncol; ++c) {
+                p.v_begin = h->class_off[c];
+                p.v_end = h->class_off[c + 1];
+                CK(launch_csr_packed_phase(p, h->d_pk, h->st));
+            }
+        }
+        CK(launch_pack_rows(h->d_s8, h->d_pk, h->n, h->R, true, h->st));
+    }
+    for (int32_t s = 0; s < (packed ? 0 : ns); ++s) {
         p.t = h->t + (uint32_t)s;
         if (sched) {
             if (h->wtype == ISING_W_I32)

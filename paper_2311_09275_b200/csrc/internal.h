@@ -39,6 +39,23 @@ constexpr int32_t kI8PipeMinBlocks = 4;
 constexpr int32_t kI8Ring = ISING_I8_RING;
 constexpr int32_t kI8RingUnroll = ISING_I8_RING_UNROLL;  // main-loop unroll (multiple of kI8Ring, divides 32; 8 measured -1.3%)
 constexpr int32_t kI8RingMinBlocks = ISING_I8_RING_MINB;  // resident CTAs per SM the ring kernel's registers are sized for
+// packed-row working copy of the int8 state for float + padded-table sweeps:
+// resident CTAs per SM its registers are sized for, and the fewest sweeps per call that use it
+// (each call packs the state before its first sweep and unpacks it after its last)
+#ifndef ISING_I8_PACKED_MINB
+#define ISING_I8_PACKED_MINB 3
+#endif
+// (4 resident CTAs per SM at 64 registers: -0.3%)
+constexpr int32_t kI8PackedMinBlocks = ISING_I8_PACKED_MINB;
+constexpr int32_t kI8PackedMinSweeps = 4;
+#ifndef ISING_I8_PACKED_RING
+#define ISING_I8_PACKED_RING 4
+#endif
+constexpr int32_t kI8PackedRing = ISING_I8_PACKED_RING;  // vertices in flight per warp (2: -2.3%)
+#ifndef ISING_I8_PACKED_UNROLL
+#define ISING_I8_PACKED_UNROLL 8
+#endif
+constexpr int32_t kI8PackedUnroll = ISING_I8_PACKED_UNROLL;  // main-loop unroll (8: +2.9% over 4)
 
 // Rows of a colour class per pass of the 2-D thread mapping: threads / (Lx/2), rounded
 // down to an even number when >= 2 so that the parity (c + y) & 1 of a thread's sites is
@@ -274,6 +291,10 @@ cudaError_t launch_csr_bits(const CsrBitsParams &p, int32_t G, int32_t threads, 
 size_t csr_bits_smem(int32_t n, int32_t qmax, int32_t words_per_copy);
 int32_t csr_bits_qcap(int32_t n, int32_t qmax);
 cudaError_t launch_csr_i8_phase(const CsrI8Params &p, int32_t threads, cudaStream_t st);
+// packed-row sweeps: s[n][R] int8 <-> P[n][R/32] words (unpack = true: P -> s), and one colour
+// phase on P (float weights, padded table, R % 256 == 0)
+cudaError_t launch_pack_rows(const int8_t *s, uint32_t *P, int64_t n, int64_t R, bool unpack, cudaStream_t st);
+cudaError_t launch_csr_packed_phase(const CsrI8Params &p, uint32_t *P, cudaStream_t st);
 cudaError_t launch_energy_i8(const int8_t *s, const int32_t *rp, const int32_t *col,
                              const int32_t *wi, const float *wf, int32_t n, int32_t R,
                              int64_t *Ei, double *Ef, void *scratch, size_t scratch_bytes,

@@ -891,6 +891,334 @@ cudaError_t launch_ring(const CsrI8Params &p, cudaStream_t st)
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- packed-row variant
+// The same sweep (WORD contract, relative-sign float fold, fast decision + exact bracket) on a
+// bit-packed working copy of the int8 state: row v holds the R replicas of vertex v as R/32
+// words (R/8 bytes instead of R), so a vertex step moves 4 x 32 bytes per 256 replicas instead
+// of 4 x 256.  Bit layout: word w of a row covers the int8 row's bytes
+// 32w .. 32w+31; byte 8a + k (local replica 32w + 8a + k) is bit pk(a, k) = 8 (k & 3) +
+// 4 (k >> 2) + a.  Lane l of the warp that owns replicas 256q .. 256q+255 decides replicas
+// 256q + 8l + k (k = 0..7, the 8 attempts of one WORD Philox call, as in the int8 kernels): the
+// bits pk(l & 3, k) of word 8q + (l >> 2), a word shared by 4 lanes.
+//
+// Field: s_i h is a function of the relative-sign pattern of the vertex's DEG neighbours, and
+// the contract fold of each of the 2^DEG patterns is computed once per vertex (lane l folds
+// pattern l mod 2^DEG: the same terms in the same order as the int8 kernels, so the same
+// floats).  Rotating x_u = own ^ nb_u right by a - u puts replica k's bit u at bit u of nibble
+// 2 (k & 3) + (k >> 2) of z (one bit-select per neighbour beyond the first), and the replica's
+// field is one shuffle from lane z >> 4 nibble (index bits above the pattern select duplicate
+// lanes).  The accepted bits come from the float sign bits of the decision differences by PRMT
+// sign replication (one byte per replica k & 3, masked to bit 4 (k >> 2) + a); the 4 lanes that
+// share a word OR-combine them by two xor-shuffles and lane a = 0 writes the word.
+__device__ __forceinline__ uint32_t pk_bit(uint32_t a, uint32_t k) { return 8u * (k & 3u) + 4u * (k >> 2) + a; }
+
+__global__ void k_pack_rows(const int8_t *__restrict__ s, uint32_t *__restrict__ P, uint64_t nwords)
+{
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(s) + 2 * w;
+        const uint4 u0 = __ldg(src), u1 = __ldg(src + 1);
+        const uint32_t b[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+        uint32_t out = 0u;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {  // byte i = 8a + k (bit 7 of the byte: spin -1)
+            const uint32_t bit = (b[i >> 2] >> (8 * (i & 3) + 7)) & 1u;
+            out |= bit << pk_bit((uint32_t)i >> 3, (uint32_t)i & 7u);
+        }
+        P[w] = out;
+    }
+}
+
+__global__ void k_unpack_rows(const uint32_t *__restrict__ P, int8_t *__restrict__ s, uint64_t nwords)
+{
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords;
+         w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t x = __ldg(P + w);
+        uint32_t b[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            uint32_t v = 0u;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int i = 4 * j + c;  // byte i = 8a + k
+                const uint32_t bit = (x >> pk_bit((uint32_t)i >> 3, (uint32_t)i & 7u)) & 1u;
+                v |= (bit ? 0xFFu : 0x01u) << (8 * c);
+            }
+            b[j] = v;
+        }
+        uint4 *dst = reinterpret_cast<uint4 *>(s) + 2 * w;
+        dst[0] = make_uint4(b[0], b[1], b[2], b[3]);
+        dst[1] = make_uint4(b[4], b[5], b[6], b[7]);
+    }
+}
+
+// rotate right (funnel shift of x with itself)
+__device__ __forceinline__ uint32_t rotr(uint32_t x, uint32_t n) { return __funnelshift_r(x, x, n); }
+
+// Decide the 8 attempts of one lane for vertex v from its words own / nb[u] (this lane's word of
+// each row), the weights wq and original id io; returns the word's flip mask (all 4 lanes).
+template <int DEG>
+__device__ __forceinline__ uint32_t packed_decide(const CsrI8Params &p, uint32_t own, const uint32_t (&nb)[DEG],
+                                                  const int4 &wq, uint32_t io, uint32_t a, const uint32_t (&pm)[DEG],
+                                                  const float (&bl)[8], const PhiloxHoist &ph, uint32_t g0,
+                                                  uint32_t o, uint32_t c4b, uint32_t amask)
+{
+    const uint32_t wv[4] = {(uint32_t)wq.x, (uint32_t)wq.y, (uint32_t)wq.z, (uint32_t)wq.w};
+    // the contract fold of this lane's pattern (pattern l mod 2^DEG)
+    float sv = __uint_as_float(wv[0] ^ pm[0]);
+#pragma unroll
+    for (int u = 1; u < DEG; ++u)
+        sv = __fadd_rn(sv, __uint_as_float(wv[u] ^ pm[u]));
+    // pattern nibbles: bit u of nibble 2 (k & 3) + (k >> 2) of z = bit pk(a, k) of own ^ nb_u
+    uint32_t z = rotr(own ^ nb[0], a);
+#pragma unroll
+    for (int u = 1; u < DEG; ++u) {
+        const uint32_t ru = rotr(own ^ nb[u], (a - (uint32_t)u) & 31u);
+        const uint32_t m = 0x11111111u << u;
+        z = (z & ~m) | (ru & m);
+    }
+    const uint4 h = philox_hoisted(io, ph, p.rk);
+    const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+    float sh[8];
+    uint32_t kb[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int nib = 2 * (k & 3) + (k >> 2);
+        sh[k] = __shfl_sync(0xFFFFFFFFu, sv, (int)(z >> (4 * nib)));
+        const float e = exp_est16(bl[k], sh[k]);
+        const uint32_t hword = hw[k >> 1];
+        const float hf = (k & 1) ? hi16_fr<1>(hword, c4b) : hi16_fr<0>(hword, c4b);  // 2^23 + hi16
+        kb[k] = __float_as_uint(__fsub_rn(fast_d(hf, e), 0x1p23f - 1.5f));
+    }
+    // k < 0: fast accept (sign bit); k in [+0, 3/2] (float bits <= 0x3FC00000): undecided
+    const uint32_t kmin = min(min(min(kb[0], kb[1]), min(kb[2], kb[3])), min(min(kb[4], kb[5]), min(kb[6], kb[7])));
+    // byte j of lo / hi = 0xFF where replica j / 4 + j accepts; bit pk(a, k) kept by amask
+    const uint32_t lo = sign_bytes4(kb[0], kb[1], kb[2], kb[3]);
+    const uint32_t hi = sign_bytes4(kb[4], kb[5], kb[6], kb[7]);
+    uint32_t acc = ((lo & 0x0F0F0F0Fu) | (hi & 0xF0F0F0F0u)) & amask;
+    if (__builtin_expect(kmin <= 0x3FC00000u, 0)) {  // rare: exact decisions
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) {
+            float shv = sh[0];
+#pragma unroll
+            for (int q = 1; q < 8; ++q)
+                shv = k == q ? sh[q] : shv;  // select, no dynamic indexing
+            const uint32_t bit = 1u << pk_bit(a, (uint32_t)k);
+            if (shv >= 0.0f) {
+                acc |= bit;
+                continue;
+            }
+            const int kh = k >> 1;
+            const uint32_t hword = kh == 0 ? h.x : kh == 1 ? h.y : kh == 2 ? h.z : h.w;
+            const uint32_t hb = (k & 1) ? (hword >> 16) : (hword & 0xFFFFu);
+            const float b2v = __ldg(p.betaf + 8u * o + (uint32_t)k);
+            const float e = exp_est16(__fmul_rn(b2v, kLog2e), shv);
+            const float d = fast_d(__uint_as_float(0x4B000000u | hb), e);
+            const bool fa = fast_accept(d);
+            if (fa || fast_reject(d)) {  // the bracket decides what the k form decided (same bands)
+                acc = fa ? (acc | bit) : (acc & ~bit);
+                continue;
+            }
+            if (exact_less(hb, thr_x(__fmul_rn(b2v, shv)), io, p.t, 8u * g0 + (uint32_t)k, p.rk))
+                acc |= bit;
+            else
+                acc &= ~bit;
+        }
+    }
+    acc |= __shfl_xor_sync(0xFFFFFFFFu, acc, 1);
+    acc |= __shfl_xor_sync(0xFFFFFFFFu, acc, 2);
+    return acc;
+}
+
+// Each warp sweeps a contiguous chunk of the colour class for one 256-replica slice, with S
+// vertices' rows in flight through a per-warp shared-memory ring filled by cp.async (each lane
+// copies and reads back only its own 4-byte word of each row) and the table entries (columns,
+// weights, original id: 48 bytes) of 32 consecutive vertices in a double buffer, 32 ahead
+// (the k_csr_i8_ring scheme with 32-byte rows).
+template <int DEG, int S>
+__host__ __device__ constexpr uint32_t packed_warp_bytes()
+{
+    return (uint32_t)S * (DEG + 1) * 128u + 2u * kRingMetaBuf;
+}
+
+template <int DEG, int S>
+__global__ void __launch_bounds__(256, kI8PackedMinBlocks) k_csr_packed(const CsrI8Params p, uint32_t *P,
+                                                                         uint32_t nslice, uint32_t chunk)
+{
+    extern __shared__ __align__(16) unsigned char pk_smem[];
+    constexpr uint32_t kSlot = (DEG + 1) * 128u;
+    constexpr uint32_t kRing = S * kSlot;
+    const uint32_t lane = threadIdx.x;
+    const uint32_t gw = blockIdx.x * blockDim.y + threadIdx.y;
+    const uint32_t nv = (uint32_t)(p.v_end - p.v_begin);
+    const uint32_t slice = gw % nslice;
+    const uint32_t j0 = (gw / nslice) * chunk;
+    if (j0 >= nv)
+        return;
+    const uint32_t cnt = min(chunk, nv - j0);
+    const uint32_t o = slice * 32u + lane;  // local replicas 8o .. 8o+7
+    const uint32_t a = lane & 3u;
+    const uint32_t rwb = (uint32_t)p.R >> 3;  // packed row bytes
+    // this lane's word column of the packed rows (an opaque register copy, as in the ring kernel)
+    char *tbb;
+    asm volatile("mov.b64 %0, %1;" : "=l"(tbb) : "l"(reinterpret_cast<char *>(P) + 4u * (slice * 8u + (lane >> 2))));
+    const uint32_t g0 = (uint32_t)(p.slot0 >> 3) + o;
+    float bl[8];
+    {
+        const float4 *bp = reinterpret_cast<const float4 *>(p.betaf) + 2u * o;
+        const float4 q0 = __ldg(bp), q1 = __ldg(bp + 1);
+        const float b2[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            bl[i] = __fmul_rn(b2[i], kLog2e);
+    }
+    const PhiloxHoist ph = philox_hoist(p.t, g0, p.rk);
+    // 0x4B000000 (= 2^23) in a register the compiler cannot fold, so the PRMT building 2^23 + hi16
+    // takes its selector as an immediate (else two selector constants are re-materialised per vertex)
+    uint32_t c4b;
+    asm volatile("mov.b32 %0, %1;" : "=r"(c4b) : "r"(0x4B000000u));
+    uint32_t pm[DEG];
+#pragma unroll
+    for (int u = 0; u < DEG; ++u)
+        pm[u] = ((lane >> u) & 1u) << 31;
+    const uint32_t amask = 0x11111111u << a;
+    const uint32_t wsh = (uint32_t)__cvta_generic_to_shared(pk_smem) + threadIdx.y * packed_warp_bytes<DEG, S>();
+    const uint32_t ring0 = wsh + lane * 4u;
+    const uint32_t meta0 = wsh + kRing;
+    const uint32_t vb = (uint32_t)p.v_begin + j0;
+    auto meta_issue = [&](uint32_t blk) {
+        const uint32_t j = blk * 32u + lane;
+        if (j < cnt) {
+            const uint32_t me = meta0 + (blk & 1u) * kRingMetaBuf + lane * kRingEntry;
+            cp_async16(me, p.ell_col + 4u * (vb + j));
+            cp_async16(me + 16u, p.ell_w + 4u * (vb + j));
+            cp_async4(me + 32u, p.orig + vb + j);
+        }
+    };
+    const uint32_t meta_end = meta0 + 2u * kRingMetaBuf;
+    auto rows_issue = [&](uint32_t j, uint32_t sl, uint32_t e) {
+        const int4 c = lds128(e);
+        cp_async4(sl, tbb + (uint64_t)(vb + j) * rwb);
+        cp_async4(sl + 128u, tbb + (uint64_t)(uint32_t)c.x * rwb);
+        if (DEG > 1)
+            cp_async4(sl + 256u, tbb + (uint64_t)(uint32_t)c.y * rwb);
+        if (DEG > 2)
+            cp_async4(sl + 384u, tbb + (uint64_t)(uint32_t)c.z * rwb);
+        if (DEG > 3)
+            cp_async4(sl + 512u, tbb + (uint64_t)(uint32_t)c.w * rwb);
+    };
+    meta_issue(0);
+    cp_commit();
+    cp_wait<0>();
+    __syncwarp();
+#pragma unroll
+    for (uint32_t j = 0; j + 1 < S; ++j) {
+        if (j < cnt)
+            rows_issue(j, ring0 + j * kSlot, meta0 + j * kRingEntry);
+        cp_commit();
+    }
+    constexpr uint32_t U = kI8PackedUnroll;
+    static_assert(U % S == 0 && 32 % U == 0, "unroll must be a multiple of the ring depth dividing 32");
+    // (a main loop without the per-vertex bounds tests, with a checked tail loop, measured -1%)
+    uint32_t e_cur = meta0;
+    for (uint32_t jb = 0; jb < cnt; jb += U) {
+#pragma unroll
+        for (uint32_t u = 0; u < U; ++u) {
+            const uint32_t j = jb + u;
+            if (j >= cnt)
+                break;
+            if (u == 0 && (jb & 31u) == 0) {
+                __syncwarp();
+                meta_issue((j >> 5) + 1);
+            }
+            if (j + S - 1 < cnt)
+                rows_issue(j + S - 1, ring0 + ((u + S - 1) % S) * kSlot, meta0 + ((j + S - 1) & 63u) * kRingEntry);
+            cp_commit();
+            cp_wait<S - 1>();
+            if (u == S - 1 && (jb & 31u) == 0)
+                __syncwarp();
+            const uint32_t sl = ring0 + (u % S) * kSlot;
+            const uint32_t own = lds32(sl);
+            uint32_t nb[DEG];
+#pragma unroll
+            for (int q = 0; q < DEG; ++q)
+                nb[q] = lds32(sl + (q + 1) * 128u);
+            const int4 wq = lds128(e_cur + u * kRingEntry + 16u);
+            const uint32_t io = lds32(e_cur + u * kRingEntry + 32u);
+            const uint32_t fl = packed_decide<DEG>(p, own, nb, wq, io, a, pm, bl, ph, g0, o, c4b, amask);
+            if (a == 0u)
+                asm volatile("st.global.cg.u32 [%0], %1;" ::"l"(tbb + (uint64_t)(vb + j) * rwb), "r"(own ^ fl)
+                             : "memory");
+        }
+        e_cur = e_cur + U * kRingEntry == meta_end ? meta0 : e_cur + U * kRingEntry;
+    }
+    cp_wait<0>();
+}
+
+template <int DEG, int S>
+cudaError_t launch_packed_deg(const CsrI8Params &p, uint32_t *P, cudaStream_t st)
+{
+    const uint32_t nv = (uint32_t)(p.v_end - p.v_begin);
+    if (nv == 0)
+        return cudaSuccess;
+    const uint32_t nslice = (uint32_t)p.R / 256u;
+    const size_t smem = (size_t)8 * packed_warp_bytes<DEG, S>();
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaError_t e = cudaFuncSetAttribute(k_csr_packed<DEG, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_csr_packed<DEG, S>, 256, smem);
+        if (e != cudaSuccess)
+            return e;
+        if (per_sm < 1)
+            return cudaErrorInvalidConfiguration;
+    }
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t want = (uint32_t)nsm * (uint32_t)per_sm * 8u;  // one wave of resident warps
+    uint32_t nch = want / nslice;
+    if (nch < 1)
+        nch = 1;
+    if (nch > nv)
+        nch = nv;
+    uint32_t chunk = (nv + nch - 1) / nch;
+    if (chunk < 40u)
+        chunk = 40u;
+    nch = (nv + chunk - 1) / chunk;
+    const uint32_t warps = nch * nslice;
+    k_csr_packed<DEG, S><<<(warps + 7) / 8, dim3(32, 8), smem, st>>>(p, P, nslice, chunk);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_rows(const int8_t *s, uint32_t *P, int64_t n, int64_t R, bool unpack, cudaStream_t st)
+{
+    if (R % 32 != 0)
+        return cudaErrorInvalidValue;
+    const uint64_t nwords = (uint64_t)n * (uint64_t)(R / 32);
+    if (nwords == 0)
+        return cudaSuccess;
+    const uint64_t want = (nwords + 255) / 256;
+    const unsigned grid = (unsigned)(want < 148ull * 16 ? want : 148ull * 16);
+    if (unpack)
+        k_unpack_rows<<<grid, 256, 0, st>>>(P, const_cast<int8_t *>(s), nwords);
+    else
+        k_pack_rows<<<grid, 256, 0, st>>>(s, P, nwords);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_csr_packed_phase(const CsrI8Params &p, uint32_t *P, cudaStream_t st)
+{
+    if (!p.wf || !p.ell_col || p.R % 256 != 0 || p.slot0 % 8 != 0)
+        return cudaErrorInvalidValue;
+    switch (p.ell_deg) {
+    case 1: return launch_packed_deg<1, kI8PackedRing>(p, P, st);
+    case 2: return launch_packed_deg<2, kI8PackedRing>(p, P, st);
+    case 3: return launch_packed_deg<3, kI8PackedRing>(p, P, st);
+    default: return launch_packed_deg<4, kI8PackedRing>(p, P, st);
+    }
+}
+
 cudaError_t launch_csr_i8_phase(const CsrI8Params &p, int32_t threads, cudaStream_t st)
 {
     if (p.R % 8 != 0 || p.slot0 % 8 != 0)

@@ -412,7 +412,95 @@ def test_float_int8_degenerate_weights(wset):
     assert np.allclose(eng.energies(), o.energies(), rtol=1e-5, atol=1e-5 * scale)
 
 
-def test_c5_full_size_sampled_replicas():
+@pytest.mark.parametrize("n,d,drop,K,C,sweeps", [
+    (3000, 3, 0, 32, 8, 12),      # R = 256, DEG 3 (C5 shape)
+    (2000, 4, 10, 64, 8, 8),      # R = 512: two slices per vertex, DEG 4 with pads
+    (1500, 2, 0, 32, 8, 10),      # DEG 2 (a random 2-regular graph: cycles)
+    (38, 3, 0, 16, 16, 20),       # fewer vertices per class than warps
+])
+@pytest.mark.parametrize("colouring", ["sl", "jp"])
+def test_float_packed_rows_parity(monkeypatch, n, d, drop, K, C, sweeps, colouring):
+    """Packed-row sweeps (k_csr_packed) forced on: identical spins to the
+    oracle and to the int8 ring kernel (forced off), energies within 1e-5 relative."""
+    u, v = synth.random_regular(n, d, 40 + n)
+    if drop:
+        keep = np.arange(u.size) % drop != 0
+        u, v = u[keep], v[keep]
+    w = synth.gaussian_f32(u.size, 41 + n)
+    rp, col, ww = synth.edges_to_csr(n, u, v, w)
+    inst = dict(kind="csr", n=n, row_ptr=rp, col=col, w=ww.astype(np.float32))
+    betas = synth.beta_ladder(K)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ISING_I8_PACKED", mode)
+        eng = Engine(inst, K, C, betas, seed=KEY, layout="i8", colour=colouring)
+        run_pt(eng, sweeps, 0)
+        out[mode] = ([eng.spins(r) for r in range(eng.R)], eng.energies())
+        eng.close()
+    colour, _ = (oracle.greedy_colour_jp if colouring == "jp" else oracle.greedy_colour_sl)(n, rp, col)
+    o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=oracle.RNG_WORD, colour=colour).run(sweeps, 0)
+    for r in range(o.R):
+        assert np.array_equal(out["1"][0][r], o.s[r]), f"slot {r}"
+        assert np.array_equal(out["0"][0][r], o.s[r]), f"slot {r} (int8 ring)"
+    assert np.allclose(out["1"][1], o.energies(), rtol=1e-5, atol=0)
+    assert np.array_equal(out["1"][1], out["0"][1])  # same spins, same energy kernel
+
+
+def test_float_packed_rows_call_pattern(monkeypatch):
+    """Packed rows over mixed call patterns on one handle: single-sweep calls (pack / unpack
+    around every sweep), a long call, spins written between calls, and an annealing schedule
+    (per-sweep betas) -- identical to the int8 kernels throughout."""
+    n, K, C = 2500, 32, 8
+    inst = _regular_inst(n, 77)
+    betas = synth.beta_ladder(K)
+    sched = np.stack([betas * (0.5 + 0.1 * s) for s in range(6)]).astype(np.float64)
+    res = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ISING_I8_PACKED", mode)
+        eng = Engine(inst, K, C, betas, seed=KEY, layout="i8", colour="jp")
+        for _ in range(3):
+            eng.sweep(1)
+        eng.sweep(9)
+        s0 = eng.spins(5)
+        s0[: n // 2] *= -1
+        eng.set_spins(5, s0)
+        eng.sweep(5)
+        eng.anneal(sched)
+        res[mode] = ([eng.spins(r) for r in range(eng.R)], eng.energies())
+        eng.close()
+    for r in range(K * C):
+        assert np.array_equal(res["1"][0][r], res["0"][0][r]), f"slot {r}"
+    assert np.array_equal(res["1"][1], res["0"][1])
+
+
+@pytest.mark.parametrize("wset", [
+    [-1.0, 0.0, 1.0],
+    [0.0, -0.0, 0.5, -0.5, 1e-3, -1e-3, 1e-38, -1e-38, 1e-41, -1e-41, 3.0, -3.0],
+])
+def test_float_packed_rows_degenerate_weights(monkeypatch, wset):
+    """The packed-row kernel on degenerate couplings (signed zeros, s h = 0 ties through the
+    exact path, tiny and subnormal terms): spins identical to the oracle."""
+    monkeypatch.setenv("ISING_I8_PACKED", "1")
+    n, K, C, sweeps = 2000, 32, 8, 20
+    u, v = synth.random_regular(n, 3, 60)
+    pick = (synth.splitmix64(61, u.size) % np.uint64(len(wset))).astype(np.int64)
+    w = np.asarray(wset, np.float32)[pick]
+    rp, col, ww = synth.edges_to_csr(n, u, v, w)
+    inst = dict(kind="csr", n=n, row_ptr=rp, col=col, w=ww.astype(np.float32))
+    betas = synth.beta_ladder(K)
+    eng = Engine(inst, K, C, betas, seed=KEY, layout="i8", colour="jp")
+    run_pt(eng, sweeps, 0)
+    colour, _ = oracle.greedy_colour_jp(n, rp, col)
+    o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=oracle.RNG_WORD, colour=colour).run(sweeps, 0)
+    for r in range(o.R):
+        assert np.array_equal(eng.spins(r), o.s[r]), f"slot {r}"
+    scale = float(np.abs(w.astype(np.float64)).sum())
+    assert np.allclose(eng.energies(), o.energies(), rtol=1e-5, atol=1e-5 * scale)
+
+
+@pytest.mark.parametrize("packed", ["1", "0"])
+def test_c5_full_size_sampled_replicas(monkeypatch, packed):
+    monkeypatch.setenv("ISING_I8_PACKED", packed)
     cfg = synth.CONFIGS["c5"]
     inst = synth.make_instance(cfg)
     betas = synth.beta_ladder(cfg["K"])

@@ -54,12 +54,16 @@ def plan(w):
     if w == "c4b:clusters":  # the cluster launch the persistent one replaced (ISING_GRID_SCHED=0)
         return (["--workload", "c4b", "--sweeps", str(SWEEPS)] + base, "k_grid_bits", 1,
                 n * cfg["K"] * cfg["C"] * SWEEPS)
+    if w == "c5:packed":  # one whole sweep (the 4 colour-class launches) of the packed-row kernel
+        return (["--workload", "c5", "--sweeps", "4"] + base, "k_csr_packed", 16, n * cfg["K"] * cfg["C"], 4)
     kern = {"c2": "k_grid_bits", "c3": "k_csr_bits", "c4a": "k_grid_sched", "c4b": "k_grid_sched"}[w]
     return (["--workload", w, "--sweeps", str(SWEEPS)] + base, kern, 1, n * cfg["K"] * cfg["C"] * SWEEPS)
 
 
 def run(w):
-    args, kern, skip, attempts = plan(w)
+    pl = plan(w)
+    args, kern, skip, attempts = pl[:4]
+    count = pl[4] if len(pl) > 4 else 1
     tag = w.replace(":", "_")
     cmd = [sys.executable, "bench.py"] + args
     env = dict(os.environ)
@@ -73,17 +77,20 @@ def run(w):
     # (the band split's cooperative launch, c4b:share16, fails under ncu in kernel and in
     # application replay alike: its copy barriers spin on global memory)
     prof = subprocess.run(["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "-k",
-                           f"regex:{kern}", "-s", str(skip), "-c", "1", "--csv"] + cmd, cwd=ROOT,
+                           f"regex:{kern}", "-s", str(skip), "-c", str(count), "--csv"] + cmd, cwd=ROOT,
                           capture_output=True, text=True, timeout=1800, env=env)
     with open(csvp, "w") as f:
         f.write(prof.stdout + prof.stderr)
     vals = {}
     for r in csv.reader(prof.stdout.splitlines()):
         if len(r) > 14 and r[0] != "ID":
-            try:
-                vals[r[12]] = float(r[14].replace(",", ""))
+            try:  # summed over the profiled launches
+                vals[r[12]] = vals.get(r[12], 0.0) + float(r[14].replace(",", ""))
             except ValueError:
                 pass
+    for k in list(vals):  # rates are averaged over the profiled launches, counts summed
+        if "pct" in k or k.endswith(".avg"):
+            vals[k] /= count
     if "smsp__inst_executed.sum" not in vals:
         print(w, "no ncu data; see", csvp)
         return
@@ -105,10 +112,10 @@ def merge():
     files = sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "pipes_*.json")), key=lambda f: "_full" in f)
     for f in files:
         d = json.load(open(f))
-        key = {"c4b:share16": "c4b_bands", "c4b": "c4b_sched", "c4a": "c4a_sched",
+        key = {"c5:packed": "c5_packed", "c4b:share16": "c4b_bands", "c4b": "c4b_sched", "c4a": "c4a_sched",
                "c4b:clusters": "c4b", "c4b:full": "c4b_sched", "c4a:full": "c4a_sched"}.get(d["workload"], d["workload"])
         e = db.setdefault(key, {})
-        e.update({"kernel": d["kernel"], "layout": "bits" if d["kernel"] != "k_i8_cluster" else "i8",
+        e.update({"kernel": d["kernel"], "layout": "bits" if d["kernel"] not in ("k_i8_cluster", "k_csr_packed") else "i8",
                   "warp_inst_per_attempt": d["warp_inst_per_attempt"],
                   "alu_fma_pipe_inst_per_attempt": d["alu_fma_pipe_inst_per_attempt"],
                   "dram_bytes_per_launch": d["dram_bytes_per_launch"],
