@@ -176,6 +176,8 @@ def cpu_oracle_sample(cfg, target_s=12.0):
     betas = synth.beta_ladder(K)
     cores = os.cpu_count() or 1
     threads = max(1, min(cores, cfg["C"], 16))
+    if cfg["C"] == 1 and cfg["K"] > 64:  # one copy: threads take disjoint replica pairs instead
+        threads = max(1, min(cores, 16, cfg["K"] // 2))
     n = inst["n"]
     kex = cfg["k_ex"] if cfg["k_ex"] > 0 else 0
     rng = oracle.RNG_PLANE if cfg["layout"] == "bits" else oracle.RNG_WORD

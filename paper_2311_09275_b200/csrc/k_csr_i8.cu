@@ -1075,8 +1075,7 @@ __global__ void __launch_bounds__(256, kI8PackedMinBlocks) k_csr_packed(const Cs
     const PhiloxHoist ph = philox_hoist(p.t, g0, p.rk);
     // 0x4B000000 (= 2^23) in a register the compiler cannot fold, so the PRMT building 2^23 + hi16
     // takes its selector as an immediate (else two selector constants are re-materialised per vertex)
-    uint32_t c4b;
-    asm volatile("mov.b32 %0, %1;" : "=r"(c4b) : "r"(0x4B000000u));
+    const uint32_t c4b = 0x4B000000u | ((uint32_t)p.R >> 31);  // p.R > 0: the bit is 0
     uint32_t pm[DEG];
 #pragma unroll
     for (int u = 0; u < DEG; ++u)
