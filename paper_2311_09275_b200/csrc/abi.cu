@@ -1023,6 +1023,22 @@ int launch_sweeps_i8(ising_handle *h, int32_t ns, const void *sched)
 
 int launch_sweeps(ising_handle *h, int32_t ns)
 {
+    if (h->kernel == KER_GRID_BITS && h->sched_ok && ns >= 2 && ns % 2 == 0) {
+        // more word groups than resident CTAs: the persistent kernel with tasks (group, half of
+        // the sweeps) keeps every SM busy (waves of whole groups would leave the last wave part-
+        // filled: 512 groups = 3.46 x 148); same RNG counters, same result
+        GridBitsParams p = grid_params(h, 2, ns / 2, false);
+        const cudaError_t le = launch_grid_sched(p, h->sched_ctas, h->threads, h->smem, h->st);
+        if (le == cudaErrorCooperativeLaunchTooLarge) {
+            cudaGetLastError();
+            h->sched_ok = false;
+        } else {
+            CK(le);
+            h->cur ^= 1;
+            h->t += (uint32_t)ns;
+            return ISING_OK;
+        }
+    }
     if (h->kernel == KER_GRID_BITS) {
         CK(launch_grid(h, grid_params(h, 1, ns, false)));
         h->cur ^= 1;
@@ -1489,7 +1505,7 @@ int ising_create_grid(int32_t Lx, int32_t Ly, const int8_t *J_right, const int8_
         }
         if (want) {
             const size_t nbw = ((size_t)n + 31) / 32;
-            CK(h->alloc(&h->d_xs_ctl, 1 + 2 * (size_t)h->C_local));
+            CK(h->alloc(&h->d_xs_ctl, 1 + 2 * (size_t)h->C_local + (size_t)h->G));
             CK(h->alloc(&h->d_xs_E, (size_t)h->G * 32));
             CK(h->alloc(&h->d_xs_B, (size_t)2 * h->G * 2 * nbw));
             CK(h->alloc(&h->d_xs_M, (size_t)h->C_local * h->wpc));

@@ -226,6 +226,10 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_sched(const GridBit
     const int nbw = (n + 31) / 32;
     const uint32_t bytes = 4u * (uint32_t)n;  // n % 4 == 0 (even tori): whole 16-byte units
     uint32_t *ticket = p.xs_ctl, *cnt = p.xs_ctl + 1, *ready = p.xs_ctl + 1 + C_local;
+    // plain sweeps (p.pt == 0): tasks (group, chunk of k_ex sweeps) wait only for the group's
+    // previous chunk, published per group after the copy counters
+    uint32_t *gready = p.xs_ctl + 1 + 2 * C_local;
+    const bool pt = p.pt != 0;
 
     RoundKeys rkr;
 #pragma unroll
@@ -267,7 +271,8 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_sched(const GridBit
             // ---- the copy's exchange of the previous round must be published; then one TMA
             // bulk copy of the stored state straight into S and the pending swaps applied in place
             if (tid == 0) {
-                while (ld_acquire(ready + c_local) < (uint32_t)round)
+                const uint32_t *rw = pt ? ready + c_local : gready + gl;
+                while (ld_acquire(rw) < (uint32_t)round)
                     __nanosleep(256);
                 asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired data -> async proxy
                 bulk_load(sS, scratch, bytes, mb);
@@ -277,6 +282,8 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_sched(const GridBit
             // planes are read only after it
             mbar_wait(mb, phase);
             phase ^= 1u;
+        }
+        if (pt && round > 0) {
             const uint32_t *M = p.xs_M + (size_t)c_local * KW;
             const uint32_t Mw = __ldcg(M + wt);
             const uint32_t Min = Mw & 0x7FFFFFFFu;
@@ -311,14 +318,15 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_sched(const GridBit
             for (int c = 0; c < 2; ++c)
                 grid::colour_phase<SPILL>(X, c, U, rkr, P);
         }
-        atomicAdd(&Ucnt[X.lane], grid::unsat_counts(X, S, JB));
+        if (pt || last)  // plain sweeps: the energies of the call's last sweep only
+            atomicAdd(&Ucnt[X.lane], grid::unsat_counts(X, S, JB));
         if (last) {
             // ---- the launch's output, original order (the PT step applies the last swaps there)
             uint32_t *dst = p.state_out + (size_t)gl * n;
             for (int y = X.warp; y < G.Ly; y += X.nwarps)
                 for (int x = X.lane; x < G.Lx; x += 32)
                     dst[y * G.Lx + x] = S[((x + y) & 1) * G.half + y * G.hx + (x >> 1)];
-        } else {
+        } else if (pt) {
             // ---- this round's boundary bit planes (parity round & 1), then one bulk store of S
             uint32_t *Bo = p.xs_B + ((size_t)(round & 1) * Gl + gl) * 2 * nbw;
             for (int b = X.warp * 32; b < nbw * 32; b += nt) {
@@ -336,12 +344,22 @@ __global__ void __launch_bounds__(kGridMaxThreads, 1) k_grid_sched(const GridBit
         // store below reads S, the next task's bulk load overwrites it)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();  // Ucnt complete; S final
-        if (tid < 32)
+        if (pt && tid < 32)
             p.xs_E[(size_t)gl * 32 + tid] = 2 * (int64_t)Ucnt[tid] - 2 * (int64_t)n;
+        if (!pt && last && tid < 32)
+            p.E_out[(size_t)gl * 32 + tid] = 2 * (int64_t)Ucnt[tid] - 2 * (int64_t)n;
         if (tid == 0 && !last)
             bulk_store_wait(scratch, sS, bytes);
         __threadfence();
         __syncthreads();
+        if (!pt) {  // plain sweeps: publish the group's chunk, take the next ticket
+            if (tid == 0) {
+                st_release(gready + gl, (uint32_t)(round + 1));
+                s_task = (int32_t)next;
+            }
+            __syncthreads();
+            continue;
+        }
         if (tid == 0) {
             const uint32_t done = atomicAdd(cnt + c_local, 1u) + 1u;
             s_last = done == (uint32_t)KW * (uint32_t)(round + 1);
@@ -389,8 +407,10 @@ cudaError_t launch_grid_sched(const GridBitsParams &p, int32_t ctas, int32_t thr
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return e;
-    // control words: ticket, per-copy task counters and published exchange rounds
-    e = cudaMemsetAsync(p.xs_ctl, 0, sizeof(uint32_t) * (1 + 2 * (size_t)(p.n_groups / p.words_per_copy)), st);
+    // control words: ticket, per-copy task counters and published exchange rounds, per-group
+    // published chunks (plain sweeps)
+    e = cudaMemsetAsync(p.xs_ctl, 0,
+                        sizeof(uint32_t) * (1 + 2 * (size_t)(p.n_groups / p.words_per_copy) + (size_t)p.n_groups), st);
     if (e != cudaSuccess)
         return e;
     // per-copy best of this launch: slot -1 = none yet (all bytes 0xFF)

@@ -204,6 +204,64 @@ def test_sched_fused_pt_parity(Lx, Ly, K, C, sweeps, kex, monkeypatch):
     assert np.array_equal(ref.walkers(), eng.walkers())
 
 
+@pytest.mark.parametrize("Lx,Ly,K,C,sweeps,kex", [
+    (16, 16, 64, 2, 40, 10),     # 4 groups, per-round sweep calls of 10 (2 chunks of 5)
+    (6, 4, 32, 3, 21, 4),        # one word per copy; a tail call of 1 sweep (odd: k_grid_bits)
+    (8, 8, 128, 41, 24, 6),      # 164 groups > 148 SMs: chunks of a group on different CTAs
+    (80, 100, 32, 2, 20, 10),    # C2 geometry (leftover-row spill)
+])
+def test_sched_plain_sweeps_parity(Lx, Ly, K, C, sweeps, kex, monkeypatch):
+    """Plain sweep calls on k_grid_sched (tasks = (group, half of the call's sweeps), the per-round
+    path of run_pt(gather=True)): every slot, walker and the best record equal the oracle's and
+    the k_grid_bits sweeps' (ISING_GRID_SCHED=0)."""
+    monkeypatch.setenv("ISING_GRID_BANDS", "1")
+    inst = grid(Lx, Ly, 191 + Lx * Ly)
+    betas = synth.beta_ladder(K)
+    res = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ISING_GRID_SCHED", mode)
+        eng = Engine(inst, K, C, betas, seed=KEY, layout="bits")
+        assert (eng.info.fused_pt == 3) == (mode == "1")
+        rec = run_pt(eng, sweeps, kex, fused=False)
+        res[mode] = (eng.energies(), eng.walkers(), [eng.spins(r) for r in range(K * C)], rec)
+        eng.close()
+    o = oracle.Oracle(inst, K, betas, KEY, 0, C, rng=oracle.RNG_PLANE).run(sweeps, kex)
+    for mode in ("1", "0"):
+        E, W, S, rec = res[mode]
+        assert np.array_equal(E, o.energies()), mode
+        assert np.array_equal(W, o.walker), mode
+        for r in range(K * C):
+            assert np.array_equal(S[r], o.s[r]), f"{mode}: slot {r}"
+        assert (rec["E"], rec["slot"], rec["sweep"]) == (o.best.E, o.best.slot, o.best.sweep)
+
+
+def test_c4b_north_star_mode_sched_sweeps(monkeypatch):
+    """C4b's per-round path (sweep calls of 10 on the persistent kernel, record export, gathered
+    records, exchange) over 100 sweeps equals the fused schedule on every slot of 3 sampled
+    copies and in the best record."""
+    cfg = synth.CONFIGS["c4b"]
+    inst = synth.make_instance(cfg)
+    K, C, kex = cfg["K"], cfg["C"], cfg["k_ex"]
+    betas = synth.beta_ladder(K)
+    eng = Engine(inst, K, C, betas, seed=KEY, layout="bits")
+    assert eng.info.fused_pt == 3
+    send, recv = eng.record_buffers(1)
+    for _ in range(10):
+        eng.sweep(kex)
+        eng.exchange_begin(send)
+        recv.copy_(send)
+        eng.exchange_end(recv)
+    ref = Engine(inst, K, C, betas, seed=KEY, layout="bits")
+    ref.run(10, kex)
+    assert np.array_equal(eng.energies(), ref.energies())
+    assert np.array_equal(eng.walkers(), ref.walkers())
+    for c in (0, 63, 127):
+        for r in range(c * K, (c + 1) * K, 5):
+            assert np.array_equal(eng.spins(r), ref.spins(r)), f"slot {r}"
+    b, rb = eng.best(spins=False), ref.best(spins=False)
+    assert (b["E"], b["slot"], b["sweep"]) == (rb["E"], rb["slot"], rb["sweep"])
+
+
 def test_sched_split_runs_and_state_roundtrip(monkeypatch):
     """Two ising_run calls (the second continuing t and e) and a checkpoint of the persistent
     launch's state, resumed on a fresh handle, equal one oracle run."""
