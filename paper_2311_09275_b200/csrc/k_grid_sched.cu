@@ -413,10 +413,12 @@ cudaError_t launch_grid_sched(const GridBitsParams &p, int32_t ctas, int32_t thr
                         sizeof(uint32_t) * (1 + 2 * (size_t)(p.n_groups / p.words_per_copy) + (size_t)p.n_groups), st);
     if (e != cudaSuccess)
         return e;
-    // per-copy best of this launch: slot -1 = none yet (all bytes 0xFF)
-    e = cudaMemsetAsync(p.copy_best, 0xFF, sizeof(int64_t) * 3 * (size_t)(p.n_groups / p.words_per_copy), st);
-    if (e != cudaSuccess)
-        return e;
+    // per-copy best of this launch: slot -1 = none yet (all bytes 0xFF); plain sweeps keep none
+    if (p.pt) {
+        e = cudaMemsetAsync(p.copy_best, 0xFF, sizeof(int64_t) * 3 * (size_t)(p.n_groups / p.words_per_copy), st);
+        if (e != cudaSuccess)
+            return e;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)ctas);
     cfg.blockDim = dim3((unsigned)threads);

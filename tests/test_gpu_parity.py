@@ -473,6 +473,26 @@ def test_float_packed_rows_call_pattern(monkeypatch):
     assert np.array_equal(res["1"][1], res["0"][1])
 
 
+def test_float_packed_rows_sharded_handles(monkeypatch):
+    """Packed rows on copy shards (slot0 = 256: the Philox counter words of the second shard's
+    lanes start at 32): two 8-copy handles equal one 16-copy handle slot for slot."""
+    monkeypatch.setenv("ISING_I8_PACKED", "1")
+    n, K, C, sweeps = 1800, 32, 16, 9
+    inst = _regular_inst(n, 91)
+    betas = synth.beta_ladder(K)
+    full = Engine(inst, K, C, betas, seed=KEY, layout="i8", colour="jp")
+    full.sweep(sweeps)
+    Ef = full.energies()
+    for lo, hi in ((0, 8), (8, 16)):
+        part = Engine(inst, K, C, betas, seed=KEY, layout="i8", colour="jp", copy_begin=lo, copy_end=hi)
+        part.sweep(sweeps)
+        Ep = part.energies()
+        for r in range(part.R):
+            assert np.array_equal(part.spins(lo * K + r), full.spins(lo * K + r)), f"slot {lo * K + r}"
+        assert np.array_equal(Ep, Ef[lo * K:hi * K])
+        part.close()
+
+
 @pytest.mark.parametrize("wset", [
     [-1.0, 0.0, 1.0],
     [0.0, -0.0, 0.5, -0.5, 1e-3, -1e-3, 1e-38, -1e-38, 1e-41, -1e-41, 3.0, -3.0],
