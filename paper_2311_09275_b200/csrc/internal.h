@@ -38,6 +38,11 @@ constexpr int32_t kI8PipeMinBlocks = 4;
 #endif
 constexpr int32_t kI8Ring = ISING_I8_RING;
 constexpr int32_t kI8RingUnroll = ISING_I8_RING_UNROLL;  // main-loop unroll (multiple of kI8Ring, divides 32; 8 measured -1.3%)
+#ifndef ISING_I8_RING_PATTERN
+#define ISING_I8_RING_PATTERN 1
+#endif
+// ring kernel: fields by per-vertex pattern folds + one shuffle per replica
+constexpr bool kI8RingPattern = ISING_I8_RING_PATTERN != 0;
 constexpr int32_t kI8RingMinBlocks = ISING_I8_RING_MINB;  // resident CTAs per SM the ring kernel's registers are sized for
 // packed-row working copy of the int8 state for float + padded-table sweeps:
 // resident CTAs per SM its registers are sized for, and the fewest sweeps per call that use it

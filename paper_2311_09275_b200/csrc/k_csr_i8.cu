@@ -525,15 +525,29 @@ __device__ __forceinline__ void pipe_issue(I8Rows<DEG> &r, const char *tbb, uint
 }
 
 // Decide the 8 attempts of vertex v (internal id) and write its row.
-template <int DEG>
+// PAT (the ring kernel: a warp is one vertex's 256-replica slice): the field of each replica is
+// looked up by one shuffle from the lane that folded its relative-sign pattern (lane l folds
+// pattern l mod 2^DEG with the sign masks pm; the same terms in the same order, so the same
+// floats as field4), the pattern of byte b being bits 8b .. 8b+DEG-1 of
+// z = OR_u x_u >> (7 - u).
+template <int DEG, bool PAT = false>
 __device__ __forceinline__ void pipe_decide(const CsrI8Params &p, const I8Rows<DEG> &r, const I8Meta &m,
                                             uint32_t v, char *tbb, uint32_t rwb, const float (&bl)[8],
-                                            const PhiloxHoist &ph, uint32_t g0, uint32_t o, uint32_t c4b)
+                                            const PhiloxHoist &ph, uint32_t g0, uint32_t o, uint32_t c4b,
+                                            const uint32_t *pm = nullptr)
 {
     uint2 x[DEG];
 #pragma unroll
     for (int u = 0; u < DEG; ++u)
         x[u] = make_uint2((r.own.x ^ r.nb[u].x) & 0x80808080u, (r.own.y ^ r.nb[u].y) & 0x80808080u);
+    float sv = 0.0f;
+    if (PAT) {
+        const uint32_t wv[4] = {(uint32_t)m.w.x, (uint32_t)m.w.y, (uint32_t)m.w.z, (uint32_t)m.w.w};
+        sv = __uint_as_float(wv[0] ^ pm[0]);
+#pragma unroll
+        for (int u = 1; u < DEG; ++u)
+            sv = __fadd_rn(sv, __uint_as_float(wv[u] ^ pm[u]));
+    }
     const uint4 h = philox_hoisted(m.io, ph, p.rk);
     const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
     uint32_t fm[2];
@@ -541,7 +555,15 @@ __device__ __forceinline__ void pipe_decide(const CsrI8Params &p, const I8Rows<D
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
         float sh[4];
-        if (half)
+        if (PAT) {
+            uint32_t z = (half ? x[0].y : x[0].x) >> 7;
+#pragma unroll
+            for (int u = 1; u < DEG; ++u)
+                z |= (half ? x[u].y : x[u].x) >> (7 - u);
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                sh[b] = __shfl_sync(0xFFFFFFFFu, sv, (int)(z >> (8 * b)));
+        } else if (half)
             field4<DEG, 1>(x, m.w, sh);
         else
             field4<DEG, 0>(x, m.w, sh);
@@ -779,6 +801,10 @@ __global__ void __launch_bounds__(256, kI8RingMinBlocks) k_csr_i8_ring(const Csr
     }
     const PhiloxHoist ph = philox_hoist(p.t, g0, p.rk);
     const uint32_t c4b = 0x4B000000u | (rwb >> 31);
+    uint32_t pm[DEG];  // sign masks of this lane's relative-sign pattern (lane mod 2^DEG)
+#pragma unroll
+    for (int u = 0; u < DEG; ++u)
+        pm[u] = ((lane >> u) & 1u) << 31;
     // shared addresses: this lane's bytes of ring slot 0, and the warp's table double buffer
     const uint32_t wsh = (uint32_t)__cvta_generic_to_shared(ring_smem) + threadIdx.y * ring_warp_bytes<DEG, S>();
     const uint32_t ring0 = wsh + lane * 8u;
@@ -847,7 +873,7 @@ __global__ void __launch_bounds__(256, kI8RingMinBlocks) k_csr_i8_ring(const Csr
             I8Meta m;
             m.w = lds128(e_cur + u * kRingEntry + 16u);
             m.io = lds32(e_cur + u * kRingEntry + 32u);
-            pipe_decide<DEG>(p, r, m, vb + j, tbb, rwb, bl, ph, g0, o, c4b);
+            pipe_decide<DEG, kI8RingPattern>(p, r, m, vb + j, tbb, rwb, bl, ph, g0, o, c4b, pm);
         }
         e_cur = e_cur + U * kRingEntry == meta_end ? meta0 : e_cur + U * kRingEntry;
     }
