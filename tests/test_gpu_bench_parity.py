@@ -7,8 +7,9 @@
   bit: spins of every slot of the copy, energies, walker ids and the per-copy best record.
 * C2 (configs[1]) and C3 (configs[2]): 2 whole copies x 2,000 sweeps of the full 64-copy fused
   launch.
-* C5 (configs[4]): 8 replicas of the full 4e6-vertex instance x 50 sweeps of the ring kernel:
-  identical spins, energies within 1e-5 relative.
+* C5 (configs[4]): 8 replicas of the full 4e6-vertex instance x 50 sweeps, and 16 replicas x 200
+  sweeps in one call (the bench's packed-row kernel): identical spins, energies within 1e-5
+  relative.
 * k_grid_sched on small tori (forced with ISING_GRID_SCHED=1): every slot against the oracle and
   against the cluster launch, incl. swaps that cross words and tail sweeps after the rounds.
 PAPER.md P:53 (PT exchanges replicas across temperatures), P:59 (sweeps as the unit of work).
@@ -153,6 +154,36 @@ def test_c5_full_size_eight_replicas_50_sweeps():
     col, _ = (oracle.greedy_colour_jp if cfg["colouring"] == "jp" else oracle.greedy_colour_sl)(
         inst["n"], inst["row_ptr"], inst["col"])
     slots = (0, 37, 64, 101, 128, 170, 211, 255)
+    res = {}
+
+    def work(lo):
+        o = oracle.Oracle(inst, K, betas, KEY, 0, 1, rng=oracle.RNG_WORD, colour=col, slots=(lo, lo + 1))
+        o.sweeps(sweeps)
+        res[lo] = (o.s[0].copy(), o.energies()[0])
+
+    ts = [threading.Thread(target=work, args=(lo,)) for lo in slots]
+    [t.start() for t in ts]
+    [t.join() for t in ts]
+    for lo in slots:
+        s, e = res[lo]
+        assert np.array_equal(eng.spins(lo), s), f"slot {lo}"
+        assert abs(E[lo] - e) <= 1e-5 * abs(e)
+
+
+def test_c5_packed_rows_16_replicas_200_sweeps():
+    """C5 at full size on the bench's kernel (the packed-row working copy: one ising_sweep call of
+    200 sweeps) against the oracle for 16 replicas spread over the 256 (every lane group of a
+    warp, both halves of a Philox call): identical spins, energies within 1e-5 relative."""
+    cfg = synth.CONFIGS["c5"]
+    inst = synth.make_instance(cfg)
+    K = cfg["K"]
+    betas = synth.beta_ladder(K)
+    eng = Engine(inst, K, cfg["C"], betas, seed=KEY, layout="i8", colour=cfg["colouring"])
+    sweeps = 200
+    eng.sweep(sweeps)
+    E = eng.energies()
+    col, _ = oracle.greedy_colour_jp(inst["n"], inst["row_ptr"], inst["col"])
+    slots = (1, 14, 30, 47, 62, 77, 91, 108, 126, 143, 157, 172, 190, 205, 222, 254)
     res = {}
 
     def work(lo):
