@@ -409,6 +409,13 @@ def measure(args, workload, world, rank, local, steps, warmup, e2e_steps, copies
         ev[1].record(stream)
         kev.append(ev)
 
+    def packed_extra(ns):
+        """k_pack_rows + k_unpack_rows around a packed-row sweep call."""
+        if inst.get("w") is None or inst["w"].dtype != np.float32 or R % 256 or cfg["layout"] != "i8":
+            return 0
+        mode = os.environ.get("ISING_I8_PACKED")
+        return 2 if mode == "1" or (mode != "0" and ns >= 4) else 0
+
     def schedule(e, kev=None):
         """One pass of the whole hot path over the workload; returns our kernel launches."""
         launches = 0
@@ -419,11 +426,11 @@ def measure(args, workload, world, rank, local, steps, warmup, e2e_steps, copies
             for _ in range(rounds):
                 timed(kev, e.sweep, kex)
                 e.exchange()
-                launches += (1 if cfg["layout"] == "bits" else kex * e.info.n_colours + 2) + 2
+                launches += (1 if cfg["layout"] == "bits" else kex * e.info.n_colours + 2 + packed_extra(kex)) + 2
         if rem:
             timed(kev, e.sweep, rem)
             e.check_best()
-            launches += (1 if cfg["layout"] == "bits" else rem * e.info.n_colours + 2) + 1
+            launches += (1 if cfg["layout"] == "bits" else rem * e.info.n_colours + 2 + packed_extra(rem)) + 1
         return launches
 
     def step(kev=None):
