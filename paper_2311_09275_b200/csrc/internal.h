@@ -53,6 +53,12 @@ constexpr int32_t kI8RingMinBlocks = ISING_I8_RING_MINB;  // resident CTAs per S
 // (4 resident CTAs per SM at 64 registers: -0.3%)
 constexpr int32_t kI8PackedMinBlocks = ISING_I8_PACKED_MINB;
 constexpr int32_t kI8PackedMinSweeps = 4;
+// timing probe of the packed kernel's arithmetic alone (rows from registers, no row loads or
+// stores; results wrong): abtest builds with -DISING_I8_PACKED_NOMEM=1
+#ifndef ISING_I8_PACKED_NOMEM
+#define ISING_I8_PACKED_NOMEM 0
+#endif
+constexpr bool kI8PackedNoMem = ISING_I8_PACKED_NOMEM != 0;
 #ifndef ISING_I8_PACKED_RING
 #define ISING_I8_PACKED_RING 4
 #endif

@@ -1147,6 +1147,7 @@ __global__ void __launch_bounds__(256, kI8PackedMinBlocks) k_csr_packed(const Cs
     // (measured and dropped: a main loop without the per-vertex bounds tests, with a checked tail
     // loop, -1%; the next vertex's Philox call issued before this vertex's decision, -4.6%)
     uint32_t e_cur = meta0;
+    uint32_t sink = lane;  // kI8PackedNoMem probe: keeps the decisions live
     for (uint32_t jb = 0; jb < cnt; jb += U) {
 #pragma unroll
         for (uint32_t u = 0; u < U; ++u) {
@@ -1157,28 +1158,39 @@ __global__ void __launch_bounds__(256, kI8PackedMinBlocks) k_csr_packed(const Cs
                 __syncwarp();
                 meta_issue((j >> 5) + 1);
             }
-            if (j + S - 1 < cnt)
+            if (!kI8PackedNoMem && j + S - 1 < cnt)
                 rows_issue(j + S - 1, ring0 + ((u + S - 1) % S) * kSlot, meta0 + ((j + S - 1) & 63u) * kRingEntry);
             cp_commit();
             cp_wait<S - 1>();
             if (u == S - 1 && (jb & 31u) == 0)
                 __syncwarp();
             const uint32_t sl = ring0 + (u % S) * kSlot;
-            const uint32_t own = lds32(sl);
-            uint32_t nb[DEG];
+            uint32_t own, nb[DEG];
+            if (kI8PackedNoMem) {  // timing probe only (wrong results): rows from registers
+                own = (j * 0x9E3779B9u) ^ (lane * 0x01000193u);  // independent of earlier vertices
 #pragma unroll
-            for (int q = 0; q < DEG; ++q)
-                nb[q] = lds32(sl + (q + 1) * 128u);
+                for (int q = 0; q < DEG; ++q)
+                    nb[q] = own * (0x85EBCA6Bu + 2u * q);
+            } else {
+                own = lds32(sl);
+#pragma unroll
+                for (int q = 0; q < DEG; ++q)
+                    nb[q] = lds32(sl + (q + 1) * 128u);
+            }
             const int4 wq = lds128(e_cur + u * kRingEntry + 16u);
             const uint32_t io = lds32(e_cur + u * kRingEntry + 32u);
             const uint32_t fl = packed_decide<DEG>(p, own, nb, wq, io, a, pm, bl, ph, g0, o, c4b, amask);
-            if (a == 0u)
+            if (kI8PackedNoMem)
+                sink += fl;
+            else if (a == 0u)
                 asm volatile("st.global.cg.u32 [%0], %1;" ::"l"(tbb + (uint64_t)(vb + j) * rwb), "r"(own ^ fl)
                              : "memory");
         }
         e_cur = e_cur + U * kRingEntry == meta_end ? meta0 : e_cur + U * kRingEntry;
     }
     cp_wait<0>();
+    if (kI8PackedNoMem && sink == 0x7FFFFFFFu)
+        P[0] = sink;
 }
 
 template <int DEG, int S>
