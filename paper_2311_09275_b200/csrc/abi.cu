@@ -126,6 +126,8 @@ struct ising_handle {
     double *d_Ef = nullptr;
     int64_t *d_walker = nullptr;
     uint32_t *d_swapmask = nullptr;
+    int64_t *d_xpart = nullptr;  // k_exchange partial bests
+    uint32_t *d_xctr = nullptr;  // k_exchange CTA ticket
     uint8_t *d_jbyte = nullptr;
     uint8_t *d_jrd = nullptr;  // grid: original order, bit 0 J_right=-1, bit 1 J_down=-1 (ICM energies)
     uint32_t f = 0;            // Houdayer/ICM moves done
@@ -301,6 +303,9 @@ int build_common_device(ising_handle *h, int64_t sum_abs_w)
         CK(h->alloc(&h->d_Ef, h->R));
     CK(h->alloc(&h->d_walker, h->R));
     CK(h->alloc(&h->d_swapmask, (size_t)h->C_local * h->wpc));
+    CK(h->alloc(&h->d_xpart, 2 * (size_t)kExMaxBlocks));
+    CK(h->alloc(&h->d_xctr, 1));
+    CK(cudaMemsetAsync(h->d_xctr, 0, sizeof(uint32_t), h->st));
     CK(h->alloc(&h->d_best, 1));
     CK(h->alloc(&h->d_cbest, (size_t)h->C_local * 3));
     {
@@ -1055,6 +1060,8 @@ int launch_sweeps(ising_handle *h, int32_t ns)
 ExchangeParams exchange_params(ising_handle *h)
 {
     ExchangeParams p{};
+    p.xpart = h->d_xpart;
+    p.xctr = h->d_xctr;
     p.E = h->d_E;
     p.walker = h->d_walker;
     p.cbest = h->d_cbest;

@@ -205,7 +205,12 @@ constexpr int64_t kI8SmallMaxBytes = 96 * 1024;
 // fused small int8 runs: spread each copy over a cluster of K/8 CTAs (K <= 64)
 constexpr bool kI8Cluster = true;
 
+// k_exchange: CTA size and the most CTAs (size of the handle's partial-best scratch)
+constexpr int32_t kExThreads = 256, kExMaxBlocks = 64;
+
 struct ExchangeParams {
+    int64_t *xpart;            // [2 kExMaxBlocks] per-CTA best (E, slot) of the candidates
+    uint32_t *xctr;            // CTA ticket (zero between launches)
     int64_t *E;                // [R_local] (int64 or double bits)
     int64_t *walker;           // [R_local]
     int64_t *cbest;            // [C_local][3] persistent per-copy best (E, slot, sweep)

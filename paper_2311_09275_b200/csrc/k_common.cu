@@ -81,47 +81,78 @@ __device__ __forceinline__ int8_t spin_of(const ExchangeParams &p, int64_t rl, i
 
 }  // namespace
 
-// Single CTA.  (1) best-so-far: argmin over the candidate records (strict <,
-// ties -> lowest global slot); the handle owning the
-// winning slot snapshots its configuration.  (2) exchange e: per local copy,
-// pairs (k, k+1) with k = e%2 + 2p; d = E_b - E_a; accept iff d >= 0 or
-// U64x(k, e, c) < Tx[k][d] = floor(exp((beta_{k+1}-beta_k) d) 2^64)
-// (min(1, exp(dbeta dH))).  Accepted pairs swap
-// energies and walker ids here and set bit k of the copy's swap mask; the
-// configurations are swapped by k_swap_* right after.
-__global__ void __launch_bounds__(1024) k_exchange(const ExchangeParams p)
+// (1) best-so-far: argmin over the candidate records (strict <, ties -> lowest global slot;
+// SPEC.md S:261-264); the handle owning the winning slot snapshots its configuration.
+// (2) exchange e: per local copy, pairs (k, k+1) with k = e%2 + 2p; d = E_b - E_a; accept iff
+// d >= 0 or U64x(k, e, c) < Tx[k][d] = floor(exp((beta_{k+1}-beta_k) d) 2^64) (min(1,
+// exp(dbeta dH))).  Accepted pairs swap energies and walker ids here
+// and set bit k of the copy's swap mask; the configurations are swapped by k_swap_* right after.
+//
+// One CTA per group of copies (the work is a few dependent global loads per item, so it is
+// latency-bound: spreading it over SMs, not threads, is what shortens it).  Each CTA takes the
+// per-copy best of its copies, the best over its candidates (its copies' slots, read before its
+// own swaps; or its slice of the gathered records) into xpart, then its copies' exchanges; the
+// CTA that finishes last (atomic ticket) merges the partial bests -- (E, slot) is a total order,
+// so the merge equals one sequential scan -- updates the record and takes the snapshot.
+__global__ void __launch_bounds__(kExThreads) k_exchange(const ExchangeParams p)
 {
-    __shared__ int64_t wE[32], wS[32];
-    __shared__ int s_update;
+    __shared__ int64_t wE[kExThreads / 32], wS[kExThreads / 32];
+    __shared__ int s_update, s_last;
     __shared__ int64_t s_slot;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = (int)(blockDim.x >> 5);
     const bool is_f = p.is_float != 0;
+    const int32_t cpb = (p.C_local + (int32_t)gridDim.x - 1) / (int32_t)gridDim.x;
+    const int32_t c0 = min(p.C_local, (int32_t)blockIdx.x * cpb), c1 = min(p.C_local, c0 + cpb);
     if (p.do_best) {
-        // per-copy best-so-far (trials = copies; NEXT-2 harness): strict <, ties -> lowest slot
-        for (int c = tid; c < p.C_local; c += blockDim.x) {
+        // per-copy best-so-far (trials = copies; NEXT-2 harness): strict <, ties -> lowest slot;
+        // one warp per copy (lanes over the temperatures, then a shuffle argmin)
+        for (int c = c0 + warp; c < c1; c += nwarps) {
             int64_t bE = 0, bS = -1;
-            for (int k = 0; k < p.K; ++k) {
+#pragma unroll 4
+            for (int k = lane; k < p.K; k += 32) {
                 const int64_t e = p.E[(int64_t)c * p.K + k];
-                if (bS < 0 || key_less(e, p.slot0 + (int64_t)c * p.K + k, bE, bS, is_f)) {
+                const int64_t sl = p.slot0 + (int64_t)c * p.K + k;
+                if (bS < 0 || key_less(e, sl, bE, bS, is_f)) {
                     bE = e;
-                    bS = p.slot0 + (int64_t)c * p.K + k;
+                    bS = sl;
                 }
             }
-            int64_t *cb = p.cbest + 3 * c;
-            const bool better = cb[1] < 0 || (is_f ? __longlong_as_double(bE) < __longlong_as_double(cb[0])
-                                                  : bE < cb[0]);
-            if (better) {
-                cb[0] = bE;
-                cb[1] = bS;
-                cb[2] = p.t;
+            for (int o = 16; o > 0; o >>= 1) {
+                const int64_t oE = __shfl_down_sync(0xFFFFFFFFu, bE, o);
+                const int64_t oS = __shfl_down_sync(0xFFFFFFFFu, bS, o);
+                if (oS >= 0 && (bS < 0 || key_less(oE, oS, bE, bS, is_f))) {
+                    bE = oE;
+                    bS = oS;
+                }
+            }
+            if (lane == 0) {
+                int64_t *cb = p.cbest + 3 * c;
+                const bool better = cb[1] < 0 || (is_f ? __longlong_as_double(bE) < __longlong_as_double(cb[0])
+                                                      : bE < cb[0]);
+                if (better) {
+                    cb[0] = bE;
+                    cb[1] = bS;
+                    cb[2] = p.t;
+                }
             }
         }
+        // this CTA's candidates: its slice of the gathered records, or its copies' slots
+        int64_t r0, r1;
+        if (p.recs) {
+            const int64_t per = (p.n_recs + gridDim.x - 1) / gridDim.x;
+            r0 = min(p.n_recs, (int64_t)blockIdx.x * per);
+            r1 = min(p.n_recs, r0 + per);
+        } else {
+            r0 = (int64_t)c0 * p.K;
+            r1 = (int64_t)c1 * p.K;
+        }
         int64_t bE = 0, bS = -1;
-        const int64_t ncand = p.recs ? p.n_recs : p.R_local;
-        for (int64_t r = tid; r < ncand; r += blockDim.x) {
+#pragma unroll 4
+        for (int64_t r = r0 + tid; r < r1; r += blockDim.x) {
             const int64_t e = p.recs ? p.recs[r].energy : p.E[r];
             const int64_t s = p.recs ? p.recs[r].slot : p.slot0 + r;
-            if (bS < 0 || key_less(e, s, bE, bS, is_f)) {
+            if (s >= 0 && (bS < 0 || key_less(e, s, bE, bS, is_f))) {
                 bE = e;
                 bS = s;
             }
@@ -138,46 +169,77 @@ __global__ void __launch_bounds__(1024) k_exchange(const ExchangeParams p)
             wE[warp] = bE;
             wS[warp] = bS;
         }
-        __syncthreads();
+        __syncthreads();  // (also: every read of this CTA's energies precedes its swaps below)
         if (tid == 0) {
             int64_t E0 = 0, S0 = -1;
-            for (int w = 0; w < (int)((blockDim.x + 31) / 32); ++w)
+            for (int w = 0; w < nwarps; ++w)
                 if (wS[w] >= 0 && (S0 < 0 || key_less(wE[w], wS[w], E0, S0, is_f))) {
                     E0 = wE[w];
                     S0 = wS[w];
                 }
-            BestDev b = *p.best;
-            bool better = S0 >= 0 && (b.slot < 0 ||
-                                      (is_f ? __longlong_as_double(E0) < __longlong_as_double(b.energy)
-                                            : E0 < b.energy));
-            s_update = better ? 1 : 0;
-            s_slot = S0;
-            if (better) {
-                b.energy = E0;
-                b.slot = S0;
-                b.sweep = p.t;
-                b.owner = (S0 >= p.slot0 && S0 < p.slot0 + p.R_local) ? 1 : 0;
-                *p.best = b;
+            p.xpart[2 * blockIdx.x] = E0;
+            p.xpart[2 * blockIdx.x + 1] = S0;
+            __threadfence();
+            s_last = atomicAdd(p.xctr, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            if (warp == 0) {  // the merge: lanes over the CTAs' partials, then a shuffle argmin
+                __threadfence();
+                int64_t E0 = 0, S0 = -1;
+                for (uint32_t q = lane; q < gridDim.x; q += 32) {
+                    const int64_t e = __ldcg(p.xpart + 2 * q), sl = __ldcg(p.xpart + 2 * q + 1);
+                    if (sl >= 0 && (S0 < 0 || key_less(e, sl, E0, S0, is_f))) {
+                        E0 = e;
+                        S0 = sl;
+                    }
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    const int64_t oE = __shfl_down_sync(0xFFFFFFFFu, E0, o);
+                    const int64_t oS = __shfl_down_sync(0xFFFFFFFFu, S0, o);
+                    if (oS >= 0 && (S0 < 0 || key_less(oE, oS, E0, S0, is_f))) {
+                        E0 = oE;
+                        S0 = oS;
+                    }
+                }
+                if (lane == 0) {
+                    *p.xctr = 0u;  // ready for the next launch (stream order)
+                    BestDev bd = *p.best;
+                    const bool better = S0 >= 0 && (bd.slot < 0 ||
+                                                    (is_f ? __longlong_as_double(E0) < __longlong_as_double(bd.energy)
+                                                          : E0 < bd.energy));
+                    s_update = better ? 1 : 0;
+                    s_slot = S0;
+                    if (better) {
+                        bd.energy = E0;
+                        bd.slot = S0;
+                        bd.sweep = p.t;
+                        bd.owner = (S0 >= p.slot0 && S0 < p.slot0 + p.R_local) ? 1 : 0;
+                        *p.best = bd;
+                    }
+                }
+            }
+            __syncthreads();
+            // the snapshot reads configurations, which k_exchange never changes (k_swap_* does)
+            if (s_update && s_slot >= p.slot0 && s_slot < p.slot0 + p.R_local) {
+                const int64_t rl = s_slot - p.slot0;
+#pragma unroll 4
+                for (int32_t i = tid; i < p.n; i += blockDim.x)
+                    p.best_spins[i] = spin_of(p, rl, i);
             }
         }
-        __syncthreads();
-        if (s_update && s_slot >= p.slot0 && s_slot < p.slot0 + p.R_local) {
-            const int64_t rl = s_slot - p.slot0;
-            for (int32_t i = tid; i < p.n; i += blockDim.x)
-                p.best_spins[i] = spin_of(p, rl, i);
-        }
-        __syncthreads();
     }
     if (p.do_swap && p.K >= 2) {
         const int32_t wpc = p.words_per_copy;
-        for (int idx = tid; idx < p.C_local * wpc; idx += blockDim.x)
+        for (int idx = c0 * wpc + tid; idx < c1 * wpc; idx += blockDim.x)
             p.swapmask[idx] = 0u;
         __syncthreads();
         const int32_t par = (int32_t)(p.e & 1u);
         const int32_t npairs = (p.K - par) / 2;
-        const int64_t total = (int64_t)p.C_local * npairs;
+        const int64_t total = (int64_t)(c1 - c0) * npairs;
+#pragma unroll 2
         for (int64_t idx = tid; idx < total; idx += blockDim.x) {
-            const int32_t c = (int32_t)(idx / npairs);
+            const int32_t c = c0 + (int32_t)(idx / npairs);
             const int32_t k = par + 2 * (int32_t)(idx % npairs);
             const int64_t a = (int64_t)c * p.K + k, b = a + 1;
             const int64_t d = p.E[b] - p.E[a];
@@ -206,7 +268,10 @@ __global__ void __launch_bounds__(1024) k_exchange(const ExchangeParams p)
 
 cudaError_t launch_exchange(const ExchangeParams &p, cudaStream_t st)
 {
-    k_exchange<<<1, 1024, 0, st>>>(p);
+    // about 4 copies per CTA, at most kExMaxBlocks CTAs (the partial-best scratch)
+    int32_t nb = (p.C_local + 3) / 4;
+    nb = nb < 1 ? 1 : (nb > kExMaxBlocks ? kExMaxBlocks : nb);
+    k_exchange<<<nb, kExThreads, 0, st>>>(p);
     return cudaGetLastError();
 }
 
