@@ -16,7 +16,12 @@ enum Kernel : int32_t { KER_GRID_BITS = 0, KER_CSR_BITS = 1, KER_CSR_I8 = 2 };
 // CTA size limits (and launch bounds) of the bit-packed kernels, multiples of 4 warps so the
 // four schedulers get equal work.  Measured on C2/C4b/C3: the torus kernel
 // runs fastest with 16 warps and up to 128 registers per thread, the CSR kernel with 24.
-constexpr int32_t kGridMaxThreads = 512;
+// (A/B on C4b, abtest/c4b_max.sh: a 640-thread cap -- 600-thread passes -- -6%; a 576 cap, i.e.
+// 512 threads at <= 112 registers, +0.1%)
+#ifndef ISING_GRID_MAX_THREADS
+#define ISING_GRID_MAX_THREADS 512
+#endif
+constexpr int32_t kGridMaxThreads = ISING_GRID_MAX_THREADS;
 constexpr int32_t kCsrMaxThreads = 768;
 
 // k_csr_i8_phase CTA size and the resident CTAs per SM its register budget is sized for
